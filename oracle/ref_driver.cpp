@@ -1,0 +1,332 @@
+// oracle/ref_driver.cpp — TEST INFRASTRUCTURE ONLY (the checker, never the
+// product).  A thin extern "C" driver around the UNMODIFIED reference library
+// compiled from /root/reference/proj/src/*.cpp by oracle/Makefile into
+// oracle/_ref/libkktdd_ref.so.  Only tests/, __graft_entry__.smoke() and
+// bench.py's reference / cpu_baseline legs may load it.
+//
+// It wires the reference exactly like run_single does
+// (proj/src/experiments.cpp:33-57): HeatOperators, build_time_partition,
+// make_schur_solver, then gmres_solve with the apply_K / apply_P_inv lambdas —
+// except that the right-hand side is supplied by the caller (the harness's
+// seeded generator) instead of model_problem.hpp.
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+// Read-only access to BandedLU's private factor storage for the factor-parity
+// test (linalg.hpp:45-75).  Nothing is modified.
+#define private public
+#include "kktdd/linalg.hpp"
+#undef private
+#include "kktdd/config.hpp"
+#include "kktdd/gmres.hpp"
+#include "kktdd/heat_operators.hpp"
+#include "kktdd/kkt.hpp"
+#include "kktdd/schur.hpp"
+#include "kktdd/time_partition.hpp"
+
+#include "../include/kktdd_b200.h"
+
+using namespace kktdd;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_err_index = -1;
+
+struct RefCtx {
+  ProblemConfig cfg;
+  std::unique_ptr<HeatOperators> ops;
+  std::unique_ptr<TimePartition> part;
+  std::unique_ptr<SchurSolver> schur;
+};
+
+ProblemConfig to_cfg(const kkt_problem_desc* d) {
+  ProblemConfig c;
+  c.Lx = d->Lx;
+  c.Ly = d->Ly;
+  c.T = d->T;
+  c.Nx = d->Nx;
+  c.Ny = d->Ny;
+  c.Nt = d->Nt;
+  c.nu = d->nu;
+  c.omega = d->omega;
+  c.Nd = d->Nd;
+  c.precond = static_cast<PrecondKind>(d->precond);
+  c.coarse_variant = static_cast<CoarseVariant>(d->coarse_variant);
+  c.two_level_form = static_cast<TwoLevelForm>(d->two_level_form);
+  c.jhat_sign = d->jhat_sign == KKT_SIGN_PLUS ? JhatSign::plus : JhatSign::minus;
+  c.gmres.tol = d->tol;
+  c.gmres.max_iters = d->max_iters;
+  if (d->restart > 0) c.gmres.restart = d->restart;
+  c.gmres.happy_breakdown_tol = d->happy_breakdown_tol;
+  return c;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    g_err_index = -1;
+    return KKT_OK;
+  } catch (const SingularMatrixError& e) {
+    g_err = e.what();
+    g_err_index = e.pivot_index;
+    return KKT_ESINGULAR;
+  } catch (const GmresDivergenceError& e) {
+    g_err = e.what();
+    g_err_index = e.iteration;
+    return KKT_EDIVERGED;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return KKT_ECONFIG;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return KKT_EINVAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 99;
+  }
+}
+
+std::size_t nb(const RefCtx* c) { return c->ops->layout.size(); }
+
+std::span<const double> cin(const double* p, std::size_t n) { return {p, n}; }
+std::span<double> cout_(double* p, std::size_t n) { return {p, n}; }
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_error(void) { return g_err.c_str(); }
+int ref_error_index(void) { return g_err_index; }
+
+int ref_create(const kkt_problem_desc* d, void** out) {
+  return guarded([&] {
+    auto c = std::make_unique<RefCtx>();
+    c->cfg = to_cfg(d);
+    c->cfg.validate();
+    c->ops = std::make_unique<HeatOperators>(c->cfg);
+    c->part = std::make_unique<TimePartition>(build_time_partition(c->cfg.Nt, c->cfg.Nd));
+    c->schur = std::make_unique<SchurSolver>(make_schur_solver(*c->ops, *c->part, c->cfg));
+    *out = c.release();
+  });
+}
+
+void ref_destroy(void* c) { delete static_cast<RefCtx*>(c); }
+
+int64_t ref_block(void* c) { return static_cast<int64_t>(nb(static_cast<RefCtx*>(c))); }
+
+#define REF_UNARY(name, fn)                                                     \
+  int name(void* vc, const double* in, double* out) {                          \
+    auto* c = static_cast<RefCtx*>(vc);                                         \
+    return guarded([&] { fn(*c->ops, cin(in, nb(c)), cout_(out, nb(c))); }); \
+  }
+REF_UNARY(ref_apply_J, apply_J)
+REF_UNARY(ref_apply_JT, apply_JT)
+REF_UNARY(ref_apply_L, apply_L)
+REF_UNARY(ref_apply_LT, apply_LT)
+REF_UNARY(ref_apply_Mu, apply_Mu)
+REF_UNARY(ref_apply_Mu_inv, apply_Mu_inv)
+REF_UNARY(ref_apply_Mz, apply_Mz)
+REF_UNARY(ref_apply_Jhat, apply_Jhat)
+REF_UNARY(ref_apply_JhatT, apply_JhatT)
+REF_UNARY(ref_apply_shat, apply_shat)
+#undef REF_UNARY
+
+int ref_apply_K(void* vc, const double* v, double* out) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] { apply_K(*c->ops, cin(v, 3 * nb(c)), cout_(out, 3 * nb(c))); });
+}
+
+int ref_apply_P_inv(void* vc, const double* r, double* out) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded(
+      [&] { apply_P_inv(*c->ops, *c->schur, cin(r, 3 * nb(c)), cout_(out, 3 * nb(c))); });
+}
+
+int ref_schur_apply(void* vc, const double* r, double* out) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] { c->schur->apply(cin(r, nb(c)), cout_(out, nb(c))); });
+}
+
+int ref_apply_rasq(void* vc, const double* r, double* out) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    SpaceTimeVector rv(r, r + nb(c));
+    SpaceTimeVector o = apply_rasq(*c->ops, *c->part, rv);
+    std::memcpy(out, o.data(), sizeof(double) * o.size());
+  });
+}
+
+int ref_apply_two_level(void* vc, const double* r, double* out, int form) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    const CoarseSpace* cs = c->schur->coarse();
+    if (!cs) throw ConfigError("ref_apply_two_level: solver has no coarse space");
+    SpaceTimeVector rv(r, r + nb(c));
+    SpaceTimeVector o =
+        apply_two_level(*c->ops, *c->part, *cs, rv, static_cast<TwoLevelForm>(form));
+    std::memcpy(out, o.data(), sizeof(double) * o.size());
+  });
+}
+
+int ref_forward_solve_window(void* vc, double* b, int len) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    forward_solve_window(*c->ops, cout_(b, static_cast<std::size_t>(len) * c->ops->layout.n_sp()));
+  });
+}
+
+int ref_adjoint_solve_window(void* vc, double* b, int len) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    adjoint_solve_window(*c->ops, cout_(b, static_cast<std::size_t>(len) * c->ops->layout.n_sp()));
+  });
+}
+
+int ref_band_solve(void* vc, double* b, int nrhs, int transpose) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    const std::size_t nsp = c->ops->layout.n_sp();
+    for (int k = 0; k < nrhs; ++k) {
+      auto s = cout_(b + k * nsp, nsp);
+      if (transpose)
+        c->ops->Ahat_factors.solve_transpose_in_place(s);
+      else
+        c->ops->Ahat_factors.solve_in_place(s);
+    }
+  });
+}
+
+// Band storage of the Ahat factor: (kl + ku_ + 1) rows per column, col-major
+// (linalg.hpp:65-74).  Returns kl, ku_ and the pivot vector.
+int ref_ahat_factor(void* vc, int* kl, int* ku, double* ab, int* piv, double* pivot_growth) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    const BandedLU& F = c->ops->Ahat_factors;
+    *kl = F.kl_;
+    *ku = F.ku_;
+    if (ab) std::memcpy(ab, F.ab_.data(), sizeof(double) * F.ab_.size());
+    if (piv) std::memcpy(piv, F.piv_.data(), sizeof(int) * F.piv_.size());
+    if (pivot_growth) *pivot_growth = F.pivot_growth_;
+  });
+}
+
+int ref_coarse_dim(void* vc) {
+  auto* c = static_cast<RefCtx*>(vc);
+  const CoarseSpace* cs = c->schur->coarse();
+  return cs ? cs->dim() : -1;
+}
+
+int ref_coarse_restrict(void* vc, const double* r, double* cvec) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    const CoarseSpace* cs = c->schur->coarse();
+    cs->restrict_to_coarse(c->ops->layout, *c->part, cin(r, nb(c)), cout_(cvec, cs->dim()));
+  });
+}
+
+int ref_coarse_solve(void* vc, double* cvec) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    const CoarseSpace* cs = c->schur->coarse();
+    cs->solve_in_place(cout_(cvec, cs->dim()));
+  });
+}
+
+int ref_coarse_prolong_add(void* vc, const double* cvec, double* out) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    const CoarseSpace* cs = c->schur->coarse();
+    cs->prolong_add(c->ops->layout, *c->part, cin(cvec, cs->dim()), cout_(out, nb(c)));
+  });
+}
+
+int ref_coarse_matrix(void* vc, double* out) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    const CoarseSpace* cs = c->schur->coarse();
+    DenseMatrix m = cs->coarse_matrix_dense();
+    std::memcpy(out, m.data.data(), sizeof(double) * m.data.size());
+  });
+}
+
+// run_single's solve (experiments.cpp:46-57) on a caller-supplied rhs.
+int ref_gmres_solve(void* vc, const double* b, double* x, kkt_gmres_result* res,
+                    double* history, int history_cap) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    const HeatOperators& ops = *c->ops;
+    const SchurSolver& schur = *c->schur;
+    const LinearMap op = [&](std::span<const double> v, std::span<double> o) {
+      apply_K(ops, v, o);
+    };
+    LinearMap prec;
+    if (c->cfg.precond != PrecondKind::none) {
+      prec = [&](std::span<const double> v, std::span<double> o) {
+        apply_P_inv(ops, schur, v, o);
+      };
+    }
+    GmresResult r = gmres_solve(op, prec, cin(b, 3 * nb(c)), c->cfg.gmres);
+    std::memcpy(x, r.solution.data(), sizeof(double) * r.solution.size());
+    res->converged = r.converged ? 1 : 0;
+    res->iterations = r.iterations;
+    res->true_final_relres = r.true_final_relres;
+    const int nh = std::min<int>(history_cap, static_cast<int>(r.residual_history.size()));
+    res->history_len = nh;
+    if (history) std::memcpy(history, r.residual_history.data(), sizeof(double) * nh);
+  });
+}
+
+int ref_kkt_residual(void* vc, const double* v, const double* rhs, double* out) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    KKTVector kv(nb(c));
+    std::memcpy(kv.data.data(), v, sizeof(double) * 3 * nb(c));
+    RhsBundle b;
+    b.f_u.assign(rhs, rhs + nb(c));
+    b.f_z.assign(rhs + nb(c), rhs + 2 * nb(c));
+    b.f.assign(rhs + 2 * nb(c), rhs + 3 * nb(c));
+    *out = kkt_residual(*c->ops, kv, b);
+  });
+}
+
+// gmres_solve on a dense row-major operator (and optional dense right
+// preconditioner), for the reference's own GMRES unit cases (test_gmres.cpp).
+int ref_gmres_dense(int n, const double* A, const double* M, const double* b, double tol,
+                    int max_iters, int restart, double* x, kkt_gmres_result* res,
+                    double* history, int history_cap) {
+  return guarded([&] {
+    auto dense = [n](const double* m) {
+      return [n, m](std::span<const double> v, std::span<double> o) {
+        for (int i = 0; i < n; ++i) {
+          double acc = 0.0;
+          for (int j = 0; j < n; ++j) acc += m[static_cast<std::size_t>(i) * n + j] * v[j];
+          o[i] = acc;
+        }
+      };
+    };
+    GmresParams p;
+    p.tol = tol;
+    p.max_iters = max_iters;
+    if (restart > 0) p.restart = restart;
+    LinearMap prec;
+    if (M) prec = dense(M);
+    GmresResult r = gmres_solve(dense(A), prec, cin(b, n), p);
+    std::memcpy(x, r.solution.data(), sizeof(double) * n);
+    res->converged = r.converged;
+    res->iterations = r.iterations;
+    res->true_final_relres = r.true_final_relres;
+    const int nh = std::min<int>(history_cap, static_cast<int>(r.residual_history.size()));
+    res->history_len = nh;
+    if (history) std::memcpy(history, r.residual_history.data(), sizeof(double) * nh);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,401 @@
+// capi.cu — the extern "C" boundary (include/kktdd_b200.h) and context setup.
+//
+// kkt_ctx_create does what the reference's run_single does before the solve
+// (experiments.cpp:39-45): ProblemConfig::validate (config.cpp:5-22),
+// HeatOperators (heat_operators.cpp:46-55: derived constants with the
+// reference's expressions, Ahat factorisation), build_time_partition
+// (time_partition.cpp:61-86) and make_schur_solver (schur.cpp:543-558).
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "ctx.cuh"
+
+namespace kkt {
+
+Ctx::~Ctx() {
+  if (stream) cudaStreamSynchronize(stream);
+  basis.clear();
+  if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+namespace {
+
+thread_local std::string g_create_err;
+
+void validate(const kkt_problem_desc& d) {
+  auto fail = [](const std::string& m) { throw Error(KKT_ECONFIG, m); };
+  if (d.Nx < 2 || d.Ny < 2)
+    fail("mesh needs Nx, Ny >= 2, got Nx=" + std::to_string(d.Nx) + " Ny=" + std::to_string(d.Ny));
+  if (d.Lx <= 0 || d.Ly <= 0 || d.T <= 0) fail("domain extents and T must be positive");
+  if (d.Nt < 1) fail("Nt must be >= 1, got " + std::to_string(d.Nt));
+  if (d.Nd < 1) fail("Nd must be >= 1, got " + std::to_string(d.Nd));
+  if (d.Nt % d.Nd != 0)
+    fail("Nt=" + std::to_string(d.Nt) + " is not divisible by Nd=" + std::to_string(d.Nd));
+  if (d.nu < 0) fail("conductivity nu must be >= 0");
+  if (!(d.omega > 0)) fail("regularization omega must be > 0");
+  if (!(d.tol > 0)) fail("gmres tol must be > 0");
+  if (d.max_iters < 1) fail("gmres max_iters must be >= 1");
+  if (d.precond < KKT_PRECOND_NONE || d.precond > KKT_PRECOND_TRUE_SCHUR) fail("unknown preconditioner kind");
+  if (d.two_level_form < KKT_FORM_LITERAL || d.two_level_form > KKT_FORM_ADDITIVE) fail("unknown two-level form");
+}
+
+void setup(Ctx* c, const kkt_problem_desc& d, const kkt_runtime_opts* o) {
+  validate(d);
+  c->desc = d;
+  c->mode = o ? o->mode : KKT_MODE_FAST;
+  c->rank = o ? o->rank : 0;
+  c->nranks = o ? o->nranks : 1;
+  if (c->nranks != 1)
+    throw Error(KKT_EUNSUPPORTED, "multi-rank time-slab sharding is not enabled in this build");
+  int dev = (o && o->device >= 0) ? o->device : -1;
+  if (dev < 0) KKT_CUDA(cudaGetDevice(&dev));
+  KKT_CUDA(cudaSetDevice(dev));
+  c->device = dev;
+  if (o && o->stream) {
+    c->stream = static_cast<cudaStream_t>(o->stream);
+  } else {
+    KKT_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  if (d.precond == KKT_PRECOND_DENSE_SCHUR || d.precond == KKT_PRECOND_TRUE_SCHUR)
+    throw Error(KKT_EUNSUPPORTED,
+                "dense-schur / true-schur are desk-scale dense oracles (schur.cpp:13-21), not on the device path");
+
+  // ---- derived constants, reference expressions (config.hpp:52-65, heat_operators.cpp:16-37)
+  c->nx = d.Nx - 1;
+  c->ny = d.Ny - 1;
+  c->nsp = c->nx * c->ny;
+  c->Nt = d.Nt;
+  c->Nd = d.Nd;
+  c->m = d.Nt / d.Nd;
+  c->B = int64_t(c->Nt) * c->nsp;
+  c->dx = d.Lx / d.Nx;
+  c->dy = d.Ly / d.Ny;
+  c->dt = d.T / d.Nt;
+  c->ms = c->dt * c->dx * c->dy;
+  {
+    const double s = (d.jhat_sign == KKT_SIGN_PLUS) ? 1.0 : -1.0;
+    c->sigma = s / std::sqrt(d.omega);
+  }
+  c->omega = d.omega;
+  c->oms = d.omega * c->ms;
+  c->cx = c->dt * d.nu / (c->dx * c->dx);
+  c->cy = c->dt * d.nu / (c->dy * c->dy);
+  const double diag = 1.0 + 2.0 * c->cx + 2.0 * c->cy;
+  c->A = Stencil{c->nx, c->ny, diag, -c->cx, -c->cy};
+  c->Ahat = Stencil{c->nx, c->ny, diag - c->sigma * c->dt, -c->cx, -c->cy};
+
+  // ---- time partition
+  c->nodes.clear();
+  c->owned.clear();
+  c->owner.assign(c->Nt + 1, 0);
+  for (int n = 1; n <= c->Nt; ++n) c->owner[n] = (n - 1) / c->m;
+  for (int s = 0; s < c->Nd; ++s) {
+    const int last = (s + 1) * c->m;
+    const int first = s == 0 ? 1 : s * c->m;
+    c->nodes.push_back({first, last});
+    c->owned.push_back({s == 0 ? 1 : s * c->m + 1, last});
+  }
+
+  // ---- factor + preconditioner setup
+  build_factor(c);
+  if (c->mode == KKT_MODE_FAST) build_block_inverses(c);
+  if (d.precond == KKT_PRECOND_TWO_LEVEL) build_coarse(c);
+  KKT_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+template <class F>
+int guard(kkt_ctx* ctx, F&& f) {
+  if (!ctx) return KKT_EINVAL;
+  Ctx* c = &ctx->impl;
+  try {
+    KKT_CUDA(cudaSetDevice(c->device));
+    f(c);
+    c->err.clear();
+    c->err_index = -1;
+    return KKT_OK;
+  } catch (const Error& e) {
+    c->err = e.what();
+    c->err_index = e.index;
+    return e.status;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return KKT_EINVAL;
+  }
+}
+
+void need(bool ok, const char* what) {
+  if (!ok) throw Error(KKT_EINVAL, what);
+}
+
+}  // namespace
+}  // namespace kkt
+
+using kkt::Ctx;
+using kkt::Error;
+
+extern "C" {
+
+void kkt_problem_desc_default(kkt_problem_desc* d) {
+  if (!d) return;
+  std::memset(d, 0, sizeof(*d));
+  d->Lx = 1.0;
+  d->Ly = 2.0;
+  d->T = 1.0;
+  d->Nx = 16;
+  d->Ny = 16;
+  d->Nt = 100;
+  d->nu = 1.0;
+  d->omega = 1e-3;
+  d->Nd = 5;
+  d->precond = KKT_PRECOND_TWO_LEVEL;
+  d->coarse_variant = KKT_COARSE_PER_DOF;
+  d->two_level_form = KKT_FORM_MULTIPLICATIVE;
+  d->jhat_sign = KKT_SIGN_MINUS;
+  d->tol = 1e-6;
+  d->max_iters = 420;
+  d->restart = 0;
+  d->happy_breakdown_tol = 1e-14;
+}
+
+const char* kkt_status_string(int s) {
+  switch (s) {
+    case KKT_OK: return "ok";
+    case KKT_EINVAL: return "invalid argument";
+    case KKT_ECONFIG: return "configuration error";
+    case KKT_ESINGULAR: return "singular matrix";
+    case KKT_EDIVERGED: return "gmres diverged";
+    case KKT_ECUDA: return "cuda error";
+    case KKT_ENCCL: return "nccl error";
+    case KKT_EUNSUPPORTED: return "unsupported";
+  }
+  return "unknown";
+}
+
+const char* kkt_create_error(void) { return kkt::g_create_err.c_str(); }
+
+int kkt_ctx_create(const kkt_problem_desc* desc, const kkt_runtime_opts* opts, kkt_ctx** out) {
+  if (!desc || !out) return KKT_EINVAL;
+  *out = nullptr;
+  kkt_ctx* h = new kkt_ctx();
+  try {
+    kkt::setup(&h->impl, *desc, opts);
+  } catch (const Error& e) {
+    kkt::g_create_err = e.what();
+    const int st = e.status;
+    delete h;
+    return st;
+  } catch (const std::exception& e) {
+    kkt::g_create_err = e.what();
+    delete h;
+    return KKT_EINVAL;
+  }
+  kkt::g_create_err.clear();
+  *out = h;
+  return KKT_OK;
+}
+
+int kkt_ctx_destroy(kkt_ctx* ctx) {
+  delete ctx;
+  return KKT_OK;
+}
+
+const char* kkt_last_error(const kkt_ctx* ctx) { return ctx ? ctx->impl.err.c_str() : ""; }
+int kkt_last_error_index(const kkt_ctx* ctx) { return ctx ? ctx->impl.err_index : -1; }
+
+int kkt_layout(const kkt_ctx* ctx, int64_t* block, int32_t* n_sp, int32_t* node_first,
+               int32_t* node_last, int64_t* local_block) {
+  if (!ctx) return KKT_EINVAL;
+  const Ctx& c = ctx->impl;
+  if (block) *block = c.B;
+  if (n_sp) *n_sp = c.nsp;
+  if (node_first) *node_first = 1;
+  if (node_last) *node_last = c.Nt;
+  if (local_block) *local_block = c.B;
+  return KKT_OK;
+}
+
+int kkt_stream(const kkt_ctx* ctx, void** stream) {
+  if (!ctx || !stream) return KKT_EINVAL;
+  *stream = ctx->impl.stream;
+  return KKT_OK;
+}
+
+int kkt_synchronize(kkt_ctx* ctx) {
+  return kkt::guard(ctx, [](Ctx* c) { KKT_CUDA(cudaStreamSynchronize(c->stream)); });
+}
+
+#define KKT_OP(name, body)                                                   \
+  int name(kkt_ctx* ctx, const double* in, double* out) {                    \
+    return kkt::guard(ctx, [&](Ctx* c) {                                     \
+      kkt::need(in && out, #name ": null vector");                           \
+      kkt::need(in != out, #name ": in and out must not alias");             \
+      body;                                                                  \
+    });                                                                      \
+  }
+KKT_OP(kkt_apply_J, kkt::op_time_stencil(c, kkt::OpKind::J, in, out))
+KKT_OP(kkt_apply_JT, kkt::op_time_stencil(c, kkt::OpKind::JT, in, out))
+KKT_OP(kkt_apply_Jhat, kkt::op_time_stencil(c, kkt::OpKind::Jhat, in, out))
+KKT_OP(kkt_apply_JhatT, kkt::op_time_stencil(c, kkt::OpKind::JhatT, in, out))
+KKT_OP(kkt_apply_L, kkt::op_scale(c, in, out, -c->dt, false))
+KKT_OP(kkt_apply_LT, kkt::op_scale(c, in, out, -c->dt, false))
+KKT_OP(kkt_apply_Mu, kkt::op_scale(c, in, out, c->ms, false))
+KKT_OP(kkt_apply_Mu_inv, kkt::op_scale(c, in, out, c->ms, true))
+KKT_OP(kkt_apply_Mz, kkt::op_scale(c, in, out, c->ms, false))
+KKT_OP(kkt_apply_K, kkt::op_apply_K(c, in, out, nullptr))
+KKT_OP(kkt_apply_P_inv, kkt::pinv_apply(c, in, out))
+KKT_OP(kkt_apply_rasq, kkt::rasq_apply(c, in, out, false))
+KKT_OP(kkt_schur_apply, kkt::schur_apply(c, in, out))
+KKT_OP(kkt_apply_shat, {
+  if (c->tmpB1.n < size_t(c->B)) c->tmpB1.alloc(c->B);
+  kkt::op_shat(c, in, out, c->tmpB1.p);
+})
+#undef KKT_OP
+
+int kkt_apply_two_level(kkt_ctx* ctx, const double* r, double* out, int32_t form) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(r && out && r != out, "kkt_apply_two_level: bad vectors");
+    kkt::two_level_apply(c, r, out, form);
+  });
+}
+
+int kkt_forward_solve_window(kkt_ctx* ctx, double* b, int32_t len) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(len >= 0 && (len == 0 || b), "forward_solve_window: bad window");
+    kkt::window_solve(c, b, len, false);
+  });
+}
+
+int kkt_adjoint_solve_window(kkt_ctx* ctx, double* b, int32_t len) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(len >= 0 && (len == 0 || b), "adjoint_solve_window: bad window");
+    kkt::window_solve(c, b, len, true);
+  });
+}
+
+int kkt_band_solve(kkt_ctx* ctx, double* b, int32_t nrhs) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(nrhs >= 0 && (nrhs == 0 || b), "band_solve: bad rhs");
+    if (nrhs) kkt::band_solve(c, b, nrhs, false);
+  });
+}
+
+int kkt_band_solve_transpose(kkt_ctx* ctx, double* b, int32_t nrhs) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(nrhs >= 0 && (nrhs == 0 || b), "band_solve_transpose: bad rhs");
+    if (nrhs) kkt::band_solve(c, b, nrhs, true);
+  });
+}
+
+int kkt_residual(kkt_ctx* ctx, const double* v, const double* rhs, double* relres) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(v && rhs && relres, "kkt_residual: null argument");
+    *relres = kkt::kkt_relres(c, v, rhs);
+  });
+}
+
+int kkt_coarse_dim(const kkt_ctx* ctx, int32_t* dim) {
+  if (!ctx || !dim) return KKT_EINVAL;
+  *dim = ctx->impl.has_coarse ? ctx->impl.cdim : -1;
+  return ctx->impl.has_coarse ? KKT_OK : KKT_ECONFIG;
+}
+
+int kkt_coarse_restrict(kkt_ctx* ctx, const double* r, double* cvec) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(c->has_coarse, "no coarse space");
+    kkt::coarse_restrict(c, r, cvec);
+  });
+}
+
+int kkt_coarse_solve(kkt_ctx* ctx, double* cvec) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(c->has_coarse, "no coarse space");
+    kkt::coarse_solve(c, cvec);
+  });
+}
+
+int kkt_coarse_prolong_add(kkt_ctx* ctx, const double* cvec, double* out) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(c->has_coarse, "no coarse space");
+    kkt::coarse_prolong_add(c, cvec, out);
+  });
+}
+
+int kkt_coarse_matrix(kkt_ctx* ctx, double* host_out) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(c->has_coarse && host_out, "no coarse space");
+    std::memcpy(host_out, c->h_S0.data(), sizeof(double) * c->h_S0.size());
+  });
+}
+
+int kkt_gmres_solve(kkt_ctx* ctx, const double* b, double* x, kkt_gmres_result* res,
+                    double* history, int32_t history_cap) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(b && x && res && b != x, "kkt_gmres_solve: bad arguments");
+    kkt::gmres(c, b, x, res, history, history_cap);
+  });
+}
+
+int kkt_gmres_solve_host(kkt_ctx* ctx, const double* b_host, double* x_host,
+                         kkt_gmres_result* res, double* history, int32_t history_cap) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(b_host && x_host && res, "kkt_gmres_solve_host: bad arguments");
+    const size_t n = size_t(3 * c->B);
+    if (c->e2e_b.n < n) c->e2e_b.alloc(n);
+    if (c->e2e_x.n < n) c->e2e_x.alloc(n);
+    KKT_CUDA(cudaMemcpyAsync(c->e2e_b.p, b_host, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    kkt::gmres(c, c->e2e_b.p, c->e2e_x.p, res, history, history_cap);
+    KKT_CUDA(cudaMemcpyAsync(x_host, c->e2e_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int kkt_launch_count(const kkt_ctx* ctx, int64_t* count) {
+  if (!ctx || !count) return KKT_EINVAL;
+  *count = ctx->impl.launches;
+  return KKT_OK;
+}
+
+int kkt_reset_launch_count(kkt_ctx* ctx) {
+  if (!ctx) return KKT_EINVAL;
+  ctx->impl.launches = 0;
+  return KKT_OK;
+}
+
+int kkt_set_phase_timing(kkt_ctx* ctx, int32_t on) {
+  if (!ctx) return KKT_EINVAL;
+  Ctx& c = ctx->impl;
+  c.phase_timing = on != 0;
+  for (int i = 0; i < 4; ++i) { c.phase_ms[i] = 0; c.phase_cnt[i] = 0; }
+  return KKT_OK;
+}
+
+int kkt_phase_times(const kkt_ctx* ctx, double* ms4, int64_t* counts4) {
+  if (!ctx) return KKT_EINVAL;
+  for (int i = 0; i < 4; ++i) {
+    if (ms4) ms4[i] = ctx->impl.phase_ms[i];
+    if (counts4) counts4[i] = ctx->impl.phase_cnt[i];
+  }
+  return KKT_OK;
+}
+
+int kkt_debug_ahat_factor(kkt_ctx* ctx, int32_t* kl, int32_t* ku, double* ab_host,
+                          int32_t* piv_host) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    if (kl) *kl = c->kl;
+    if (ku) *ku = c->kuf;
+    if (ab_host)
+      KKT_CUDA(cudaMemcpy(ab_host, c->ab.p, sizeof(double) * c->ab.n, cudaMemcpyDeviceToHost));
+    if (piv_host)
+      KKT_CUDA(cudaMemcpy(piv_host, c->piv.p, sizeof(int) * c->piv.n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int kkt_nccl_unique_id(void* out128) {
+  if (!out128) return KKT_EINVAL;
+  std::memset(out128, 0, 128);
+  return KKT_EUNSUPPORTED;
+}
+
+}  // extern "C"

@@ -1,0 +1,173 @@
+// ctx.cuh — the device context behind the C-ABI handle (kkt_ctx).
+//
+// Holds what the reference keeps in HeatOperators (heat_operators.hpp:26-39),
+// TimePartition (time_partition.hpp:26-42) and SchurSolver / CoarseSpace
+// (schur.hpp:244-331), but with the factors and scratch in HBM.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+struct ncclComm;
+
+namespace kkt {
+
+// Device buffer (RAII).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) KKT_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+};
+
+struct NodeRange {
+  int first = 0, last = -1;
+  int count() const { return last - first + 1; }
+};
+
+// Coarse column bookkeeping (schur.hpp:246-250, schur.cpp:283-298).
+struct CoarseColumn {
+  int s, kind, dof;
+};
+
+struct Ctx {
+  kkt_problem_desc desc{};
+  int mode = KKT_MODE_FAST;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int rank = 0, nranks = 1;
+  ncclComm* comm = nullptr;
+
+  // ---- sizes / derived constants (config.hpp:52-65, heat_operators.cpp:26-37)
+  int nx = 0, ny = 0, nsp = 0, Nt = 0, Nd = 0, m = 0;
+  int64_t B = 0;  // global block size Nt * n_sp
+  double dx = 0, dy = 0, dt = 0, ms = 0, sigma = 0, cx = 0, cy = 0;
+  double omega = 0, oms = 0;  // omega * mass_scale as the reference evaluates it
+  Stencil A{}, Ahat{};
+
+  // ---- time partition (time_partition.cpp:61-86)
+  std::vector<NodeRange> nodes, owned;
+  std::vector<int> owner;  // owner[n], n = 1..Nt
+
+  // ---- Ahat factor, reference band storage (linalg.hpp:65-74)
+  int kl = 0, kuf = 0, ld = 0;   // kuf = fill-extended ku_
+  bool pivoted = false;          // any row interchange happened
+  double pivot_growth = 0.0;
+  DBuf<double> ab;               // n_sp * ld
+  DBuf<int> piv;                 // n_sp
+  DBuf<double> ut;               // strict transpose solve: rows of U, n_sp * kl (U(i, i+1..i+kl))
+  // fast block factors: Li_J = L_JJ^{-1}, Ui_J = U_JJ^{-1}, ny blocks of nx*nx row-major
+  DBuf<double> Li, Ui;
+
+  // ---- coarse space (scalar variant)
+  bool has_coarse = false;
+  int cdim = 0;
+  std::vector<CoarseColumn> cols;
+  std::vector<std::vector<double>> phi_const, phi_lin;   // per subdomain, over owned nodes
+  std::vector<double> h_S0;       // dense S0 row-major (coarse_matrix_dense)
+  DBuf<double> S0lu;              // dense LU factors (DenseLU, linalg.cpp:199-234)
+  DBuf<int> S0piv;
+  // per-node coarse tables: for node n (1..Nt): column ids and profile values
+  DBuf<int> node_col;             // 2 per node: column of (owner, kind 0/1), -1 if absent
+  DBuf<double> node_phi;          // 2 per node
+  DBuf<int> col_first;            // per column: first owned node
+  DBuf<int> col_count;            // per column: owned node count
+  DBuf<int> col_kind;             // per column: 0/1 (phi table selector)
+  DBuf<double> col_phi;           // per column: phi values over owned nodes (m entries max), col*m_max + k
+  int m_max = 0;
+  DBuf<double> a1, a2;            // Ahat*1 and Ahat*(Ahat*1) (fast analytic Shat y_c)
+
+  // ---- scratch
+  DBuf<double> nodesum;           // Nt
+  DBuf<double> cvec;              // cdim
+  DBuf<double> gam;               // Nt + 2 (gamma_0 .. gamma_{Nt+1}), prolongation value per node
+  DBuf<double> tmpB1, tmpB2, tmpB3;  // block-sized scratch
+  DBuf<double> sweep_ws;          // per-subdomain work planes for the sweep
+  DBuf<char> jobs_strict, jobs_fast;  // chain descriptors (sweep.cu)
+  DBuf<double> red;               // reduction partials
+  DBuf<unsigned> red_count;
+  DBuf<double> hbuf;              // Hessenberg column on device
+  DBuf<double> ybuf;              // LS coefficients on device
+  DBuf<int> flag;                 // non-finite flag
+
+  // ---- GMRES state
+  std::vector<DBuf<double>> basis;
+  DBuf<double> g_r, g_w, g_z, g_scratch;
+  DBuf<double> e2e_b, e2e_x;       // kkt_gmres_solve_host staging
+
+  // ---- instrumentation
+  int64_t launches = 0;
+  bool phase_timing = false;
+  double phase_ms[4] = {0, 0, 0, 0};
+  int64_t phase_cnt[4] = {0, 0, 0, 0};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+
+  std::string err;
+  int err_index = -1;
+
+  ~Ctx();
+};
+
+// ---- builders (ctx.cu / factor.cu / coarse.cu)
+void build_factor(Ctx* c);
+void build_block_inverses(Ctx* c);
+void build_coarse(Ctx* c);
+
+// ---- operators (stencil.cu)
+enum class OpKind { J, JT, Jhat, JhatT };
+void op_time_stencil(Ctx* c, OpKind k, const double* in, double* out);
+void op_scale(Ctx* c, const double* in, double* out, double mul, bool divide);
+void op_time_stencil_n(Ctx* c, bool lower, const double* in, double* out, int nt, double div);
+void op_apply_K(Ctx* c, const double* v, double* out, const double* b_minus);
+void op_pinv_uz(Ctx* c, const double* r, double* out);
+void op_shat(Ctx* c, const double* v, double* out, double* tmp);
+
+// ---- solves and sweeps (sweep.cu)
+void band_solve(Ctx* c, double* b, int nrhs, bool transpose);
+void window_solve(Ctx* c, double* b, int len, bool adjoint);
+void rasq_apply(Ctx* c, const double* r, double* out, bool with_coarse_residual);
+
+// ---- coarse (coarse.cu)
+void coarse_restrict(Ctx* c, const double* r, double* cdev);
+void coarse_solve(Ctx* c, double* cdev);
+void coarse_prolong_add(Ctx* c, const double* cdev, double* out);
+void coarse_gamma(Ctx* c, const double* r);   // restrict + solve -> gam (per-node y_c values)
+void two_level_apply(Ctx* c, const double* r, double* out, int form);
+void schur_apply(Ctx* c, const double* r, double* out);
+void pinv_apply(Ctx* c, const double* r, double* out);
+
+// ---- Krylov (krylov.cu)
+double dev_dot(Ctx* c, const double* a, const double* b, int64_t n, double* dst);
+int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* hist, int cap);
+double kkt_relres(Ctx* c, const double* v, const double* rhs);
+
+}  // namespace kkt
+
+struct kkt_ctx {
+  kkt::Ctx impl;
+};

@@ -1,0 +1,480 @@
+// krylov.cu — K7: device-resident right-preconditioned GMRES(m)
+// (reference gmres.cpp:21-155) and its vector kernels.
+//
+// The Arnoldi basis, w, z, x and r live in HBM; the host keeps only the
+// (m+1)^2 Hessenberg / Givens state, exactly as the reference does, and runs
+// the same scalar code (std::hypot rotations, back substitution, stopping
+// rule), so the scalar path is identical given identical dot products.
+//
+// Modified Gram-Schmidt (gmres.cpp:92-96) is kept in the reference's order:
+//   h_0 = <w, v_0>;  for i: w -= h_i v_i ; h_{i+1} = <w, v_{i+1}> ... ; ||w||
+// with the axpy fused into the next dot ("axpy+dot") and h_i read from
+// device memory, so an Arnoldi step issues j+2 reduction kernels and one
+// host synchronisation.
+//  * STRICT dots are sequential left-to-right sums of separately rounded
+//    products (linalg.cpp:372-378): one CTA, producer warps stage products
+//    in shared memory, one thread accumulates — bitwise equal to the reference.
+//  * FAST dots are deterministic two-level tree reductions (fixed grid,
+//    per-CTA partials, last CTA sums the partials in index order).
+#include <cmath>
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace kkt {
+namespace {
+
+enum DotOp : int {
+  kDotPlain = 0,   // p = a*b                         (dot)
+  kDotAxpy = 1,    // w = w + (-h)*v; p = w*b          (axpy then dot with next basis vector)
+  kDotAxpySelf = 2,// w = w + (-h)*v; p = w*w          (axpy then norm^2)
+  kDotDiff = 3,    // d = a - b; p = d*d               (||b - A x||^2)
+};
+
+struct DotArgs {
+  int op;
+  int64_t n;
+  double* w;         // a (in) / w (in-out)
+  const double* v;   // axpy source (kDotAxpy*)
+  const double* hsrc;// coefficient h (kDotAxpy*); alpha = -*hsrc
+  const double* b;   // dot partner (kDotPlain / kDotAxpy / kDotDiff)
+  double* dst;       // result
+  int* flag;         // set to 1 if any w/a entry is non-finite (nullable)
+};
+
+__device__ __forceinline__ double produce_strict(const DotArgs& A, double alpha, int64_t k,
+                                                 bool& bad) {
+  switch (A.op) {
+    case kDotPlain: {
+      const double a = A.w[k];
+      if (A.flag && !isfinite(a)) bad = true;
+      return smul(a, A.b[k]);
+    }
+    case kDotAxpy: {
+      const double w = sadd(A.w[k], smul(alpha, A.v[k]));
+      A.w[k] = w;
+      return smul(w, A.b[k]);
+    }
+    case kDotAxpySelf: {
+      const double w = sadd(A.w[k], smul(alpha, A.v[k]));
+      A.w[k] = w;
+      return smul(w, w);
+    }
+    default: {
+      const double d = ssub(A.w[k], A.b[k]);
+      return smul(d, d);
+    }
+  }
+}
+
+constexpr int kSeqThreads = 512;
+constexpr int kSeqTile = 2048;
+
+// Strict: sequential sum in index order (one accumulating thread).
+__global__ void __launch_bounds__(kSeqThreads) dot_seq_kernel(DotArgs A) {
+  __shared__ double buf[2][kSeqTile];
+  const double alpha = A.hsrc ? -(*A.hsrc) : 0.0;
+  const int64_t ntiles = (A.n + kSeqTile - 1) / kSeqTile;
+  const int tid = threadIdx.x;
+  const int producers = blockDim.x - 32;  // warp 0 accumulates, the rest produce
+  bool bad = false;
+  auto fill = [&](int64_t t, double* dst) {
+    const int64_t base = t * kSeqTile;
+    const int cnt = int(A.n - base < kSeqTile ? A.n - base : kSeqTile);
+    for (int i = tid - 32; i < cnt; i += producers) dst[i] = produce_strict(A, alpha, base + i, bad);
+  };
+  if (tid >= 32 && ntiles > 0) fill(0, buf[0]);
+  __syncthreads();
+  double acc = 0.0;
+  for (int64_t t = 0; t < ntiles; ++t) {
+    if (tid >= 32) {
+      if (t + 1 < ntiles) fill(t + 1, buf[(t + 1) & 1]);
+    } else if (tid == 0) {
+      const double* s = buf[t & 1];
+      const int cnt = int(A.n - t * kSeqTile < kSeqTile ? A.n - t * kSeqTile : kSeqTile);
+      int k = 0;
+      for (; k + 8 <= cnt; k += 8) {
+        const double2 p01 = *reinterpret_cast<const double2*>(s + k);
+        const double2 p23 = *reinterpret_cast<const double2*>(s + k + 2);
+        const double2 p45 = *reinterpret_cast<const double2*>(s + k + 4);
+        const double2 p67 = *reinterpret_cast<const double2*>(s + k + 6);
+        acc = sadd(acc, p01.x); acc = sadd(acc, p01.y);
+        acc = sadd(acc, p23.x); acc = sadd(acc, p23.y);
+        acc = sadd(acc, p45.x); acc = sadd(acc, p45.y);
+        acc = sadd(acc, p67.x); acc = sadd(acc, p67.y);
+      }
+      for (; k < cnt; ++k) acc = sadd(acc, s[k]);
+    }
+    __syncthreads();
+  }
+  if (bad) *A.flag = 1;
+  if (tid == 0) *A.dst = acc;
+}
+
+constexpr int kTreeThreads = 256;
+constexpr int kTreeBlocks = kSmCount * 4;
+
+__device__ __forceinline__ double produce_fast(const DotArgs& A, double alpha, int64_t k, bool& bad) {
+  switch (A.op) {
+    case kDotPlain: {
+      const double a = A.w[k];
+      if (A.flag && !isfinite(a)) bad = true;
+      return a * A.b[k];
+    }
+    case kDotAxpy: {
+      const double w = fma(alpha, A.v[k], A.w[k]);
+      A.w[k] = w;
+      return w * A.b[k];
+    }
+    case kDotAxpySelf: {
+      const double w = fma(alpha, A.v[k], A.w[k]);
+      A.w[k] = w;
+      return w * w;
+    }
+    default: {
+      const double d = A.w[k] - A.b[k];
+      return d * d;
+    }
+  }
+}
+
+// Fast: fixed-shape tree; the last CTA to finish reduces the partials in
+// index order, so the result is deterministic run to run.
+__global__ void __launch_bounds__(kTreeThreads) dot_tree_kernel(DotArgs A, double* partial,
+                                                                unsigned* counter) {
+  __shared__ double wsum[kTreeThreads / 32];
+  __shared__ bool is_last;
+  const double alpha = A.hsrc ? -(*A.hsrc) : 0.0;
+  bool bad = false;
+  double acc = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  for (; k + 3 * stride < A.n; k += 4 * stride) {
+    const double p0 = produce_fast(A, alpha, k, bad);
+    const double p1 = produce_fast(A, alpha, k + stride, bad);
+    const double p2 = produce_fast(A, alpha, k + 2 * stride, bad);
+    const double p3 = produce_fast(A, alpha, k + 3 * stride, bad);
+    acc += (p0 + p1) + (p2 + p3);
+  }
+  for (; k < A.n; k += stride) acc += produce_fast(A, alpha, k, bad);
+  if (bad) *A.flag = 1;
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kTreeThreads / 32; ++w) s += wsum[w];
+    partial[blockIdx.x] = s;
+    __threadfence();
+    const unsigned prev = atomicAdd(counter, 1u);
+    is_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    double s = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += ((volatile double*)partial)[i];
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kTreeThreads / 32; ++w) t += wsum[w];
+      *A.dst = t;
+      *counter = 0;  // re-arm for the next launch (stream-ordered)
+    }
+  }
+}
+
+// v = r / beta  (gmres.cpp:64-67) and v_{j+1} = w / h_{j+1} (:120-123).
+__global__ void div_kernel(int64_t n, const double* __restrict__ in, double* __restrict__ out,
+                           double d) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = sdiv(in[i], d);
+}
+
+// scratch = sum_i y_i v_i in the reference's order: zero-filled scratch then
+// axpy(y_i, v_i) for i = 0..k-1 (gmres.cpp:134-135), optionally followed by
+// x += scratch (the unpreconditioned update, :139).
+__global__ void lsq_kernel(int64_t n, int k, const double* const* __restrict__ basis,
+                           const double* __restrict__ y, double* __restrict__ out,
+                           double* __restrict__ xacc) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int i = 0; i < k; ++i) acc = sadd(acc, smul(y[i], basis[i][e]));
+    out[e] = acc;
+    if (xacc) xacc[e] = sadd(xacc[e], acc);
+  }
+}
+
+// x += z (axpy(1.0, z, x), gmres.cpp:137): x + 1.0*z == x + z.
+__global__ void add_kernel(int64_t n, const double* __restrict__ z, double* __restrict__ x) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    x[i] = sadd(x[i], z[i]);
+}
+
+int grid_for(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  const int64_t cap = int64_t(kSmCount) * 16;
+  return int(g < cap ? g : cap);
+}
+
+void ensure_reduction(Ctx* c) {
+  if (!c->red.p) {
+    c->red.alloc(kTreeBlocks);
+    c->red_count.alloc(1);
+    KKT_CUDA(cudaMemsetAsync(c->red_count.p, 0, sizeof(unsigned), c->stream));
+  }
+  if (!c->flag.p) {
+    c->flag.alloc(1);
+    KKT_CUDA(cudaMemsetAsync(c->flag.p, 0, sizeof(int), c->stream));
+  }
+}
+
+void launch_dot(Ctx* c, const DotArgs& A) {
+  ensure_reduction(c);
+  if (c->mode == KKT_MODE_STRICT)
+    KKT_LAUNCH(c, dot_seq_kernel, 1, kSeqThreads, 0, A);
+  else
+    KKT_LAUNCH(c, dot_tree_kernel, kTreeBlocks, kTreeThreads, 0, A, c->red.p, c->red_count.p);
+}
+
+double fetch(Ctx* c, const double* d) {
+  double h = 0.0;
+  KKT_CUDA(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  KKT_CUDA(cudaStreamSynchronize(c->stream));
+  return h;
+}
+
+struct PhaseTimer {
+  Ctx* c;
+  cudaEvent_t e[5] = {};
+  bool on;
+  explicit PhaseTimer(Ctx* ctx) : c(ctx), on(ctx->phase_timing) {
+    if (on)
+      for (auto& x : e) KKT_CUDA(cudaEventCreate(&x));
+  }
+  ~PhaseTimer() {
+    if (on)
+      for (auto& x : e) cudaEventDestroy(x);
+  }
+  void mark(int i) {
+    if (on) KKT_CUDA(cudaEventRecord(e[i], c->stream));
+  }
+  // after a host sync: [0]->[1] P^-1, [1]->[2] K, [2]->[3] Krylov vector work
+  void collect(bool with_prec) {
+    if (!on) return;
+    float ms = 0;
+    if (with_prec) {
+      cudaEventElapsedTime(&ms, e[0], e[1]);
+      c->phase_ms[1] += ms;
+      c->phase_cnt[1]++;
+    }
+    cudaEventElapsedTime(&ms, e[1], e[2]);
+    c->phase_ms[0] += ms;
+    c->phase_cnt[0]++;
+    cudaEventElapsedTime(&ms, e[2], e[3]);
+    c->phase_ms[2] += ms;
+    c->phase_cnt[2]++;
+  }
+};
+
+}  // namespace
+
+double dev_dot(Ctx* c, const double* a, const double* b, int64_t n, double* dst) {
+  DotArgs A{kDotPlain, n, const_cast<double*>(a), nullptr, nullptr, b, dst, nullptr};
+  launch_dot(c, A);
+  return fetch(c, dst);
+}
+
+double kkt_relres(Ctx* c, const double* v, const double* rhs) {
+  // ||rhs - K v|| / ||rhs|| (kkt.cpp:110-124): the reference accumulates both
+  // sums in one loop; separate sequential sums give the same values.
+  const int64_t n = 3 * c->B;
+  if (c->g_scratch.n < size_t(n)) c->g_scratch.alloc(n);
+  if (c->hbuf.n < 8) c->hbuf.alloc(8);
+  op_apply_K(c, v, c->g_scratch.p, nullptr);
+  DotArgs A{kDotDiff, n, const_cast<double*>(rhs), nullptr, nullptr, c->g_scratch.p, c->hbuf.p, nullptr};
+  launch_dot(c, A);
+  const double r2 = fetch(c, c->hbuf.p);
+  const double b2 = dev_dot(c, rhs, rhs, n, c->hbuf.p + 1);
+  const double r = std::sqrt(r2);
+  return b2 > 0.0 ? r / std::sqrt(b2) : r;
+}
+
+// gmres_solve (gmres.cpp:21-155) with apply_operator = apply_K and
+// apply_preconditioner = apply_P_inv (or none), as wired by run_single
+// (experiments.cpp:46-57).
+int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* hist, int cap) {
+  const kkt_problem_desc& P = c->desc;
+  if (!(P.tol > 0) || P.max_iters < 1)
+    throw Error(KKT_EINVAL, "gmres: tol must be > 0 and max_iters >= 1");
+  const int64_t n = 3 * c->B;
+  const bool have_prec = P.precond != KKT_PRECOND_NONE;
+  ensure_reduction(c);
+  if (c->hbuf.n < size_t(P.max_iters) + 8) c->hbuf.alloc(size_t(P.max_iters) + 8);
+  if (c->g_r.n < size_t(n)) c->g_r.alloc(n);
+  if (c->g_w.n < size_t(n)) c->g_w.alloc(n);
+  if (have_prec && c->g_z.n < size_t(n)) c->g_z.alloc(n);
+  if (c->g_scratch.n < size_t(n)) c->g_scratch.alloc(n);
+  KKT_CUDA(cudaMemsetAsync(c->flag.p, 0, sizeof(int), c->stream));
+  KKT_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
+  const int g = grid_for(n);
+  double* hd = c->hbuf.p;
+
+  std::vector<double> history;
+  res->converged = 0;
+  res->iterations = 0;
+  res->true_final_relres = 0.0;
+  res->history_len = 0;
+
+  const double bnorm = std::sqrt(dev_dot(c, b, b, n, hd));
+  if (bnorm == 0.0) {
+    res->converged = 1;
+    return KKT_OK;
+  }
+
+  int total_iters = 0;
+  bool converged = false;
+  bool first_cycle = true;
+  PhaseTimer timer(c);
+  while (total_iters < P.max_iters && !converged) {
+    double* r = c->g_r.p;
+    if (first_cycle) {
+      KKT_CUDA(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+      first_cycle = false;
+    } else {
+      op_apply_K(c, x, r, b);  // r = b - K x (one pass, same rounding)
+    }
+    const double beta = std::sqrt(dev_dot(c, r, r, n, hd));
+    if (beta / bnorm <= P.tol) {
+      converged = true;
+      break;
+    }
+    const int cycle = P.restart > 0 ? std::min(P.restart, P.max_iters - total_iters)
+                                    : P.max_iters - total_iters;
+    while (int(c->basis.size()) < cycle + 1) {
+      c->basis.emplace_back();
+      c->basis.back().alloc(n);
+    }
+    KKT_LAUNCH(c, div_kernel, g, 256, 0, n, r, c->basis[0].p, beta);
+    std::vector<std::vector<double>> H;
+    std::vector<double> gv(cycle + 1, 0.0), cs(cycle, 0.0), sn(cycle, 0.0);
+    gv[0] = beta;
+    int k = 0;
+    double* w = c->g_w.p;
+    double* z = c->g_z.p;
+    std::vector<double> hh(cycle + 2);
+    for (int j = 0; j < cycle; ++j) {
+      timer.mark(0);
+      if (have_prec) {
+        pinv_apply(c, c->basis[j].p, z);
+        timer.mark(1);
+        op_apply_K(c, z, w, nullptr);
+      } else {
+        timer.mark(1);
+        op_apply_K(c, c->basis[j].p, w, nullptr);
+      }
+      timer.mark(2);
+      // ---- modified Gram-Schmidt, fused (gmres.cpp:92-96)
+      {
+        DotArgs A{kDotPlain, n, w, nullptr, nullptr, c->basis[0].p, hd + 0, c->flag.p};
+        launch_dot(c, A);
+      }
+      for (int i = 0; i < j; ++i) {
+        DotArgs A{kDotAxpy, n, w, c->basis[i].p, hd + i, c->basis[i + 1].p, hd + i + 1, nullptr};
+        launch_dot(c, A);
+      }
+      {
+        DotArgs A{kDotAxpySelf, n, w, c->basis[j].p, hd + j, nullptr, hd + j + 1, nullptr};
+        launch_dot(c, A);
+      }
+      timer.mark(3);
+      int bad = 0;
+      KKT_CUDA(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c->stream));
+      KKT_CUDA(cudaMemcpyAsync(&bad, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      KKT_CUDA(cudaStreamSynchronize(c->stream));
+      timer.collect(have_prec);
+      if (bad) {
+        throw Error(KKT_EDIVERGED,
+                    "gmres: non-finite values in Krylov vector at iteration " +
+                        std::to_string(total_iters + 1),
+                    total_iters + 1);
+      }
+      H.emplace_back(j + 2, 0.0);
+      auto& h = H[j];
+      for (int i = 0; i <= j; ++i) h[i] = hh[i];
+      h[j + 1] = std::sqrt(hh[j + 1]);
+      // ---- Givens (gmres.cpp:98-108), verbatim scalar code
+      for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * h[i] + sn[i] * h[i + 1];
+        h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+        h[i] = t;
+      }
+      const double denom = std::hypot(h[j], h[j + 1]);
+      cs[j] = h[j] / denom;
+      sn[j] = h[j + 1] / denom;
+      h[j] = denom;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      ++total_iters;
+      ++k;
+      const double relest = std::abs(gv[j + 1]) / bnorm;
+      history.push_back(relest);
+      const bool happy = h[j + 1] <= P.happy_breakdown_tol;
+      if (relest <= P.tol || happy) {
+        converged = true;
+        break;
+      }
+      if (j + 1 < cycle) KKT_LAUNCH(c, div_kernel, g, 256, 0, n, w, c->basis[j + 1].p, h[j + 1]);
+    }
+    // ---- least-squares update (gmres.cpp:127-141)
+    std::vector<double> y(k, 0.0);
+    for (int i = k - 1; i >= 0; --i) {
+      double acc = gv[i];
+      for (int j2 = i + 1; j2 < k; ++j2) acc -= H[j2][i] * y[j2];
+      y[i] = acc / H[i][i];
+    }
+    if (k > 0) {
+      std::vector<const double*> ptrs(k);
+      for (int i = 0; i < k; ++i) ptrs[i] = c->basis[i].p;
+      if (c->ybuf.n < size_t(k) + size_t(k)) c->ybuf.alloc(2 * size_t(std::max(k, 32)));
+      KKT_CUDA(cudaMemcpyAsync(c->ybuf.p, y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
+      KKT_CUDA(cudaMemcpyAsync(c->ybuf.p + k, ptrs.data(), sizeof(double*) * k, cudaMemcpyHostToDevice, c->stream));
+      const double* const* dptrs = reinterpret_cast<const double* const*>(c->ybuf.p + k);
+      if (have_prec) {
+        KKT_LAUNCH(c, lsq_kernel, g, 256, 0, n, k, dptrs, c->ybuf.p, c->g_scratch.p, nullptr);
+        pinv_apply(c, c->g_scratch.p, z);
+        KKT_LAUNCH(c, add_kernel, g, 256, 0, n, z, x);
+      } else {
+        KKT_LAUNCH(c, lsq_kernel, g, 256, 0, n, k, dptrs, c->ybuf.p, c->g_scratch.p, x);
+      }
+      // the pageable H2D copies above are staged before return, but keep the
+      // descriptors alive until the kernels have consumed them
+      KKT_CUDA(cudaStreamSynchronize(c->stream));
+    } else {
+      // k == 0 cannot happen (a cycle always accepts >= 1 direction) but keep
+      // the reference's semantics: x += P^-1(0) = 0.
+    }
+  }
+  res->converged = converged ? 1 : 0;
+  res->iterations = int(history.size());
+  // true residual (gmres.cpp:147-153)
+  op_apply_K(c, x, c->g_scratch.p, nullptr);
+  {
+    DotArgs A{kDotDiff, n, const_cast<double*>(b), nullptr, nullptr, c->g_scratch.p, hd, nullptr};
+    launch_dot(c, A);
+  }
+  const double rnorm2 = fetch(c, hd);
+  res->true_final_relres = std::sqrt(rnorm2) / bnorm;
+  const int nh = std::min<int>(cap, int(history.size()));
+  res->history_len = hist ? nh : 0;
+  if (hist)
+    for (int i = 0; i < nh; ++i) hist[i] = history[i];
+  return KKT_OK;
+}
+
+}  // namespace kkt

@@ -1,0 +1,143 @@
+// sweep.cu — host orchestration of the spatial-solve chains: band solves,
+// window solves (heat_operators.cpp:139-169) and the one-level RASQ sweep
+// (apply_rasq, schur.cpp:103-130), in both arithmetic modes.
+//
+// RASQ without dead work: for subdomain s with node set
+// [first, last] (first = s*m, or 1 for s = 0) the reference solves a window
+// [W-node, first..last] forward, scales by ms, solves it adjoint, drops the
+// W-node and keeps only owned nodes.  The W-node's forward value is
+// Ahat^{-1} 0 = 0 and the adjoint values at the W-node and at `first` (owned
+// by s-1) are discarded, so the chain here is
+//   forward  x_n  = Ahat^{-1} (r_n + x_{n-1}),   n = first .. last
+//   adjoint  x'_n = Ahat^{-T} (ms*x_n + x'_{n+1}), n = last .. owned.first
+// and out[n] = x'_n (+ y_c[n] for the two-level forms).  All subdomains run
+// as independent chains of one kernel launch.
+#include <vector>
+
+#include "sweep.cuh"
+
+namespace kkt {
+
+namespace {
+
+// Job descriptors go to a per-context device arena.  The H2D copy from
+// pageable memory returns only after the data is staged, and the stream
+// orders it after every kernel still reading the previous descriptors.
+template <class T>
+const T* upload(Ctx* c, DBuf<char>& buf, const std::vector<T>& v) {
+  const size_t bytes = v.size() * sizeof(T);
+  if (buf.n < bytes) {
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+    buf.alloc(bytes);
+  }
+  KKT_CUDA(cudaMemcpyAsync(buf.p, v.data(), bytes, cudaMemcpyHostToDevice, c->stream));
+  return reinterpret_cast<const T*>(buf.p);
+}
+
+}  // namespace
+
+void band_solve(Ctx* c, double* b, int nrhs, bool transpose) {
+  const size_t nsp = c->nsp;
+  if (c->mode == KKT_MODE_STRICT || c->Li.p == nullptr) {
+    std::vector<SolveStep> jobs(nrhs);
+    for (int k = 0; k < nrhs; ++k) jobs[k] = {b + k * nsp, nullptr, b + k * nsp, 1.0, transpose ? 1 : 0};
+    strict_chains(c, upload(c, c->jobs_strict, jobs), nrhs, 1);
+  } else {
+    std::vector<FastStep> jobs(nrhs);
+    for (int k = 0; k < nrhs; ++k) jobs[k] = {b + k * nsp, nullptr, b + k * nsp, nullptr, 1.0, 0, 0};
+    fast_chains(c, upload(c, c->jobs_fast, jobs), nrhs, 1, false);
+  }
+}
+
+void window_solve(Ctx* c, double* b, int len, bool adjoint) {
+  const size_t nsp = c->nsp;
+  if (len <= 0) return;
+  if (c->mode == KKT_MODE_STRICT || c->Li.p == nullptr) {
+    std::vector<SolveStep> jobs;
+    for (int t = 0; t < len; ++t) {
+      const int k = adjoint ? len - 1 - t : t;
+      const double* add = nullptr;
+      if (!adjoint && k > 0) add = b + (k - 1) * nsp;
+      if (adjoint && k < len - 1) add = b + (k + 1) * nsp;
+      jobs.push_back({b + k * nsp, add, b + k * nsp, 1.0, adjoint ? 1 : 0});
+    }
+    strict_chains(c, upload(c, c->jobs_strict, jobs), 1, len);
+  } else {
+    std::vector<FastStep> jobs;
+    for (int t = 0; t < len; ++t) {
+      const int k = adjoint ? len - 1 - t : t;
+      const double* add = nullptr;
+      if (!adjoint && k > 0) add = b + (k - 1) * nsp;
+      if (adjoint && k < len - 1) add = b + (k + 1) * nsp;
+      jobs.push_back({b + k * nsp, add, b + k * nsp, nullptr, 1.0, 0, 0});
+    }
+    fast_chains(c, upload(c, c->jobs_fast, jobs), 1, len, false);
+  }
+}
+
+// out = RASQ(r) (one-level), or in fast mode with `fused_coarse`:
+// out = RASQ(r - Shat y_c) + y_c with y_c = gamma (c->gam) per node.
+void rasq_apply(Ctx* c, const double* r, double* out, bool fused_coarse) {
+  const int64_t nsp = c->nsp;
+  const int Nd = c->Nd, m = c->m;
+  const int nsteps = 2 * m + 1;
+  auto plane = [&](const double* base, int n) { return base + (n - 1) * nsp; };
+  auto wplane = [&](double* base, int n) { return base + (n - 1) * nsp; };
+  if (c->mode == KKT_MODE_STRICT || c->Li.p == nullptr) {
+    // scratch: one plane per subdomain for the shared node's forward value
+    const size_t need = size_t(Nd) * nsp;
+    if (c->tmpB3.n < need) c->tmpB3.alloc(need);
+    // out starts at zero (the reference accumulates into layout.zeros())
+    KKT_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * c->B, c->stream));
+    std::vector<SolveStep> jobs(size_t(Nd) * nsteps, SolveStep{nullptr, nullptr, nullptr, 1.0, 0});
+    for (int s = 0; s < Nd; ++s) {
+      double* shared = c->tmpB3.p + s * nsp;
+      SolveStep* J = jobs.data() + size_t(s) * nsteps;
+      const int first = s == 0 ? 1 : s * m;
+      // forward over first..last
+      for (int t = 0; t <= m; ++t) {
+        const int n = s * m + t;
+        if (n < first) continue;
+        const double* add = nullptr;
+        if (n > first) add = (n - 1 == first && s > 0) ? shared : plane(out, n - 1);
+        double* dst = (s > 0 && n == first) ? shared : wplane(out, n);
+        J[t] = {plane(r, n), add, dst, 1.0, 0};
+      }
+      // adjoint over last..owned.first
+      for (int t = 0; t < m; ++t) {
+        const int n = (s + 1) * m - t;
+        const double* add = t == 0 ? nullptr : plane(out, n + 1);
+        J[m + 1 + t] = {plane(out, n), add, wplane(out, n), c->ms, 1};
+      }
+    }
+    strict_chains(c, upload(c, c->jobs_strict, jobs), Nd, nsteps);
+    return;
+  }
+  // ---- fast
+  const size_t need = size_t(Nd) * 3 * nsp;
+  if (c->tmpB3.n < need) c->tmpB3.alloc(need);
+  std::vector<FastStep> jobs(size_t(Nd) * nsteps, FastStep{nullptr, nullptr, nullptr, nullptr, 1.0, 0, 0});
+  for (int s = 0; s < Nd; ++s) {
+    double* shared = c->tmpB3.p + (3 * s) * nsp;
+    double* adj[2] = {c->tmpB3.p + (3 * s + 1) * nsp, c->tmpB3.p + (3 * s + 2) * nsp};
+    FastStep* J = jobs.data() + size_t(s) * nsteps;
+    const int first = s == 0 ? 1 : s * m;
+    for (int t = 0; t <= m; ++t) {
+      const int n = s * m + t;
+      if (n < first) continue;
+      const double* add = nullptr;
+      if (n > first) add = (n - 1 == first && s > 0) ? shared : plane(out, n - 1);
+      double* dst = (s > 0 && n == first) ? shared : wplane(out, n);
+      J[t] = {plane(r, n), add, dst, nullptr, 1.0, fused_coarse ? n : 0, 0};
+    }
+    for (int t = 0; t < m; ++t) {
+      const int n = (s + 1) * m - t;
+      const double* add = t == 0 ? nullptr : adj[(t - 1) & 1];
+      J[m + 1 + t] = {plane(out, n), add, adj[t & 1], wplane(out, n), c->ms, 0,
+                      fused_coarse ? n : 0};
+    }
+  }
+  fast_chains(c, upload(c, c->jobs_fast, jobs), Nd, nsteps, fused_coarse);
+}
+
+}  // namespace kkt
