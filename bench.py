@@ -1,0 +1,362 @@
+"""Benchmark: space-time unknowns/s per preconditioned KKT solve (fp64).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 1] [--mode fast|strict]
+
+A "step" is one full right-preconditioned GMRES solve (two-level RASQ,
+scalar coarse space) of BASELINE config 1 (127x127 interior, Nt=512, Nd=16,
+omega=1e-3, GMRES(30), rtol 1e-8) from b resident in HBM to x in HBM, through
+the C-ABI (kkt_gmres_solve).  value = N * 3*Nt*n_sp / (max-over-ranks device
+time per solve).  e2e repeats the solve through kkt_gmres_solve_host with b
+and x in pinned host memory (copies inside the timed region).
+
+N > 1 runs one independent solve per GPU (weak scaling, replicas): the
+time-slab sharded path is not wired into this build yet.
+
+--impl reference times the UNMODIFIED reference (oracle/_ref, compiled from
+/root/reference by oracle/Makefile) on the host CPU: each step is a bounded
+sample — GMRES iterations of the config-1 grid on a shortened time axis (Nt=64,
+Nd=2, m=32 as in config 1) — scaled to a full config-1 solve by the per-iteration
+cost's linearity in Nt and the reference's own iteration count.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2305_04421_b200 import problems as P  # noqa: E402
+
+METRIC = "space-time unknowns/sec per preconditioned KKT solve (fp64)"
+UNIT = "unknowns/s"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def hbm_peak():
+    try:
+        d = json.load(open(PEAKS))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def workload_desc(cfg, p):
+    return (f"config{cfg}: {p.nx_int}x{p.ny_int} interior, Nt={p.Nt}, Nd={p.Nd}, nu={p.nu}, "
+            f"omega={p.omega}, two-level {p.coarse_variant} multiplicative (minus), "
+            f"GMRES({p.restart}) rtol {p.tol}")
+
+
+def sweep_bytes(p):
+    """Algorithmic bytes of one RASQ sweep:
+    (2Nt + Nd - 1) * 5 planes * n_sp * 8  +  (2m+1) * F,  F = 8 n_sp (2 nx + 1)."""
+    m = p.Nt // p.Nd
+    planes = (2 * p.Nt + p.Nd - 1) * 5 * p.n_sp * 8
+    F = 8 * p.n_sp * (2 * p.nx_int + 1)
+    return planes + (2 * m + 1) * F
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def __enter__(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.proc or not self.f:
+            return None
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[2:6]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i in range(4) if r[i].lower().startswith("active")})
+        loaded = [s for s, _, _ in rows if s > 300] or [s for s, _, _ in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _ in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (the reference arm and the cpu_baseline leg)
+# ---------------------------------------------------------------------------
+def reference_sample(cfg, iters_full, sample_iters=2, nt_sample=64):
+    """Time `sample_iters` GMRES iterations of the reference on the config grid
+    with a shortened time axis (same m = Nt/Nd), and scale to a full solve."""
+    from oracle.bindings import Ref
+    p = P.config(cfg)
+    m = p.Nt // p.Nd
+    nd_s = max(1, nt_sample // m)
+    ps = p.replace(Nt=nd_s * m, Nd=nd_s, max_iters=sample_iters, restart=p.restart)
+    b = P.kkt_rhs(cfg, ps)
+    t0 = time.perf_counter()
+    ref = Ref(ps)
+    t_setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    out = ref.gmres_solve(b)
+    t_solve = time.perf_counter() - t0
+    # gmres_solve does `it` (K + P^-1) iterations, one LS P^-1 and one true-residual K
+    per_iter = t_solve / (out["iterations"] + 1)
+    scale = p.Nt / ps.Nt
+    t_full = per_iter * scale * (iters_full + 1)
+    value = 3 * p.Nt * p.n_sp / t_full
+    sample = (f"reference (1 thread) on the config-{cfg} grid {p.nx_int}x{p.ny_int} with Nt={ps.Nt}, "
+              f"Nd={ps.Nd} (m={m} as in config {cfg}), {out['iterations']} GMRES iterations in "
+              f"{t_solve:.2f} s (+{t_setup:.2f} s setup); per-iteration cost scaled x{scale:g} in Nt and "
+              f"to {iters_full} iterations (+1 final P^-1/K) => {t_full:.1f} s per full solve")
+    return value, t_full, sample, t_solve + t_setup
+
+
+def reference_iterations(cfg):
+    path = os.path.join(ROOT, "tests", "golden", f"solve_c{cfg}_two-level_scalar.json")
+    if os.path.exists(path):
+        return int(json.load(open(path))["iterations"]), "reference golden record"
+    return None, None
+
+
+def run_reference_arm(args, ws, rank):
+    if rank != 0:
+        return
+    from oracle import bindings
+    if not bindings.available("ref"):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libkktdd_ref.so not built"}))
+        return
+    p = P.config(args.config)
+    iters, src = reference_iterations(args.config)
+    if iters is None:
+        iters, src = 60, "assumed (no golden record)"
+    vals, times = [], []
+    for i in range(args.warmup + args.steps):
+        v, t_full, sample, wall = reference_sample(args.config, iters)
+        if i >= args.warmup:
+            vals.append(v)
+            times.append(t_full)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SplitMix64 + Box-Muller, paper_2305_04421_b200/problems.py)",
+        "config": {"workload": workload_desc(args.config, p), "iterations": iters,
+                   "iterations_source": src},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# the device arm
+# ---------------------------------------------------------------------------
+def run_ours(args, ws, rank, local):
+    import torch
+    from paper_2305_04421_b200.solver import HeatKKT
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    p = P.config(args.config)
+    b_host = P.kkt_rhs(args.config, p)
+    n = b_host.size
+    unknowns = 3 * p.Nt * p.n_sp
+    k = HeatKKT(p, mode=args.mode, device=local)
+    b = torch.from_numpy(b_host).to(dev)
+    x = torch.empty_like(b)
+
+    for _ in range(args.warmup):
+        out = k.gmres_solve(b, x)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K solves, device time with CUDA events on the launch stream
+    k.set_phase_timing(True)
+    l0 = k.launch_count()
+    iters = []
+    barrier(ws)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            out = k.gmres_solve(b, x)
+            iters.append(out.iterations)
+        ev1.record()
+        torch.cuda.synchronize()
+    barrier(ws)
+    launches = k.launch_count() - l0
+    ms_total = ev0.elapsed_time(ev1)
+    ms_total = max_over_ranks(ms_total, ws)
+    ms_step = ms_total / args.steps
+    phase_ms, phase_cnt = k.phase_times()
+    k.set_phase_timing(False)
+    value = ws * unknowns / (ms_step / 1000.0)
+
+    # ---- e2e through the host-buffer entry point (pinned memory)
+    bh = torch.from_numpy(b_host).pin_memory()
+    xh = torch.empty(n, dtype=torch.float64).pin_memory()
+    k.gmres_solve_host(bh.numpy(), xh.numpy())  # warm
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record()
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        k.gmres_solve_host(bh.numpy(), xh.numpy())
+    e1.record()
+    torch.cuda.synchronize()
+    wall_e2e = (time.perf_counter() - w0) / e2e_steps
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1) / e2e_steps, ws)
+    e2e_value = ws * unknowns / (ms_e2e / 1000.0)
+
+    # ---- roofline of the dominant kernel (the RASQ sweep, K5)
+    peak, peak_src = hbm_peak()
+    sweep_ms = phase_ms[3] / max(1, phase_cnt[3])
+    achieved = sweep_bytes(p) / (sweep_ms / 1000.0) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("sweep_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SplitMix64 + Box-Muller target, paper_2305_04421_b200/problems.py)",
+        "config": {
+            "workload": workload_desc(args.config, p), "mode": args.mode,
+            "iterations": iters[-1], "iterations_all": sorted(set(iters)),
+            "true_final_relres": out.true_final_relres,
+            "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+            "l2": "KKT vectors are 198 MB each (> 126 MB L2); no flush between solves",
+            "phase_ms_per_step": {"K": phase_ms[0] / args.steps, "P_inv": phase_ms[1] / args.steps,
+                                  "krylov_vectors": phase_ms[2] / args.steps,
+                                  "sweep_kernel": phase_ms[3] / args.steps},
+        },
+        "roofline": {
+            "kernel": "fast_chain_kernel (RASQ sweep, K5)", "bound": "hbm",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": sweep_bytes(p), "avg_launch_ms": sweep_ms,
+            "launches": phase_cnt[3],
+            "share_of_step": phase_ms[3] / max(1e-9, ms_total),
+        },
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n, "ms_per_step": ms_e2e, "wall_ms_per_step": 1000 * wall_e2e},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and ws == 1:
+        try:
+            from oracle import bindings
+            if bindings.available("ref"):
+                v, t_full, sample, wall = reference_sample(args.config, iters[-1])
+                line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "reference",
+                                        "sample": sample, "host_nproc": os.cpu_count()}
+            else:
+                line["cpu_baseline"] = None
+        except Exception as e:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"error": str(e)}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--mode", default="fast", choices=["fast", "strict"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args, ws, rank)
+        else:
+            run_ours(args, ws, rank, local)
+    finally:
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -16,7 +16,48 @@ namespace kkt {
 Ctx::~Ctx() {
   if (stream) cudaStreamSynchronize(stream);
   basis.clear();
+  for (auto e : ev_pool) cudaEventDestroy(e);
+  for (auto& iv : ev_pending) { cudaEventDestroy(iv.a); cudaEventDestroy(iv.b); }
+  for (auto e : ev_open) if (e) cudaEventDestroy(e);
   if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+static cudaEvent_t pool_get(Ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  KKT_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void Ctx::tbegin(int slot) {
+  if (!phase_timing) return;
+  if (!ev_open[slot]) ev_open[slot] = pool_get(this);
+  KKT_CUDA(cudaEventRecord(ev_open[slot], stream));
+}
+
+void Ctx::tend(int slot) {
+  if (!phase_timing || !ev_open[slot]) return;
+  cudaEvent_t b = pool_get(this);
+  KKT_CUDA(cudaEventRecord(b, stream));
+  ev_pending.push_back({slot, ev_open[slot], b});
+  ev_open[slot] = nullptr;
+}
+
+void Ctx::tcollect() {
+  for (auto& iv : ev_pending) {
+    float ms = 0.f;
+    KKT_CUDA(cudaEventSynchronize(iv.b));
+    KKT_CUDA(cudaEventElapsedTime(&ms, iv.a, iv.b));
+    phase_ms[iv.slot] += ms;
+    phase_cnt[iv.slot] += 1;
+    ev_pool.push_back(iv.a);
+    ev_pool.push_back(iv.b);
+  }
+  ev_pending.clear();
 }
 
 namespace {
@@ -373,6 +414,7 @@ int kkt_set_phase_timing(kkt_ctx* ctx, int32_t on) {
 
 int kkt_phase_times(const kkt_ctx* ctx, double* ms4, int64_t* counts4) {
   if (!ctx) return KKT_EINVAL;
+  const_cast<kkt_ctx*>(ctx)->impl.tcollect();
   for (int i = 0; i < 4; ++i) {
     if (ms4) ms4[i] = ctx->impl.phase_ms[i];
     if (counts4) counts4[i] = ctx->impl.phase_cnt[i];

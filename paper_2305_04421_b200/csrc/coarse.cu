@@ -460,7 +460,7 @@ static void ensure_tmp(Ctx* c) {
 void two_level_apply(Ctx* c, const double* r, double* out, int form) {
   if (!c->has_coarse) throw Error(KKT_ECONFIG, "two-level apply: no coarse space");
   coarse_gamma(c, r);
-  const bool fast = c->mode == KKT_MODE_FAST && c->Li.p != nullptr;
+  const bool fast = c->mode == KKT_MODE_FAST && c->has_fast();
   if (form == KKT_FORM_MULTIPLICATIVE && fast) {
     rasq_apply(c, r, out, true);
     return;

@@ -83,6 +83,10 @@ struct Ctx {
   DBuf<double> ut;               // strict transpose solve: rows of U, n_sp * kl (U(i, i+1..i+kl))
   // fast block factors: Li_J = L_JJ^{-1}, Ui_J = U_JJ^{-1}, ny blocks of nx*nx row-major
   DBuf<double> Li, Ui;
+  // fast v2 (nx <= 128): packed Li_J (lower rows) + D_J^{-1}, Lpk_stride doubles per block
+  DBuf<double> Lpk;
+  int Lpk_stride = 0;
+  bool has_fast() const { return Li.p != nullptr || Lpk.p != nullptr; }
 
   // ---- coarse space (scalar variant)
   bool has_coarse = false;
@@ -125,7 +129,15 @@ struct Ctx {
   bool phase_timing = false;
   double phase_ms[4] = {0, 0, 0, 0};
   int64_t phase_cnt[4] = {0, 0, 0, 0};
-  cudaEvent_t ev[2] = {nullptr, nullptr};
+  // deferred CUDA-event intervals on the context stream: begin/end record
+  // events, collect() (after a host sync) accumulates them into phase_ms
+  std::vector<cudaEvent_t> ev_pool;
+  struct Interval { int slot; cudaEvent_t a, b; };
+  std::vector<Interval> ev_pending;
+  cudaEvent_t ev_open[4] = {nullptr, nullptr, nullptr, nullptr};
+  void tbegin(int slot);
+  void tend(int slot);
+  void tcollect();
 
   std::string err;
   int err_index = -1;

@@ -13,7 +13,7 @@
 // substitution (sweep.cu).
 #include <cmath>
 
-#include "ctx.cuh"
+#include "sweep.cuh"
 
 namespace kkt {
 namespace {
@@ -182,6 +182,32 @@ __global__ void block_inverse_kernel(int nx, int kl, int kuf, int ld, const doub
   }
 }
 
+// Packed Li_J (row a: entries 0..a at a(a+1)/2) followed by D_J^{-1}
+// (1 / U(Jnx+a, Jnx+a)), one `stride`-double block per block row.
+__global__ void pack_lower_kernel(int nx, int ny, int kuf, int ld, int stride,
+                                  const double* __restrict__ ab, const double* __restrict__ Li,
+                                  double* __restrict__ Lpk) {
+  const int J = blockIdx.x;
+  const int T = nx * (nx + 1) / 2;
+  const double* X = Li + int64_t(J) * nx * nx;
+  double* dst = Lpk + int64_t(J) * stride;
+  for (int e = threadIdx.x; e < stride; e += blockDim.x) {
+    double v = 0.0;
+    if (e < T) {
+      // row a: e in [a(a+1)/2, a(a+1)/2 + a]
+      int a = int((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while ((a + 1) * (a + 2) / 2 <= e) ++a;
+      while (a * (a + 1) / 2 > e) --a;
+      const int b = e - a * (a + 1) / 2;
+      v = X[int64_t(a) * nx + b];
+    } else if (e < T + nx) {
+      const int a = e - T;
+      v = 1.0 / ab[int64_t(J * nx + a) * ld + kuf];
+    }
+    dst[e] = v;
+  }
+}
+
 }  // namespace
 
 void build_factor(Ctx* c) {
@@ -239,6 +265,17 @@ void build_block_inverses(Ctx* c) {
   c->Ui.alloc(size_t(ny) * nx * nx);
   const int threads = ((nx + 31) / 32) * 32;
   KKT_LAUNCH(c, block_inverse_kernel, ny, threads, 0, nx, c->kl, c->kuf, c->ld, c->ab.p, c->Li.p, c->Ui.p);
+  if (tma_supported(c)) {
+    // v2 sweep: packed Li + D^{-1} only (U_JJ = D_J L_JJ^T for the symmetric Ahat)
+    const int T = nx * (nx + 1) / 2;
+    c->Lpk_stride = (T + nx + 1) & ~1;
+    c->Lpk.alloc(size_t(ny) * c->Lpk_stride);
+    KKT_LAUNCH(c, pack_lower_kernel, ny, 256, 0, nx, ny, c->kuf, c->ld, c->Lpk_stride, c->ab.p,
+               c->Li.p, c->Lpk.p);
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+    c->Li.release();
+    c->Ui.release();
+  }
 }
 
 }  // namespace kkt

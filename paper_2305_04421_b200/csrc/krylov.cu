@@ -249,39 +249,6 @@ double fetch(Ctx* c, const double* d) {
   return h;
 }
 
-struct PhaseTimer {
-  Ctx* c;
-  cudaEvent_t e[5] = {};
-  bool on;
-  explicit PhaseTimer(Ctx* ctx) : c(ctx), on(ctx->phase_timing) {
-    if (on)
-      for (auto& x : e) KKT_CUDA(cudaEventCreate(&x));
-  }
-  ~PhaseTimer() {
-    if (on)
-      for (auto& x : e) cudaEventDestroy(x);
-  }
-  void mark(int i) {
-    if (on) KKT_CUDA(cudaEventRecord(e[i], c->stream));
-  }
-  // after a host sync: [0]->[1] P^-1, [1]->[2] K, [2]->[3] Krylov vector work
-  void collect(bool with_prec) {
-    if (!on) return;
-    float ms = 0;
-    if (with_prec) {
-      cudaEventElapsedTime(&ms, e[0], e[1]);
-      c->phase_ms[1] += ms;
-      c->phase_cnt[1]++;
-    }
-    cudaEventElapsedTime(&ms, e[1], e[2]);
-    c->phase_ms[0] += ms;
-    c->phase_cnt[0]++;
-    cudaEventElapsedTime(&ms, e[2], e[3]);
-    c->phase_ms[2] += ms;
-    c->phase_cnt[2]++;
-  }
-};
-
 }  // namespace
 
 double dev_dot(Ctx* c, const double* a, const double* b, int64_t n, double* dst) {
@@ -340,7 +307,6 @@ int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* his
   int total_iters = 0;
   bool converged = false;
   bool first_cycle = true;
-  PhaseTimer timer(c);
   while (total_iters < P.max_iters && !converged) {
     double* r = c->g_r.p;
     if (first_cycle) {
@@ -369,16 +335,19 @@ int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* his
     double* z = c->g_z.p;
     std::vector<double> hh(cycle + 2);
     for (int j = 0; j < cycle; ++j) {
-      timer.mark(0);
       if (have_prec) {
+        c->tbegin(1);
         pinv_apply(c, c->basis[j].p, z);
-        timer.mark(1);
+        c->tend(1);
+        c->tbegin(0);
         op_apply_K(c, z, w, nullptr);
+        c->tend(0);
       } else {
-        timer.mark(1);
+        c->tbegin(0);
         op_apply_K(c, c->basis[j].p, w, nullptr);
+        c->tend(0);
       }
-      timer.mark(2);
+      c->tbegin(2);
       // ---- modified Gram-Schmidt, fused (gmres.cpp:92-96)
       {
         DotArgs A{kDotPlain, n, w, nullptr, nullptr, c->basis[0].p, hd + 0, c->flag.p};
@@ -392,12 +361,12 @@ int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* his
         DotArgs A{kDotAxpySelf, n, w, c->basis[j].p, hd + j, nullptr, hd + j + 1, nullptr};
         launch_dot(c, A);
       }
-      timer.mark(3);
+      c->tend(2);
       int bad = 0;
       KKT_CUDA(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c->stream));
       KKT_CUDA(cudaMemcpyAsync(&bad, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       KKT_CUDA(cudaStreamSynchronize(c->stream));
-      timer.collect(have_prec);
+      c->tcollect();
       if (bad) {
         throw Error(KKT_EDIVERGED,
                     "gmres: non-finite values in Krylov vector at iteration " +

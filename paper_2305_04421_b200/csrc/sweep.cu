@@ -38,7 +38,7 @@ const T* upload(Ctx* c, DBuf<char>& buf, const std::vector<T>& v) {
 
 void band_solve(Ctx* c, double* b, int nrhs, bool transpose) {
   const size_t nsp = c->nsp;
-  if (c->mode == KKT_MODE_STRICT || c->Li.p == nullptr) {
+  if (c->mode == KKT_MODE_STRICT || !c->has_fast()) {
     std::vector<SolveStep> jobs(nrhs);
     for (int k = 0; k < nrhs; ++k) jobs[k] = {b + k * nsp, nullptr, b + k * nsp, 1.0, transpose ? 1 : 0};
     strict_chains(c, upload(c, c->jobs_strict, jobs), nrhs, 1);
@@ -52,7 +52,7 @@ void band_solve(Ctx* c, double* b, int nrhs, bool transpose) {
 void window_solve(Ctx* c, double* b, int len, bool adjoint) {
   const size_t nsp = c->nsp;
   if (len <= 0) return;
-  if (c->mode == KKT_MODE_STRICT || c->Li.p == nullptr) {
+  if (c->mode == KKT_MODE_STRICT || !c->has_fast()) {
     std::vector<SolveStep> jobs;
     for (int t = 0; t < len; ++t) {
       const int k = adjoint ? len - 1 - t : t;
@@ -83,7 +83,7 @@ void rasq_apply(Ctx* c, const double* r, double* out, bool fused_coarse) {
   const int nsteps = 2 * m + 1;
   auto plane = [&](const double* base, int n) { return base + (n - 1) * nsp; };
   auto wplane = [&](double* base, int n) { return base + (n - 1) * nsp; };
-  if (c->mode == KKT_MODE_STRICT || c->Li.p == nullptr) {
+  if (c->mode == KKT_MODE_STRICT || !c->has_fast()) {
     // scratch: one plane per subdomain for the shared node's forward value
     const size_t need = size_t(Nd) * nsp;
     if (c->tmpB3.n < need) c->tmpB3.alloc(need);

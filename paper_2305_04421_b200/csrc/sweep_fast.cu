@@ -162,6 +162,10 @@ __global__ void __launch_bounds__(kFastThreads) fast_chain_kernel(FastParams P,
 
 void fast_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms) {
   if (nchains <= 0 || nsteps <= 0) return;
+  if (c->Lpk.p) {
+    tma_chains(c, jobs_dev, nchains, nsteps, coarse_terms);
+    return;
+  }
   const size_t need = size_t(nchains) * c->nsp;
   if (c->sweep_ws.n < need) c->sweep_ws.alloc(need);
   FastParams P;
@@ -178,7 +182,9 @@ void fast_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool
   P.ws = c->sweep_ws.p;
   P.ws_stride = c->nsp;
   const size_t smem = sizeof(double) * 3 * size_t(c->nx);
+  c->tbegin(3);
   KKT_LAUNCH(c, fast_chain_kernel, nchains, kFastThreads, smem, P, jobs_dev, nsteps, coarse_terms);
+  c->tend(3);
 }
 
 }  // namespace kkt
