@@ -80,7 +80,7 @@ def exported_symbols():
     hdr = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
                        "kktdd_b200.h")
     txt = open(hdr).read()
-    return sorted(set(re.findall(r"\b(kkt_[a-z0-9_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(kkt_[A-Za-z0-9_]+)\s*\(", txt)))
 
 
 def _raise(status, msg, index):

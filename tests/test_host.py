@@ -1,0 +1,141 @@
+"""CPU tests of the host side: the C-ABI library loads and exports every
+symbol include/kktdd_b200.h declares (no device calls), the struct mirror
+matches the header, and the seeded input generator is deterministic and
+chunk-independent.
+"""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2305_04421_b200 import _abi, problems as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "kktdd_b200.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2305_04421_b200 import build
+    from paper_2305_04421_b200 import solver
+    if not os.path.exists(solver.LIB_PATH):
+        build.build()
+    return solver.lib()
+
+
+def declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(kkt_[A-Za-z0-9_]+)\s*\(", txt)))
+
+
+def test_header_declares_the_boundary():
+    names = declared()
+    for must in ["kkt_ctx_create", "kkt_apply_K", "kkt_apply_P_inv", "kkt_gmres_solve",
+                 "kkt_gmres_solve_host", "kkt_apply_rasq", "kkt_apply_two_level", "kkt_apply_shat",
+                 "kkt_forward_solve_window", "kkt_adjoint_solve_window", "kkt_coarse_restrict"]:
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib._name], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (kkt_[A-Za-z0-9_]+)", out))
+    missing = [n for n in declared() if n not in exported]
+    assert not missing, missing
+    for n in declared():
+        getattr(lib, n)  # resolvable through ctypes
+
+
+def test_library_is_sm100a(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", lib._name], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_desc_defaults_match_reference(lib):
+    d = _abi.ProblemDesc()
+    lib.kkt_problem_desc_default(C.byref(d))
+    ref = P.Problem()  # config.hpp:36-50 defaults mirrored in problems.Problem
+    assert (d.Lx, d.Ly, d.T, d.Nx, d.Ny, d.Nt, d.nu, d.omega, d.Nd) == (
+        ref.Lx, ref.Ly, ref.T, ref.Nx, ref.Ny, ref.Nt, ref.nu, ref.omega, ref.Nd)
+    assert d.precond == P.PRECOND[ref.precond] and d.coarse_variant == P.COARSE[ref.coarse_variant]
+    assert d.tol == ref.tol and d.max_iters == ref.max_iters and d.restart == 0
+    assert d.happy_breakdown_tol == ref.happy_breakdown_tol
+
+
+def test_status_strings(lib):
+    lib.kkt_status_string.restype = C.c_char_p
+    assert lib.kkt_status_string(0) == b"ok"
+    assert lib.kkt_status_string(_abi.KKT_ESINGULAR) == b"singular matrix"
+
+
+def test_create_without_device_fails_loudly(lib):
+    """No GPU here: context creation must fail with a CUDA status, never fall back."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    d = _abi.desc_from_problem(P.config(0))
+    h = C.c_void_p()
+    st = lib.kkt_ctx_create(C.byref(d), None, C.byref(h))
+    assert st == _abi.KKT_ECUDA and not h.value
+
+
+def test_solver_refuses_without_cuda():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    from paper_2305_04421_b200.solver import HeatKKT
+    with pytest.raises(RuntimeError):
+        HeatKKT(P.config(0))
+
+
+# ---------------------------------------------------------------------------
+# input generator
+# ---------------------------------------------------------------------------
+def test_generator_is_counter_based():
+    a = P.normal(7, 1, 1000)
+    b = np.concatenate([P.normal(7, 1, 300), P.normal(7, 1, 700, offset=300)])
+    assert np.array_equal(a, b)
+    c = P.normal(7, 1, 1000, chunk=64)
+    assert np.array_equal(a, c)
+    assert not np.array_equal(a, P.normal(7, 2, 1000))
+    assert abs(a.mean()) < 0.1 and abs(a.std() - 1.0) < 0.1
+    u = P.uniform01(3, 0, np.arange(10000, dtype=np.uint64))
+    assert u.min() > 0.0 and u.max() <= 1.0
+
+
+def test_rhs_slices_agree_with_full_field():
+    p = P.config(0)
+    tgt, u0 = P.target_and_u0(0, p)
+    part, _ = P.target_and_u0(0, p, n_lo=17, n_hi=32)
+    assert np.array_equal(tgt[16:32], part)
+    b = P.kkt_rhs(0, p)
+    assert b.size == 3 * p.block
+    assert np.array_equal(b[:p.block], (p.mass_scale * tgt).reshape(-1))
+    assert not np.any(b[p.block:2 * p.block])
+
+
+def test_baseline_config_sizes():
+    # SURVEY.md §8 size table
+    rows = {0: (961, 64, 4, 184512), 1: (16129, 512, 16, 24774144), 2: (261121, 1024, 64, 802163712),
+            3: (65025, 4096, 32, 799027200), 4: (1046529, 1024, 128, 3214937088)}
+    for cfg, (nsp, nt, nd, unknowns) in rows.items():
+        p = P.config(cfg)
+        assert (p.n_sp, p.Nt, p.Nd, 3 * p.block) == (nsp, nt, nd, unknowns)
+    assert P.config(1).mass_scale == pytest.approx(1.1920928955078125e-07)
+
+
+def test_config4_modes_recorded():
+    a, k, l, m = P._modes_c4(P.SEED + 4)
+    assert a.shape == (8,) and k.min() >= 1 and k.max() <= 8 and l.min() >= 1 and m.max() <= 8
+
+
+def test_bench_roofline_bytes():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    p = P.config(1)
+    # (2Nt + Nd - 1) * 5 * n_sp * 8 + (2m+1) * 8 n_sp (2 nx + 1)
+    assert bench.sweep_bytes(p) == (2 * 512 + 15) * 5 * 16129 * 8 + 65 * 8 * 16129 * 255
