@@ -87,6 +87,10 @@ struct Ctx {
   DBuf<double> Lpk;
   int Lpk_stride = 0;
   bool has_fast() const { return Li.p != nullptr || Lpk.p != nullptr; }
+  // fast v3 (group-parallel): dense in-group inflow propagators (kMaxNx^2 each)
+  DBuf<double> Phi, Psi;
+  int grp_g = 0, grp_n = 0;
+  DBuf<double> grp_y, grp_x, grp_e, grp_f;
 
   // ---- coarse space (scalar variant)
   bool has_coarse = false;

@@ -12,6 +12,7 @@
 // lower) and Ui_J = U_JJ^{-1} (upper), the operators of the fast blocked
 // substitution (sweep.cu).
 #include <cmath>
+#include <cstdlib>
 
 #include "sweep.cuh"
 
@@ -273,6 +274,7 @@ void build_block_inverses(Ctx* c) {
     KKT_LAUNCH(c, pack_lower_kernel, ny, 256, 0, nx, ny, c->kuf, c->ld, c->Lpk_stride, c->ab.p,
                c->Li.p, c->Lpk.p);
     KKT_CUDA(cudaStreamSynchronize(c->stream));
+    if (group_supported(c) && getenv("KKT_SWEEP_V2") == nullptr) build_group_operators(c);
     c->Li.release();
     c->Ui.release();
   }

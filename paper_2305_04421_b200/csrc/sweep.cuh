@@ -34,6 +34,9 @@ struct FastStep {
 void strict_chains(Ctx* c, const SolveStep* jobs_dev, int nchains, int nsteps);
 void fast_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms);
 bool tma_supported(const Ctx* c);
+bool group_supported(const Ctx* c);
+void build_group_operators(Ctx* c);
+void group_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms);
 void tma_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms);
 
 }  // namespace kkt
