@@ -91,6 +91,7 @@ struct Ctx {
   DBuf<double> Phi, Psi;
   int grp_g = 0, grp_n = 0;
   DBuf<double> grp_y, grp_x, grp_e, grp_f;
+  DBuf<double> grp_tl, grp_tu;     // products of group-boundary propagators
 
   // ---- coarse space (scalar variant)
   bool has_coarse = false;

@@ -10,8 +10,8 @@
 // Both are affine block recurrences.  The ny block rows are cut into groups of
 // g rows; the dependent chain of 2*ny block steps per solve becomes
 //   A  every (chain, group) runs its g steps with zero inflow       (parallel)
-//   B  every chain propagates the group-boundary values:
-//        e_g = ytilde_end(g) + Phi_end(g) e_{g-1}                   (NG-1 steps)
+//   B  every (chain, group) forms its boundary value
+//        e_g = ytilde_end(g) + Phi_end(g) e_{g-1}  (unrolled, see phase B)
 //   C  every block row adds its inflow term  y_J += Phi_J e_{g-1}   (parallel,
 //      one CTA per J, all chains at once with fp64 DMMA)
 // with Phi_J = G_J ... G_{first(g)} (and Psi_J = H_J ... H_{last(g)} for the
@@ -20,8 +20,10 @@
 // the same substitution with a re-associated recurrence (rounding-level
 // differences, gated like the rest of the fast mode).
 //
-// Per spatial solve: 6 launches (A/B/C for L and U); the dependent depth per
-// sweep drops from ny to g + NG - 1 block steps and ~NG*Nd SMs work at once.
+// Phase B is unrolled into independent sums with precomputed products of the
+// group-boundary propagators, so per spatial solve there are 6 launches
+// (A/B/C for L and U) and the dependent depth per sweep drops from ny block
+// steps to g steps + 2 parallel GEMM-like phases, with ~NG*Nd SMs at work.
 #include <vector>
 
 #include "sweep_tma.cuh"
@@ -45,6 +47,8 @@ struct GrpParams {
   double inv_ms;
   const double* Phi;   // ny dense matrices (L sweep inflow propagators)
   const double* Psi;   // ny dense matrices (U sweep)
+  const double* Tl;    // NG(NG-1)/2 dense: products of group-end Phi's (L boundary pass)
+  const double* Tu;    // NG(NG-1)/2 dense: products of group-start Psi's (U boundary pass)
   int g, NG, Nd;
   double* Ytil;        // per chain nsp
   double* Xtil;        // per chain nsp
@@ -205,46 +209,56 @@ __global__ void __launch_bounds__(kThreads, 1) grpA_U_kernel(GrpParams P, const 
 }
 
 // ---------------------------------------------------------------------------
-// phase B: per chain, propagate group-boundary values through the groups
-//   L: e_0 = ytilde_end(0);  e_g = ytilde_end(g) + Phi_end(g) e_{g-1}
-//   U: f_last = xtilde_first(last); f_g = xtilde_first(g) + Psi_first(g) f_{g+1}
+// phase B: group-boundary values, all groups in parallel.  The boundary
+// recurrence  e_g = yt_end(g) + Phi_end(g) e_{g-1}  (e_0 = yt_end(0)) is
+// unrolled with the precomputed products T_{g,i} = Phi_end(g)...Phi_end(i+1):
+//     e_g = yt_end(g) + sum_{i<g} T_{g,i} yt_end(i)
+// and likewise f_g = xt_first(g) + sum_{i>g} S_{g,i} xt_first(i) for the U
+// sweep (S on mirrored group indices).  One CTA per (group, chain).
 // ---------------------------------------------------------------------------
+__host__ __device__ inline int tri_index(int g, int i) { return g * (g - 1) / 2 + i; }  // i < g
+
 template <bool kUpper>
 __global__ void __launch_bounds__(kThreads, 1) grpB_kernel(GrpParams P, const FastStep* steps,
                                                           int nsteps, int t) {
-  __shared__ double ev[kMaxNx];
   __shared__ double ov[kMaxNx];
-  const int s = blockIdx.x;
+  const int grp = blockIdx.x, s = blockIdx.y;
   const FastStep st = steps[int64_t(s) * nsteps + t];
   if (!st.in) return;
-  const int nx = P.nx, tid = threadIdx.x;
+  const int nx = P.nx, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* til = (kUpper ? P.Xtil : P.Ytil) + int64_t(s) * P.nsp;
   double* outv = (kUpper ? P.F : P.E) + int64_t(s) * P.NG * kMaxNx;
-  const double* M = kUpper ? P.Psi : P.Phi;
-  auto row_of = [&](int grp) {  // boundary row of a group
-    return kUpper ? grp * P.g : min(P.ny, (grp + 1) * P.g) - 1;
-  };
-  const int first = kUpper ? P.NG - 1 : 0;
-  const int step = kUpper ? -1 : 1;
-  if (tid < kMaxNx) {
-    const double v = tid < nx ? til[row_of(first) * nx + tid] : 0.0;
-    ev[tid] = v;
-    outv[first * kMaxNx + tid] = v;
-  }
-  __syncthreads();
-  for (int i = 1; i < P.NG; ++i) {
-    const int grp = first + step * i;
-    const int J = row_of(grp);
+  auto row_of = [&](int gg) { return kUpper ? gg * P.g : min(P.ny, (gg + 1) * P.g) - 1; };
+  // mirrored index for the U sweep: group gg -> NG-1-gg
+  const int gm = kUpper ? P.NG - 1 - grp : grp;
+  double acc[kR];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) acc[r] = 0.0;
+  for (int im = 0; im < gm; ++im) {
+    const int i = kUpper ? P.NG - 1 - im : im;  // source group
+    const double* src = til + row_of(i) * nx;
     double vr[kK];
-    load_vr(ev, nullptr, 0.0, vr, nx);
-    dense_mv(M + int64_t(J) * kDense, kLd, vr, ov, nx);
-    __syncthreads();
-    if (tid < kMaxNx) {
-      const double v = tid < nx ? til[J * nx + tid] + ov[tid] : 0.0;
-      ev[tid] = v;
-      outv[grp * kMaxNx + tid] = v;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+      const int b = lane + 32 * k;
+      vr[k] = b < nx ? src[b] : 0.0;
     }
-    __syncthreads();
+    const double* M = (kUpper ? P.Tu : P.Tl) + int64_t(tri_index(gm, im)) * kDense;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const int a = warp + kWarps * r;
+      if (a < nx) {
+        const double* row = M + a * kLd;
+#pragma unroll
+        for (int k = 0; k < kK; ++k) acc[r] = fma(row[lane + 32 * k], vr[k], acc[r]);
+      }
+    }
+  }
+  rows_reduce_store(acc, ov, nx);
+  __syncthreads();
+  if (tid < kMaxNx) {
+    const double v = tid < nx ? til[row_of(grp) * nx + tid] + (gm > 0 ? ov[tid] : 0.0) : 0.0;
+    outv[grp * kMaxNx + tid] = v;
   }
 }
 
@@ -417,6 +431,8 @@ GrpParams params(Ctx* c) {
   P.inv_ms = 1.0 / c->ms;
   P.Phi = c->Phi.p;
   P.Psi = c->Psi.p;
+  P.Tl = c->grp_tl.p;
+  P.Tu = c->grp_tu.p;
   P.g = c->grp_g;
   P.NG = c->grp_n;
   P.Nd = c->Nd;
@@ -506,6 +522,39 @@ void build_group_operators(Ctx* c) {
     }
   }
   (void)idx;
+  // boundary-pass products: Tl_{g,i} = Phi_end(g) Tl_{g-1,i}, Tl_{g,g-1} = Phi_end(g);
+  // Tu on mirrored indices with Psi_first
+  const int NG = c->grp_n;
+  const int ntri = std::max(1, NG * (NG - 1) / 2);
+  c->grp_tl.alloc(size_t(ntri) * kDense);
+  c->grp_tu.alloc(size_t(ntri) * kDense);
+  auto end_row = [&](int gg) { return std::min(ny, (gg + 1) * g) - 1; };
+  auto first_row = [&](int gg) { return gg * g; };
+  for (int side = 0; side < 2; ++side) {
+    const double* src = side == 0 ? c->Phi.p : c->Psi.p;
+    double* T = side == 0 ? c->grp_tl.p : c->grp_tu.p;
+    for (int gm = 1; gm < NG; ++gm) {
+      const int gg = side == 0 ? gm : NG - 1 - gm;
+      const int J = side == 0 ? end_row(gg) : first_row(gg);
+      // T_{gm, gm-1} = M_J
+      KKT_CUDA(cudaMemcpyAsync(T + size_t(tri_index(gm, gm - 1)) * kDense, src + size_t(J) * kDense,
+                               sizeof(double) * kDense, cudaMemcpyDeviceToDevice, c->stream));
+      if (gm >= 2) {
+        // T_{gm, i} = M_J T_{gm-1, i}, i < gm-1: dst/A/B index triples relative to
+        // separate bases -> stage M_J as matrix 0 of a scratch base
+        trips.clear();
+        for (int i = 0; i < gm - 1; ++i) {
+          trips.push_back(tri_index(gm, i));
+          trips.push_back(J);
+          trips.push_back(tri_index(gm - 1, i));
+        }
+        DBuf<int> d(trips.size());
+        KKT_CUDA(cudaMemcpyAsync(d.p, trips.data(), sizeof(int) * trips.size(), cudaMemcpyHostToDevice, c->stream));
+        KKT_LAUNCH(c, mm_batch_kernel, int(trips.size() / 3), 256, 0, d.p, src, T, T);
+        KKT_CUDA(cudaStreamSynchronize(c->stream));
+      }
+    }
+  }
   c->grp_y.alloc(size_t(c->Nd) * c->nsp);
   c->grp_x.alloc(size_t(c->Nd) * c->nsp);
   c->grp_e.alloc(size_t(c->Nd) * c->grp_n * kMaxNx);
@@ -541,10 +590,10 @@ void group_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, boo
   c->tbegin(3);
   for (int t = 0; t < nsteps; ++t) {
     KKT_LAUNCH(c, grpA_L_kernel, gA, kThreads, sA, P, jobs_dev, nsteps, t, coarse_terms);
-    KKT_LAUNCH(c, grpB_kernel<false>, nchains, kThreads, 0, P, jobs_dev, nsteps, t);
+    KKT_LAUNCH(c, grpB_kernel<false>, gA, kThreads, 0, P, jobs_dev, nsteps, t);
     KKT_LAUNCH(c, grpC_kernel<false>, c->ny, kThreads, sC, P, jobs_dev, nsteps, t);
     KKT_LAUNCH(c, grpA_U_kernel, gA, kThreads, sA, P, jobs_dev, nsteps, t);
-    KKT_LAUNCH(c, grpB_kernel<true>, nchains, kThreads, 0, P, jobs_dev, nsteps, t);
+    KKT_LAUNCH(c, grpB_kernel<true>, gA, kThreads, 0, P, jobs_dev, nsteps, t);
     KKT_LAUNCH(c, grpC_kernel<true>, c->ny, kThreads, sC, P, jobs_dev, nsteps, t);
   }
   c->tend(3);
