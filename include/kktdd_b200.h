@@ -92,8 +92,10 @@ typedef struct kkt_runtime_opts {
   int32_t mode;             /* KKT_MODE_* */
   int32_t device;           /* CUDA device ordinal, -1 = current */
   int32_t rank, nranks;     /* time-slab sharding; nranks == 1 for a single GPU */
-  const void* nccl_unique_id; /* 128-byte ncclUniqueId when nranks > 1, else NULL */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId when nranks > 1 (one process per GPU) */
   void* stream;             /* cudaStream_t, NULL = context-owned stream */
+  void* local_group;        /* kkt_local_group_create handle: ranks as host threads of one
+                               process (testing the sharded path on one device); else NULL */
 } kkt_runtime_opts;
 
 typedef struct kkt_ctx kkt_ctx;
@@ -187,8 +189,16 @@ int kkt_phase_times(const kkt_ctx* ctx, double* ms4, int64_t* counts4);
  * pivot vector to HOST buffers (either may be NULL). */
 int kkt_debug_ahat_factor(kkt_ctx* ctx, int32_t* kl, int32_t* ku, double* ab_host, int32_t* piv_host);
 
-/* Helpers for multi-rank bring-up: returns a fresh ncclUniqueId (128 bytes). */
+/* Multi-rank bring-up (time-slab sharding).  Rank g of G owns
+ * subdomains [g*Nd/G, (g+1)*Nd/G) and their nodes; every vector argument is
+ * then the rank-local slab [u_loc; z_loc; w_loc] (kkt_layout gives its size).
+ * G must divide Nd; STRICT mode is single-rank.
+ * kkt_nccl_unique_id: a fresh ncclUniqueId (128 bytes) for kkt_runtime_opts.
+ * kkt_local_group_*: an in-process group whose ranks are host threads sharing
+ * one device; exchanges are host-synchronised between launches. */
 int kkt_nccl_unique_id(void* out128);
+int kkt_local_group_create(int32_t nranks, void** out);
+int kkt_local_group_destroy(void* group);
 
 #ifdef __cplusplus
 }

@@ -36,6 +36,7 @@ class RuntimeOpts(C.Structure):
         ("mode", C.c_int32), ("device", C.c_int32),
         ("rank", C.c_int32), ("nranks", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
+        ("local_group", C.c_void_p),
     ]
 
 

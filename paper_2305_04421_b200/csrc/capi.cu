@@ -15,6 +15,7 @@ namespace kkt {
 
 Ctx::~Ctx() {
   if (stream) cudaStreamSynchronize(stream);
+  delete comm;
   basis.clear();
   for (auto e : ev_pool) cudaEventDestroy(e);
   for (auto& iv : ev_pending) { cudaEventDestroy(iv.a); cudaEventDestroy(iv.b); }
@@ -87,8 +88,16 @@ void setup(Ctx* c, const kkt_problem_desc& d, const kkt_runtime_opts* o) {
   c->mode = o ? o->mode : KKT_MODE_FAST;
   c->rank = o ? o->rank : 0;
   c->nranks = o ? o->nranks : 1;
-  if (c->nranks != 1)
-    throw Error(KKT_EUNSUPPORTED, "multi-rank time-slab sharding is not enabled in this build");
+  if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks)
+    throw Error(KKT_EINVAL, "bad rank / nranks");
+  if (c->nranks > 1) {
+    if (c->mode == KKT_MODE_STRICT)
+      throw Error(KKT_EUNSUPPORTED,
+                  "strict (bitwise) mode is single-rank: the reference's left-to-right sums cross slabs");
+    if (d.Nd % c->nranks != 0)
+      throw Error(KKT_ECONFIG, "time-slab sharding needs nranks to divide Nd (Nd=" +
+                                   std::to_string(d.Nd) + ", nranks=" + std::to_string(c->nranks) + ")");
+  }
   int dev = (o && o->device >= 0) ? o->device : -1;
   if (dev < 0) KKT_CUDA(cudaGetDevice(&dev));
   KKT_CUDA(cudaSetDevice(dev));
@@ -98,6 +107,14 @@ void setup(Ctx* c, const kkt_problem_desc& d, const kkt_runtime_opts* o) {
   } else {
     KKT_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
+  }
+  if (c->nranks > 1) {
+    if (o->local_group)
+      c->comm = make_local_comm(o->local_group, c->rank);
+    else if (o->nccl_unique_id)
+      c->comm = make_nccl_comm(o->nccl_unique_id, c->rank, c->nranks);
+    else
+      throw Error(KKT_EINVAL, "nranks > 1 needs an NCCL unique id or a local group");
   }
   if (d.precond == KKT_PRECOND_DENSE_SCHUR || d.precond == KKT_PRECOND_TRUE_SCHUR)
     throw Error(KKT_EUNSUPPORTED,
@@ -110,7 +127,14 @@ void setup(Ctx* c, const kkt_problem_desc& d, const kkt_runtime_opts* o) {
   c->Nt = d.Nt;
   c->Nd = d.Nd;
   c->m = d.Nt / d.Nd;
-  c->B = int64_t(c->Nt) * c->nsp;
+  c->Bg = int64_t(c->Nt) * c->nsp;
+  // time slab of this rank: whole subdomains [s0, s0+ndl), nodes [n0, n0+ntl)
+  c->ndl = c->Nd / c->nranks;
+  c->s0 = c->rank * c->ndl;
+  c->ntl = c->ndl * c->m;
+  c->n0 = c->s0 * c->m + 1;
+  c->B = int64_t(c->ntl) * c->nsp;
+  c->halo.alloc(size_t(4) * c->nsp);
   c->dx = d.Lx / d.Nx;
   c->dy = d.Ly / d.Ny;
   c->dt = d.T / d.Nt;
@@ -251,8 +275,9 @@ int kkt_layout(const kkt_ctx* ctx, int64_t* block, int32_t* n_sp, int32_t* node_
   const Ctx& c = ctx->impl;
   if (block) *block = c.B;
   if (n_sp) *n_sp = c.nsp;
-  if (node_first) *node_first = 1;
-  if (node_last) *node_last = c.Nt;
+  if (block) *block = c.Bg;
+  if (node_first) *node_first = c.n0;
+  if (node_last) *node_last = c.n0 + c.ntl - 1;
   if (local_block) *local_block = c.B;
   return KKT_OK;
 }
@@ -436,8 +461,23 @@ int kkt_debug_ahat_factor(kkt_ctx* ctx, int32_t* kl, int32_t* ku, double* ab_hos
 
 int kkt_nccl_unique_id(void* out128) {
   if (!out128) return KKT_EINVAL;
-  std::memset(out128, 0, 128);
-  return KKT_EUNSUPPORTED;
+  try {
+    return kkt::nccl_unique_id(out128);
+  } catch (const Error& e) {
+    kkt::g_create_err = e.what();
+    return e.status;
+  }
+}
+
+int kkt_local_group_create(int32_t nranks, void** out) {
+  if (!out || nranks < 1) return KKT_EINVAL;
+  *out = kkt::local_group_create(nranks);
+  return KKT_OK;
+}
+
+int kkt_local_group_destroy(void* group) {
+  kkt::local_group_destroy(group);
+  return KKT_OK;
 }
 
 }  // extern "C"

@@ -61,6 +61,9 @@ __global__ void __launch_bounds__(256) nodesum_tree_kernel(int nsp, const double
 
 struct CoarseTables {
   int cdim, Nt, m_max;
+  int n0;                  // first local node (node sums are slab-local)
+  int cl0, cl1;            // this rank's columns [cl0, cl1)
+  int nranks;
   const int* col_first;
   const int* col_count;
   const double* col_phi;   // cdim * m_max
@@ -70,13 +73,26 @@ struct CoarseTables {
   const int* piv;
 };
 
-// c = Z^T r from node sums (restrict_to_coarse, schur.cpp:181-204).
+// c = Z^T r from node sums (restrict_to_coarse, schur.cpp:181-204).  Only this
+// rank's columns (its subdomains own their nodes); the others are zero and
+// arrive through the all-gather.
 __device__ void restrict_from_nodesums(const CoarseTables& T, const double* ns, double* c) {
   for (int ci = threadIdx.x; ci < T.cdim; ci += blockDim.x) {
-    const int first = T.col_first[ci], cnt = T.col_count[ci];
-    const double* phi = T.col_phi + int64_t(ci) * T.m_max;
     double acc = 0.0;
-    for (int k = 0; k < cnt; ++k) acc = sadd(acc, smul(phi[k], ns[first + k - 1]));
+    if (ci >= T.cl0 && ci < T.cl1) {
+      const int first = T.col_first[ci], cnt = T.col_count[ci];
+      const double* phi = T.col_phi + int64_t(ci) * T.m_max;
+      for (int k = 0; k < cnt; ++k) acc = sadd(acc, smul(phi[k], ns[first + k - T.n0]));
+    }
+    c[ci] = acc;
+  }
+}
+
+// every position is non-zero on exactly one rank: the rank-ordered sum is exact
+__device__ void gather_columns(const CoarseTables& T, const double* call, double* c) {
+  for (int ci = threadIdx.x; ci < T.cdim; ci += blockDim.x) {
+    double acc = 0.0;
+    for (int r = 0; r < T.nranks; ++r) acc += call[int64_t(r) * T.cdim + ci];
     c[ci] = acc;
   }
 }
@@ -123,12 +139,18 @@ __device__ void gamma_from_c(const CoarseTables& T, const double* c, double* gam
   }
 }
 
-// restrict + solve + prolongation values in one single-CTA launch.
+// restrict + solve + prolongation values in one single-CTA launch.  With
+// several ranks, `call` holds every rank's restricted columns (all-gathered)
+// and `ns` is unused.
 __global__ void __launch_bounds__(kCoarseThreads) coarse_gamma_kernel(CoarseTables T,
                                                                       const double* __restrict__ ns,
+                                                                      const double* __restrict__ call,
                                                                       double* c, double* gam) {
   extern __shared__ double sb[];
-  restrict_from_nodesums(T, ns, sb);
+  if (call)
+    gather_columns(T, call, sb);
+  else
+    restrict_from_nodesums(T, ns, sb);
   __syncthreads();
   lu_solve_block(T, sb);
   for (int i = threadIdx.x; i < T.cdim; i += blockDim.x) c[i] = sb[i];
@@ -141,6 +163,12 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_restrict_kernel(CoarseT
   restrict_from_nodesums(T, ns, c);
 }
 
+__global__ void __launch_bounds__(kCoarseThreads) coarse_gather_kernel(CoarseTables T,
+                                                                       const double* __restrict__ call,
+                                                                       double* c) {
+  gather_columns(T, call, c);
+}
+
 __global__ void __launch_bounds__(kCoarseThreads) coarse_solve_kernel(CoarseTables T, double* c) {
   extern __shared__ double sb[];
   for (int i = threadIdx.x; i < T.cdim; i += blockDim.x) sb[i] = c[i];
@@ -150,12 +178,12 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_solve_kernel(CoarseTabl
 }
 
 // out[n,p] = (out[n,p] + phi_0 c_0) + phi_1 c_1 (prolong_add column order).
-__global__ void prolong_add_kernel(CoarseTables T, int nsp, const double* __restrict__ c,
+__global__ void prolong_add_kernel(CoarseTables T, int ntl, int nsp, const double* __restrict__ c,
                                    double* __restrict__ out) {
-  const int64_t total = int64_t(T.Nt) * nsp;
+  const int64_t total = int64_t(ntl) * nsp;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
-    const int n0 = int(idx / nsp);
+    const int n0 = int(idx / nsp) + T.n0 - 1;  // 0-based global node
     double o = out[idx];
     for (int k = 0; k < 2; ++k) {
       const int ci = T.node_col[2 * n0 + k];
@@ -166,12 +194,12 @@ __global__ void prolong_add_kernel(CoarseTables T, int nsp, const double* __rest
 }
 
 // y_c materialised from gamma: yc[n,p] = gamma_n.
-__global__ void broadcast_gamma_kernel(int nt, int nsp, const double* __restrict__ gam,
+__global__ void broadcast_gamma_kernel(int nt, int nsp, int n0, const double* __restrict__ gam,
                                        double* __restrict__ out) {
   const int64_t total = int64_t(nt) * nsp;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x)
-    out[idx] = gam[1 + idx / nsp];
+    out[idx] = gam[n0 + idx / nsp];
 }
 
 // out = a - b / out = a + b elementwise (schur.cpp:437, :439).
@@ -255,6 +283,10 @@ CoarseTables tables(Ctx* c) {
   T.node_phi = c->node_phi.p;
   T.lu = c->S0lu.p;
   T.piv = c->S0piv.p;
+  T.n0 = c->n0;
+  T.cl0 = c->col_lo;
+  T.cl1 = c->col_hi;
+  T.nranks = c->nranks;
   return T;
 }
 
@@ -397,13 +429,24 @@ void build_coarse(Ctx* c) {
       nphi[2 * (n - 1) + col.kind] = phi[k];
     }
   }
+  c->col_lo = dim;
+  c->col_hi = 0;
+  for (int ci = 0; ci < dim; ++ci) {
+    const int sd = c->cols[ci].s;
+    if (sd >= c->s0 && sd < c->s0 + c->ndl) {
+      c->col_lo = std::min(c->col_lo, ci);
+      c->col_hi = std::max(c->col_hi, ci + 1);
+    }
+  }
+  if (c->col_hi < c->col_lo) c->col_lo = c->col_hi = 0;
   h2d(c, c->col_first, cf);
   h2d(c, c->col_count, cc);
   h2d(c, c->col_phi, cphi);
   h2d(c, c->node_col, ncol);
   h2d(c, c->node_phi, nphi);
-  c->nodesum.alloc(Nt);
+  c->nodesum.alloc(c->ntl);
   c->cvec.alloc(dim);
+  c->call.alloc(size_t(dim) * c->nranks);
   c->gam.alloc(Nt + 2);
   KKT_CUDA(cudaMemsetAsync(c->gam.p, 0, sizeof(double) * (Nt + 2), c->stream));
 
@@ -427,14 +470,23 @@ void build_coarse(Ctx* c) {
 // ---------------------------------------------------------------------------
 static void node_sums(Ctx* c, const double* r) {
   if (c->mode == KKT_MODE_STRICT)
-    KKT_LAUNCH(c, nodesum_seq_kernel, (c->Nt + 127) / 128, 128, 0, c->Nt, c->nsp, r, c->nodesum.p);
+    KKT_LAUNCH(c, nodesum_seq_kernel, (c->ntl + 127) / 128, 128, 0, c->ntl, c->nsp, r, c->nodesum.p);
   else
-    KKT_LAUNCH(c, nodesum_tree_kernel, c->Nt, 256, 0, c->nsp, r, c->nodesum.p);
+    KKT_LAUNCH(c, nodesum_tree_kernel, c->ntl, 256, 0, c->nsp, r, c->nodesum.p);
+}
+
+// restricted columns of this rank -> every rank's columns (all-gather)
+static const double* gather_all(Ctx* c, double* local) {
+  c->comm->allgather(local, c->call.p, size_t(c->cdim), c->stream);
+  return c->call.p;
 }
 
 void coarse_restrict(Ctx* c, const double* r, double* cdev) {
   node_sums(c, r);
-  KKT_LAUNCH(c, coarse_restrict_kernel, 1, kCoarseThreads, 0, tables(c), c->nodesum.p, cdev);
+  KKT_LAUNCH(c, coarse_restrict_kernel, 1, kCoarseThreads, 0, tables(c), c->nodesum.p,
+             c->nranks > 1 ? c->cvec.p : cdev);
+  if (c->nranks > 1)
+    KKT_LAUNCH(c, coarse_gather_kernel, 1, kCoarseThreads, 0, tables(c), gather_all(c, c->cvec.p), cdev);
 }
 
 void coarse_solve(Ctx* c, double* cdev) {
@@ -442,13 +494,18 @@ void coarse_solve(Ctx* c, double* cdev) {
 }
 
 void coarse_prolong_add(Ctx* c, const double* cdev, double* out) {
-  KKT_LAUNCH(c, prolong_add_kernel, grid_for(c->B), 256, 0, tables(c), c->nsp, cdev, out);
+  KKT_LAUNCH(c, prolong_add_kernel, grid_for(c->B), 256, 0, tables(c), c->ntl, c->nsp, cdev, out);
 }
 
 void coarse_gamma(Ctx* c, const double* r) {
   node_sums(c, r);
+  const double* call = nullptr;
+  if (c->nranks > 1) {
+    KKT_LAUNCH(c, coarse_restrict_kernel, 1, kCoarseThreads, 0, tables(c), c->nodesum.p, c->cvec.p);
+    call = gather_all(c, c->cvec.p);
+  }
   KKT_LAUNCH(c, coarse_gamma_kernel, 1, kCoarseThreads, sizeof(double) * c->cdim, tables(c),
-             c->nodesum.p, c->cvec.p, c->gam.p);
+             c->nodesum.p, call, c->cvec.p, c->gam.p);
 }
 
 static void ensure_tmp(Ctx* c) {
@@ -468,7 +525,7 @@ void two_level_apply(Ctx* c, const double* r, double* out, int form) {
   ensure_tmp(c);
   double* yc = c->tmpB1.p;
   const int g = grid_for(c->B);
-  KKT_LAUNCH(c, broadcast_gamma_kernel, g, 256, 0, c->Nt, c->nsp, c->gam.p, yc);
+  KKT_LAUNCH(c, broadcast_gamma_kernel, g, 256, 0, c->ntl, c->nsp, c->n0, c->gam.p, yc);
   switch (form) {
     case KKT_FORM_LITERAL:
       rasq_apply(c, yc, out, false);

@@ -11,9 +11,8 @@
 #include <string>
 #include <vector>
 
+#include "comm.cuh"
 #include "common.cuh"
-
-struct ncclComm;
 
 namespace kkt {
 
@@ -61,11 +60,17 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int rank = 0, nranks = 1;
-  ncclComm* comm = nullptr;
+  Comm* comm = nullptr;            // null when nranks == 1
 
   // ---- sizes / derived constants (config.hpp:52-65, heat_operators.cpp:26-37)
-  int nx = 0, ny = 0, nsp = 0, Nt = 0, Nd = 0, m = 0;
-  int64_t B = 0;  // global block size Nt * n_sp
+  int nx = 0, ny = 0, nsp = 0, Nt = 0, Nd = 0, m = 0;   // Nt, Nd: global
+  // this rank's time slab: nodes n0 .. n0+ntl-1 (1-based, global numbering),
+  // subdomains s0 .. s0+ndl-1.  B is the LOCAL block size ntl * n_sp: every
+  // space-time vector passed across the C-ABI is the rank-local slab.
+  int n0 = 1, ntl = 0, s0 = 0, ndl = 0;
+  int64_t B = 0;
+  int64_t Bg = 0;  // global block size Nt * n_sp
+  DBuf<double> halo;               // 4 planes: receive buffers of the plane exchanges
   double dx = 0, dy = 0, dt = 0, ms = 0, sigma = 0, cx = 0, cy = 0;
   double omega = 0, oms = 0;  // omega * mass_scale as the reference evaluates it
   Stencil A{}, Ahat{};
@@ -109,6 +114,8 @@ struct Ctx {
   DBuf<int> col_kind;             // per column: 0/1 (phi table selector)
   DBuf<double> col_phi;           // per column: phi values over owned nodes (m entries max), col*m_max + k
   int m_max = 0;
+  int col_lo = 0, col_hi = 0;     // this rank's coarse columns
+  DBuf<double> call;              // all-gathered restricted columns (nranks x cdim)
   DBuf<double> a1, a2;            // Ahat*1 and Ahat*(Ahat*1) (fast analytic Shat y_c)
 
   // ---- scratch
@@ -147,6 +154,7 @@ struct Ctx {
   std::string err;
   int err_index = -1;
 
+  DBuf<double> red_all;            // all-gathered partial sums
   ~Ctx();
 };
 
@@ -160,6 +168,13 @@ enum class OpKind { J, JT, Jhat, JhatT };
 void op_time_stencil(Ctx* c, OpKind k, const double* in, double* out);
 void op_scale(Ctx* c, const double* in, double* out, double mul, bool divide);
 void op_time_stencil_n(Ctx* c, bool lower, const double* in, double* out, int nt, double div);
+// plane exchange with the neighbouring ranks (no-op on one rank); returns the
+// received planes (null where the neighbour does not exist)
+struct Halo {
+  const double* prev;  // plane of node n0-1 (from rank-1)
+  const double* next;  // plane of node n0+ntl (from rank+1)
+};
+Halo exchange_halo(Ctx* c, const double* v, int slot_prev, int slot_next, bool want_prev, bool want_next);
 void op_apply_K(Ctx* c, const double* v, double* out, const double* b_minus);
 void op_pinv_uz(Ctx* c, const double* r, double* out);
 void op_shat(Ctx* c, const double* v, double* out, double* tmp);

@@ -216,6 +216,15 @@ __global__ void add_kernel(int64_t n, const double* __restrict__ z, double* __re
     x[i] = sadd(x[i], z[i]);
 }
 
+// rank-ordered sum of the all-gathered partials: identical on every rank
+__global__ void sum_partials_kernel(const double* __restrict__ parts, int n, double* __restrict__ dst) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int r = 0; r < n; ++r) s += parts[r];
+    *dst = s;
+  }
+}
+
 int grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   const int64_t cap = int64_t(kSmCount) * 16;
@@ -240,6 +249,12 @@ void launch_dot(Ctx* c, const DotArgs& A) {
     KKT_LAUNCH(c, dot_seq_kernel, 1, kSeqThreads, 0, A);
   else
     KKT_LAUNCH(c, dot_tree_kernel, kTreeBlocks, kTreeThreads, 0, A, c->red.p, c->red_count.p);
+  if (c->nranks > 1) {
+    // the Krylov global reduction: all-gather one partial per rank, sum in rank order
+    if (c->red_all.n < size_t(c->nranks)) c->red_all.alloc(c->nranks);
+    c->comm->allgather(A.dst, c->red_all.p, 1, c->stream);
+    KKT_LAUNCH(c, sum_partials_kernel, 1, 32, 0, c->red_all.p, c->nranks, A.dst);
+  }
 }
 
 double fetch(Ctx* c, const double* d) {

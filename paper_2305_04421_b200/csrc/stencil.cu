@@ -21,11 +21,15 @@ inline int grid_for(int64_t n, int threads = kThreads) {
 // out_n = S in_n - in_{n-1} (lower: apply_J / apply_Jhat, heat_operators.cpp:57-69,111-123)
 // out_n = S in_n - in_{n+1} (upper: apply_JT / apply_JhatT, :71-83,125-137)
 // post: optional division by `div` (apply_shat's t /= ms, schur.cpp:75).
+// `prev` / `next`: the neighbouring rank's plane beyond the slab (null at the
+// global first / last node, where the reference has no coupling term).
 template <bool kLower, bool kDiv>
 __global__ void __launch_bounds__(kThreads) time_stencil_kernel(Stencil s, int nt, int nsp,
                                                                 const double* __restrict__ in,
                                                                 double* __restrict__ out,
-                                                                double div) {
+                                                                double div,
+                                                                const double* __restrict__ prev,
+                                                                const double* __restrict__ next) {
   const int64_t total = int64_t(nt) * nsp;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
@@ -35,8 +39,10 @@ __global__ void __launch_bounds__(kThreads) time_stencil_kernel(Stencil s, int n
     double acc = band_row_strict(s, plane, p);
     if (kLower) {
       if (n0 > 0) acc = ssub(acc, in[idx - nsp]);
+      else if (prev) acc = ssub(acc, prev[p]);
     } else {
       if (n0 < nt - 1) acc = ssub(acc, in[idx + nsp]);
+      else if (next) acc = ssub(acc, next[p]);
     }
     if (kDiv) acc = sdiv(acc, div);
     out[idx] = acc;
@@ -62,7 +68,9 @@ __global__ void __launch_bounds__(kThreads) apply_K_kernel(Stencil s, int nt, in
                                                            double oms, double dt,
                                                            const double* __restrict__ v,
                                                            double* __restrict__ out,
-                                                           const double* __restrict__ bm) {
+                                                           const double* __restrict__ bm,
+                                                           const double* __restrict__ u_prev,
+                                                           const double* __restrict__ w_next) {
   const int64_t B = int64_t(nt) * nsp;
   const double* u = v;
   const double* z = v + B;
@@ -75,10 +83,12 @@ __global__ void __launch_bounds__(kThreads) apply_K_kernel(Stencil s, int nt, in
     const double uu = u[idx], zz = z[idx], ww = w[idx];
     double ou = band_row_strict(s, w + off, p);
     if (n0 < nt - 1) ou = ssub(ou, w[idx + nsp]);
+    else if (w_next) ou = ssub(ou, w_next[p]);
     ou = sadd(ou, smul(ms, uu));
     const double oz = ssub(smul(oms, zz), smul(dt, ww));
     double ow = band_row_strict(s, u + off, p);
     if (n0 > 0) ow = ssub(ow, u[idx - nsp]);
+    else if (u_prev) ow = ssub(ow, u_prev[p]);
     ow = ssub(ow, smul(dt, zz));
     if (bm) {
       out[idx] = ssub(bm[idx], ou);
@@ -105,20 +115,39 @@ __global__ void __launch_bounds__(kThreads) pinv_uz_kernel(int64_t B, double ms,
 
 }  // namespace
 
+Halo exchange_halo(Ctx* c, const double* v, int slot_prev, int slot_next, bool want_prev,
+                   bool want_next) {
+  Halo h{nullptr, nullptr};
+  if (c->nranks == 1) return h;
+  const size_t nsp = c->nsp;
+  double* hp = c->halo.p + size_t(slot_prev) * nsp;
+  double* hn = c->halo.p + size_t(slot_next) * nsp;
+  // every rank that wants its `next` plane receives it from rank+1, which sends
+  // its first plane backwards; `prev` planes travel forwards (last plane)
+  c->comm->halo(want_next ? v : nullptr, want_next ? hn : nullptr,
+                want_prev ? v + size_t(c->ntl - 1) * nsp : nullptr, want_prev ? hp : nullptr, nsp,
+                c->stream);
+  if (want_prev && c->rank > 0) h.prev = hp;
+  if (want_next && c->rank + 1 < c->nranks) h.next = hn;
+  return h;
+}
+
 void op_time_stencil(Ctx* c, OpKind k, const double* in, double* out) {
   const int g = grid_for(c->B);
+  const bool lower = k == OpKind::J || k == OpKind::Jhat;
+  const Halo h = exchange_halo(c, in, 0, 1, lower, !lower);
   switch (k) {
     case OpKind::J:
-      KKT_LAUNCH(c, (time_stencil_kernel<true, false>), g, kThreads, 0, c->A, c->Nt, c->nsp, in, out, 1.0);
+      KKT_LAUNCH(c, (time_stencil_kernel<true, false>), g, kThreads, 0, c->A, c->ntl, c->nsp, in, out, 1.0, h.prev, nullptr);
       break;
     case OpKind::JT:
-      KKT_LAUNCH(c, (time_stencil_kernel<false, false>), g, kThreads, 0, c->A, c->Nt, c->nsp, in, out, 1.0);
+      KKT_LAUNCH(c, (time_stencil_kernel<false, false>), g, kThreads, 0, c->A, c->ntl, c->nsp, in, out, 1.0, nullptr, h.next);
       break;
     case OpKind::Jhat:
-      KKT_LAUNCH(c, (time_stencil_kernel<true, false>), g, kThreads, 0, c->Ahat, c->Nt, c->nsp, in, out, 1.0);
+      KKT_LAUNCH(c, (time_stencil_kernel<true, false>), g, kThreads, 0, c->Ahat, c->ntl, c->nsp, in, out, 1.0, h.prev, nullptr);
       break;
     case OpKind::JhatT:
-      KKT_LAUNCH(c, (time_stencil_kernel<false, false>), g, kThreads, 0, c->Ahat, c->Nt, c->nsp, in, out, 1.0);
+      KKT_LAUNCH(c, (time_stencil_kernel<false, false>), g, kThreads, 0, c->Ahat, c->ntl, c->nsp, in, out, 1.0, nullptr, h.next);
       break;
   }
 }
@@ -129,13 +158,13 @@ void op_time_stencil_n(Ctx* c, bool lower, const double* in, double* out, int nt
   const int g = grid_for(int64_t(nt) * c->nsp);
   const bool d = div != 0.0;
   if (lower && d)
-    KKT_LAUNCH(c, (time_stencil_kernel<true, true>), g, kThreads, 0, c->Ahat, nt, c->nsp, in, out, div);
+    KKT_LAUNCH(c, (time_stencil_kernel<true, true>), g, kThreads, 0, c->Ahat, nt, c->nsp, in, out, div, nullptr, nullptr);
   else if (lower)
-    KKT_LAUNCH(c, (time_stencil_kernel<true, false>), g, kThreads, 0, c->Ahat, nt, c->nsp, in, out, 1.0);
+    KKT_LAUNCH(c, (time_stencil_kernel<true, false>), g, kThreads, 0, c->Ahat, nt, c->nsp, in, out, 1.0, nullptr, nullptr);
   else if (d)
-    KKT_LAUNCH(c, (time_stencil_kernel<false, true>), g, kThreads, 0, c->Ahat, nt, c->nsp, in, out, div);
+    KKT_LAUNCH(c, (time_stencil_kernel<false, true>), g, kThreads, 0, c->Ahat, nt, c->nsp, in, out, div, nullptr, nullptr);
   else
-    KKT_LAUNCH(c, (time_stencil_kernel<false, false>), g, kThreads, 0, c->Ahat, nt, c->nsp, in, out, 1.0);
+    KKT_LAUNCH(c, (time_stencil_kernel<false, false>), g, kThreads, 0, c->Ahat, nt, c->nsp, in, out, 1.0, nullptr, nullptr);
 }
 
 void op_scale(Ctx* c, const double* in, double* out, double f, bool divide) {
@@ -146,20 +175,42 @@ void op_scale(Ctx* c, const double* in, double* out, double f, bool divide) {
     KKT_LAUNCH(c, scale_kernel<false>, g, kThreads, 0, c->B, in, out, f);
 }
 
+// K v on the rank's slab: u needs the plane of node n0-1 (from rank-1), w the
+// plane of node n0+ntl (from rank+1).
 void op_apply_K(Ctx* c, const double* v, double* out, const double* b_minus) {
-  KKT_LAUNCH(c, apply_K_kernel, grid_for(c->B), kThreads, 0, c->A, c->Nt, c->nsp, c->ms, c->oms,
-             c->dt, v, out, b_minus);
+  const double* u = v;
+  const double* w = v + 2 * c->B;
+  Halo h{nullptr, nullptr};
+  if (c->nranks > 1) {
+    const size_t nsp = c->nsp;
+    double* hp = c->halo.p;
+    double* hn = c->halo.p + nsp;
+    c->comm->halo(w, hn, u + size_t(c->ntl - 1) * nsp, hp, nsp, c->stream);
+    if (c->rank > 0) h.prev = hp;
+    if (c->rank + 1 < c->nranks) h.next = hn;
+  }
+  KKT_LAUNCH(c, apply_K_kernel, grid_for(c->B), kThreads, 0, c->A, c->ntl, c->nsp, c->ms, c->oms,
+             c->dt, v, out, b_minus, h.prev, h.next);
 }
 
 void op_pinv_uz(Ctx* c, const double* r, double* out) {
   KKT_LAUNCH(c, pinv_uz_kernel, grid_for(c->B), kThreads, 0, c->B, c->ms, c->oms, r, out);
 }
 
-// apply_shat (schur.cpp:71-78): t = Jhat^T v; t /= ms; out = Jhat t.
+// apply_shat (schur.cpp:71-78): t = Jhat^T v; t /= ms; out = Jhat t.  On a
+// slab, t at node n0-1 is recomputed from the received v plane so the lower
+// pass has its coupling term.
 void op_shat(Ctx* c, const double* v, double* out, double* tmp) {
   const int g = grid_for(c->B);
-  KKT_LAUNCH(c, (time_stencil_kernel<false, true>), g, kThreads, 0, c->Ahat, c->Nt, c->nsp, v, tmp, c->ms);
-  KKT_LAUNCH(c, (time_stencil_kernel<true, false>), g, kThreads, 0, c->Ahat, c->Nt, c->nsp, tmp, out, 1.0);
+  const Halo hv = exchange_halo(c, v, 0, 1, true, true);
+  KKT_LAUNCH(c, (time_stencil_kernel<false, true>), g, kThreads, 0, c->Ahat, c->ntl, c->nsp, v, tmp, c->ms, nullptr, hv.next);
+  const double* tprev = nullptr;
+  if (hv.prev) {
+    double* tp = c->halo.p + 2 * size_t(c->nsp);
+    KKT_LAUNCH(c, (time_stencil_kernel<false, true>), grid_for(c->nsp), kThreads, 0, c->Ahat, 1, c->nsp, hv.prev, tp, c->ms, nullptr, v);
+    tprev = tp;
+  }
+  KKT_LAUNCH(c, (time_stencil_kernel<true, false>), g, kThreads, 0, c->Ahat, c->ntl, c->nsp, tmp, out, 1.0, tprev, nullptr);
 }
 
 }  // namespace kkt

@@ -77,12 +77,19 @@ void window_solve(Ctx* c, double* b, int len, bool adjoint) {
 
 // out = RASQ(r) (one-level), or in fast mode with `fused_coarse`:
 // out = RASQ(r - Shat y_c) + y_c with y_c = gamma (c->gam) per node.
+// On a time slab the chains are this rank's subdomains s0 .. s0+ndl-1 and
+// plane(n) addresses global node n in the local slab; the first local
+// subdomain's shared node (n0-1, owned by the previous rank) arrives as a halo.
 void rasq_apply(Ctx* c, const double* r, double* out, bool fused_coarse) {
   const int64_t nsp = c->nsp;
-  const int Nd = c->Nd, m = c->m;
+  const int Nd = c->ndl, m = c->m;
   const int nsteps = 2 * m + 1;
-  auto plane = [&](const double* base, int n) { return base + (n - 1) * nsp; };
-  auto wplane = [&](double* base, int n) { return base + (n - 1) * nsp; };
+  const Halo hr = exchange_halo(c, r, 3, 3, true, false);
+  auto plane = [&](const double* base, int n) {
+    if (n == c->n0 - 1 && base == r) return hr.prev;  // shared node of the first local subdomain
+    return base + (n - c->n0) * nsp;
+  };
+  auto wplane = [&](double* base, int n) { return base + (n - c->n0) * nsp; };
   if (c->mode == KKT_MODE_STRICT || !c->has_fast()) {
     // scratch: one plane per subdomain for the shared node's forward value
     const size_t need = size_t(Nd) * nsp;
@@ -90,9 +97,10 @@ void rasq_apply(Ctx* c, const double* r, double* out, bool fused_coarse) {
     // out starts at zero (the reference accumulates into layout.zeros())
     KKT_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * c->B, c->stream));
     std::vector<SolveStep> jobs(size_t(Nd) * nsteps, SolveStep{nullptr, nullptr, nullptr, 1.0, 0});
-    for (int s = 0; s < Nd; ++s) {
-      double* shared = c->tmpB3.p + s * nsp;
-      SolveStep* J = jobs.data() + size_t(s) * nsteps;
+    for (int sl = 0; sl < Nd; ++sl) {
+      const int s = c->s0 + sl;
+      double* shared = c->tmpB3.p + sl * nsp;
+      SolveStep* J = jobs.data() + size_t(sl) * nsteps;
       const int first = s == 0 ? 1 : s * m;
       // forward over first..last
       for (int t = 0; t <= m; ++t) {
@@ -117,10 +125,11 @@ void rasq_apply(Ctx* c, const double* r, double* out, bool fused_coarse) {
   const size_t need = size_t(Nd) * 3 * nsp;
   if (c->tmpB3.n < need) c->tmpB3.alloc(need);
   std::vector<FastStep> jobs(size_t(Nd) * nsteps, FastStep{nullptr, nullptr, nullptr, nullptr, 1.0, 0, 0});
-  for (int s = 0; s < Nd; ++s) {
-    double* shared = c->tmpB3.p + (3 * s) * nsp;
-    double* adj[2] = {c->tmpB3.p + (3 * s + 1) * nsp, c->tmpB3.p + (3 * s + 2) * nsp};
-    FastStep* J = jobs.data() + size_t(s) * nsteps;
+  for (int sl = 0; sl < Nd; ++sl) {
+    const int s = c->s0 + sl;
+    double* shared = c->tmpB3.p + (3 * sl) * nsp;
+    double* adj[2] = {c->tmpB3.p + (3 * sl + 1) * nsp, c->tmpB3.p + (3 * sl + 2) * nsp};
+    FastStep* J = jobs.data() + size_t(sl) * nsteps;
     const int first = s == 0 ? 1 : s * m;
     for (int t = 0; t <= m; ++t) {
       const int n = s * m + t;

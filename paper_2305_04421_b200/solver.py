@@ -74,6 +74,32 @@ def lib():
     return _lib
 
 
+class LocalGroup:
+    """In-process rank group (kkt_local_group_create): the ranks are host threads
+    of this process sharing one device; exchanges are host-synchronised."""
+
+    def __init__(self, nranks: int):
+        h = _P()
+        st = lib().kkt_local_group_create(C.c_int32(nranks), C.byref(h))
+        if st != 0:
+            raise RuntimeError("kkt_local_group_create failed")
+        self.handle = h
+        self.nranks = nranks
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib().kkt_local_group_destroy(self.handle)
+            self.handle = None
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = lib().kkt_nccl_unique_id(buf)
+    if st != 0:
+        _raise(st, lib().kkt_create_error().decode(), -1)
+    return buf.raw
+
+
 def exported_symbols():
     """Names declared in include/kktdd_b200.h (for the load/export test)."""
     import re
@@ -110,7 +136,9 @@ class GmresOutcome:
 class HeatKKT:
     """Device context: HeatOperators + TimePartition + SchurSolver on one GPU."""
 
-    def __init__(self, problem: Problem, mode: str = "fast", device: int = 0, stream=None):
+    def __init__(self, problem: Problem, mode: str = "fast", device: int = 0, stream=None,
+                 rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None,
+                 local_group=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("HeatKKT needs a CUDA device (no CPU fallback)")
@@ -126,18 +154,33 @@ class HeatKKT:
             # stream order without host synchronisation
             stream = torch.cuda.Stream(device=self.device)
         self.stream = stream
+        self._nccl_id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         opts = RuntimeOpts(mode=_abi.MODE_STRICT if mode == "strict" else _abi.MODE_FAST,
-                           device=device, rank=0, nranks=1, nccl_unique_id=None,
-                           stream=C.c_void_p(stream.cuda_stream))
+                           device=device, rank=rank, nranks=nranks,
+                           nccl_unique_id=C.cast(self._nccl_id, C.c_void_p) if self._nccl_id else None,
+                           stream=C.c_void_p(stream.cuda_stream),
+                           local_group=local_group.handle if local_group is not None else None)
+        self.rank, self.nranks = rank, nranks
         h = _P()
         st = L.kkt_ctx_create(C.byref(self._desc), C.byref(opts), C.byref(h))
         if st != 0:
             _raise(st, L.kkt_create_error().decode(), -1)
         self._h = h
-        blk, nsp = C.c_int64(), C.c_int32()
-        L.kkt_layout(h, C.byref(blk), C.byref(nsp), None, None, None)
-        self.block = blk.value
+        blk, nsp, nf, nl, lb = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
+        L.kkt_layout(h, C.byref(blk), C.byref(nsp), C.byref(nf), C.byref(nl), C.byref(lb))
+        self.global_block = blk.value
+        self.block = lb.value          # rank-local block: vectors are local slabs
         self.n_sp = nsp.value
+        self.node_first, self.node_last = nf.value, nl.value
+
+    def local_slab(self, v):
+        """This rank's slab [u; z; w] (or one block) of a global vector."""
+        v = np.asarray(v)
+        G, L, off = self.global_block, self.block, (self.node_first - 1) * self.n_sp
+        if v.size == 3 * G:
+            return np.concatenate([v[k * G + off:k * G + off + L] for k in range(3)])
+        assert v.size == G
+        return v[off:off + L].copy()
 
     # -- plumbing ----------------------------------------------------------
     def close(self):

@@ -258,3 +258,34 @@ def test_e2e_host_matches_device():
     h = k.gmres_solve_host(b)
     assert h.iterations == d.iterations
     assert np.array_equal(h.solution, host(d.solution))
+
+
+def test_config1_against_golden():
+    """BASELINE config 1 (127^2 x 512, Nd=16): the reference's own solve (40 min on
+    one core, tests/golden/solve_c1_*) vs the device.  STRICT: same 44 iterations,
+    identical history and sha256-identical u, z, w.  FAST: iterations +-1 and the
+    strided sample of the solution within 1e-10 relative L2 per block."""
+    path = os.path.join(GOLD, "solve_c1_two-level_scalar.json")
+    if not os.path.exists(path):
+        pytest.skip("config-1 golden not generated")
+    gold = json.load(open(path))
+    samp = np.load(os.path.join(GOLD, "solve_c1_two-level_scalar_sample.npz"))
+    p = P.config(1)
+    b = P.kkt_rhs(1, p)
+    assert _sha(b) == gold["b_sha256"]
+    B = p.block
+    f = _kkt(p, "fast").gmres_solve(b)
+    assert abs(f.iterations - gold["iterations"]) <= 1
+    xf = host(f.solution)
+    idx, xs = samp["idx"], samp["x"]
+    for k in range(3):
+        sel = (idx >= k * B) & (idx < (k + 1) * B)
+        assert rel(xf[idx[sel]], xs[sel]) <= 1e-10, "uzw"[k]
+    for k, name in enumerate("uzw"):
+        assert abs(np.linalg.norm(xf[k * B:(k + 1) * B]) - gold["norms"][name]) <= 1e-10 * gold["norms"][name]
+    s = _kkt(p, "strict").gmres_solve(b)
+    x = host(s.solution)
+    assert s.iterations == gold["iterations"]
+    assert list(s.residual_history) == gold["history"]
+    for k, name in enumerate("uzw"):
+        assert _sha(x[k * B:(k + 1) * B]) == gold["sha256"][name], name
