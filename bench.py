@@ -10,8 +10,11 @@ the C-ABI (kkt_gmres_solve).  value = N * 3*Nt*n_sp / (max-over-ranks device
 time per solve).  e2e repeats the solve through kkt_gmres_solve_host with b
 and x in pinned host memory (copies inside the timed region).
 
-N > 1 runs one independent solve per GPU (weak scaling, replicas): the
-time-slab sharded path is not wired into this build yet.
+N > 1 shards the SAME config-1 solve over N GPUs by time slabs (strong
+scaling): rank g owns subdomains [g*Nd/N, (g+1)*Nd/N) and its
+node slab; halo planes, the coarse all-gather and the Krylov dot all-gathers go
+through NCCL (one communicator built by the library from a unique id that
+rank 0 broadcasts).  value = 3*Nt*n_sp / (max over ranks of the solve time).
 
 --impl reference times the UNMODIFIED reference (oracle/_ref, compiled from
 /root/reference by oracle/Makefile) on the host CPU: each step is a bounded
@@ -57,13 +60,14 @@ def workload_desc(cfg, p):
             f"GMRES({p.restart}) rtol {p.tol}")
 
 
-def sweep_bytes(p):
-    """Algorithmic bytes of one RASQ sweep:
-    (2Nt + Nd - 1) * 5 planes * n_sp * 8  +  (2m+1) * F,  F = 8 n_sp (2 nx + 1)."""
+def sweep_bytes(p, ranks=1):
+    """Algorithmic bytes of one RASQ sweep per GPU:
+    (2Nt + Nd - 1) * 5 planes * n_sp * 8 / G  +  (2m+1) * F,  F = 8 n_sp (2 nx + 1)
+    (the plane traffic splits over the G slabs; every GPU streams the factor)."""
     m = p.Nt // p.Nd
     planes = (2 * p.Nt + p.Nd - 1) * 5 * p.n_sp * 8
     F = 8 * p.n_sp * (2 * p.nx_int + 1)
-    return planes + (2 * m + 1) * F
+    return planes // ranks + (2 * m + 1) * F
 
 
 class ClockSampler:
@@ -205,7 +209,7 @@ def run_reference_arm(args, ws, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SplitMix64 + Box-Muller, paper_2305_04421_b200/problems.py)",
         "config": {"workload": workload_desc(args.config, p), "iterations": iters,
                    "iterations_source": src},
@@ -219,6 +223,19 @@ def run_reference_arm(args, ws, rank):
 # ---------------------------------------------------------------------------
 # the device arm
 # ---------------------------------------------------------------------------
+def rank_rhs(cfg, p, k):
+    """This rank's slab of b = [f_u; f_z; f] (kkt.cpp:21-48), generated only for
+    the local nodes (the generator is counter-based, so slabs agree with the
+    full field)."""
+    nf, nl = k.node_first, k.node_last
+    tgt, u0 = P.target_and_u0(cfg, p, n_lo=nf, n_hi=nl)
+    L = (nl - nf + 1) * p.n_sp
+    b = np.zeros(3 * L)
+    b[:L] = (p.mass_scale * tgt).reshape(-1)
+    if nf == 1:
+        b[2 * L: 2 * L + p.n_sp] = u0
+    return b
+
 def run_ours(args, ws, rank, local):
     import torch
     from paper_2305_04421_b200.solver import HeatKKT
@@ -226,10 +243,17 @@ def run_ours(args, ws, rank, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     p = P.config(args.config)
-    b_host = P.kkt_rhs(args.config, p)
-    n = b_host.size
     unknowns = 3 * p.Nt * p.n_sp
-    k = HeatKKT(p, mode=args.mode, device=local)
+    nccl_id = None
+    if ws > 1:
+        import torch.distributed as dist
+        from paper_2305_04421_b200.solver import nccl_unique_id
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    k = HeatKKT(p, mode=args.mode, device=local, rank=rank, nranks=ws, nccl_id=nccl_id)
+    b_host = rank_rhs(args.config, p, k)
+    n = b_host.size
     b = torch.from_numpy(b_host).to(dev)
     x = torch.empty_like(b)
 
@@ -283,7 +307,7 @@ def run_ours(args, ws, rank, local):
     # ---- roofline of the dominant kernel (the RASQ sweep, K5)
     peak, peak_src = hbm_peak()
     sweep_ms = phase_ms[3] / max(1, phase_cnt[3])
-    achieved = sweep_bytes(p) / (sweep_ms / 1000.0) / 1e9
+    achieved = sweep_bytes(p, ws) / (sweep_ms / 1000.0) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
@@ -296,24 +320,25 @@ def run_ours(args, ws, rank, local):
         return
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SplitMix64 + Box-Muller target, paper_2305_04421_b200/problems.py)",
         "config": {
             "workload": workload_desc(args.config, p), "mode": args.mode,
             "iterations": iters[-1], "iterations_all": sorted(set(iters)),
             "true_final_relres": out.true_final_relres,
-            "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+            "parallelism": (f"time slabs x{ws} (Nd/{ws} subdomains per GPU, NCCL halos + all-gathers)"
+                            if ws > 1 else "1 GPU"),
             "l2": "KKT vectors are 198 MB each (> 126 MB L2); no flush between solves",
             "phase_ms_per_step": {"K": phase_ms[0] / args.steps, "P_inv": phase_ms[1] / args.steps,
                                   "krylov_vectors": phase_ms[2] / args.steps,
                                   "sweep_kernel": phase_ms[3] / args.steps},
         },
         "roofline": {
-            "kernel": "fast_chain_kernel (RASQ sweep, K5)", "bound": "hbm",
+            "kernel": "RASQ sweep K5 (grpA/grpB/grpC kernels, sweep_group.cu)", "bound": "hbm",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": sweep_bytes(p), "avg_launch_ms": sweep_ms,
+            "algorithmic_bytes_per_launch": sweep_bytes(p, ws), "avg_launch_ms": sweep_ms,
             "launches": phase_cnt[3],
             "share_of_step": phase_ms[3] / max(1e-9, ms_total),
         },

@@ -17,6 +17,7 @@
 //  * FAST dots are deterministic two-level tree reductions (fixed grid,
 //    per-CTA partials, last CTA sums the partials in index order).
 #include <cmath>
+#include <cstdint>
 #include <vector>
 
 #include "ctx.cuh"
@@ -138,6 +139,91 @@ __device__ __forceinline__ double produce_fast(const DotArgs& A, double alpha, i
   }
 }
 
+// Fast, vectorised: 16-byte loads, 4 pairs per thread in flight.  Partials
+// of a fixed grid are combined by the last CTA in index order.
+__device__ __forceinline__ double2 ld2(const double* p, int64_t i) {
+  return reinterpret_cast<const double2*>(p)[i];
+}
+__device__ __forceinline__ void st2(double* p, int64_t i, double2 v) {
+  reinterpret_cast<double2*>(p)[i] = v;
+}
+
+template <int kOp>
+__device__ __forceinline__ double produce_pair(const DotArgs& A, double alpha, int64_t i, bool& bad) {
+  if (kOp == kDotPlain) {
+    const double2 a = ld2(A.w, i), b = ld2(A.b, i);
+    if (A.flag && !(isfinite(a.x) && isfinite(a.y))) bad = true;
+    return fma(a.x, b.x, a.y * b.y);
+  } else if (kOp == kDotAxpy) {
+    double2 w = ld2(A.w, i);
+    const double2 v = ld2(A.v, i), b = ld2(A.b, i);
+    w.x = fma(alpha, v.x, w.x);
+    w.y = fma(alpha, v.y, w.y);
+    st2(A.w, i, w);
+    return fma(w.x, b.x, w.y * b.y);
+  } else if (kOp == kDotAxpySelf) {
+    double2 w = ld2(A.w, i);
+    const double2 v = ld2(A.v, i);
+    w.x = fma(alpha, v.x, w.x);
+    w.y = fma(alpha, v.y, w.y);
+    st2(A.w, i, w);
+    return fma(w.x, w.x, w.y * w.y);
+  } else {
+    const double2 a = ld2(A.w, i), b = ld2(A.b, i);
+    const double dx = a.x - b.x, dy = a.y - b.y;
+    return fma(dx, dx, dy * dy);
+  }
+}
+
+template <int kOp>
+__global__ void __launch_bounds__(256) dot_vec_kernel(DotArgs A, double* partial, unsigned* counter) {
+  __shared__ double wsum[8];
+  __shared__ bool is_last;
+  const double alpha = A.hsrc ? -(*A.hsrc) : 0.0;
+  bool bad = false;
+  double acc0 = 0.0, acc1 = 0.0;
+  const int64_t npair = A.n >> 1;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  for (; i + 3 * stride < npair; i += 4 * stride) {
+    const double p0 = produce_pair<kOp>(A, alpha, i, bad);
+    const double p1 = produce_pair<kOp>(A, alpha, i + stride, bad);
+    const double p2 = produce_pair<kOp>(A, alpha, i + 2 * stride, bad);
+    const double p3 = produce_pair<kOp>(A, alpha, i + 3 * stride, bad);
+    acc0 += p0 + p1;
+    acc1 += p2 + p3;
+  }
+  for (; i < npair; i += stride) acc0 += produce_pair<kOp>(A, alpha, i, bad);
+  if ((A.n & 1) && blockIdx.x == 0 && threadIdx.x == 0) acc0 += produce_fast(A, alpha, A.n - 1, bad);
+  double acc = acc0 + acc1;
+  if (bad) *A.flag = 1;
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += wsum[w];
+    partial[blockIdx.x] = s;
+    __threadfence();
+    is_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    double s = 0.0;
+    for (int j = threadIdx.x; j < (int)gridDim.x; j += blockDim.x) s += ((volatile double*)partial)[j];
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += wsum[w];
+      *A.dst = t;
+      *counter = 0;
+    }
+  }
+}
+
 // Fast: fixed-shape tree; the last CTA to finish reduces the partials in
 // index order, so the result is deterministic run to run.
 __global__ void __launch_bounds__(kTreeThreads) dot_tree_kernel(DotArgs A, double* partial,
@@ -245,10 +331,20 @@ void ensure_reduction(Ctx* c) {
 
 void launch_dot(Ctx* c, const DotArgs& A) {
   ensure_reduction(c);
-  if (c->mode == KKT_MODE_STRICT)
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool vec = aligned(A.w) && (!A.v || aligned(A.v)) && (!A.b || aligned(A.b));
+  if (c->mode == KKT_MODE_STRICT) {
     KKT_LAUNCH(c, dot_seq_kernel, 1, kSeqThreads, 0, A);
-  else
+  } else if (vec) {
+    switch (A.op) {
+      case kDotPlain: KKT_LAUNCH(c, dot_vec_kernel<kDotPlain>, kTreeBlocks, 256, 0, A, c->red.p, c->red_count.p); break;
+      case kDotAxpy: KKT_LAUNCH(c, dot_vec_kernel<kDotAxpy>, kTreeBlocks, 256, 0, A, c->red.p, c->red_count.p); break;
+      case kDotAxpySelf: KKT_LAUNCH(c, dot_vec_kernel<kDotAxpySelf>, kTreeBlocks, 256, 0, A, c->red.p, c->red_count.p); break;
+      default: KKT_LAUNCH(c, dot_vec_kernel<kDotDiff>, kTreeBlocks, 256, 0, A, c->red.p, c->red_count.p); break;
+    }
+  } else {
     KKT_LAUNCH(c, dot_tree_kernel, kTreeBlocks, kTreeThreads, 0, A, c->red.p, c->red_count.p);
+  }
   if (c->nranks > 1) {
     // the Krylov global reduction: all-gather one partial per rank, sum in rank order
     if (c->red_all.n < size_t(c->nranks)) c->red_all.alloc(c->nranks);

@@ -104,7 +104,9 @@ def test_sharded_gmres_matches_single_rank(p, G, single):
     res = run_ranks(p, G, fn)
     for r, (it, xs, want, relres, hist) in enumerate(res):
         assert abs(it - ref.iterations) <= 1, (r, it, ref.iterations)
-        assert np.linalg.norm(xs - want) <= 1e-10 * np.linalg.norm(want), r
+        # two iterates meeting the stopping test differ by about the attained residual
+        tol = max(1e-10, 10 * ref.true_final_relres)
+        assert np.linalg.norm(xs - want) <= tol * np.linalg.norm(want), r
         assert hist == res[0][4]  # every rank runs the same scalar recurrence
     assert abs(res[0][3] - ref.true_final_relres) <= 1e-3 * ref.true_final_relres + 1e-14
 
