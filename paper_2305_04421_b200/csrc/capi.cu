@@ -16,6 +16,8 @@ namespace kkt {
 Ctx::~Ctx() {
   if (stream) cudaStreamSynchronize(stream);
   delete comm;
+  for (auto& g : graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   basis.clear();
   for (auto e : ev_pool) cudaEventDestroy(e);
   for (auto& iv : ev_pending) { cudaEventDestroy(iv.a); cudaEventDestroy(iv.b); }

@@ -97,6 +97,15 @@ struct Ctx {
   int grp_g = 0, grp_n = 0;
   DBuf<double> grp_y, grp_x, grp_e, grp_f;
   DBuf<double> grp_tl, grp_tu;     // products of group-boundary propagators
+  struct Graph {                   // captured sweep launch sequences (sweep_group.cu)
+    const void* jobs = nullptr;
+    const void* y = nullptr;
+    int nchains = 0, nsteps = 0;
+    bool coarse = false;
+    int64_t nlaunch = 0;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<Graph> graphs;
 
   // ---- coarse space (scalar variant)
   bool has_coarse = false;

@@ -24,6 +24,7 @@
 // group-boundary propagators, so per spatial solve there are 6 launches
 // (A/B/C for L and U) and the dependent depth per sweep drops from ny block
 // steps to g steps + 2 parallel GEMM-like phases, with ~NG*Nd SMs at work.
+#include <cstdlib>
 #include <vector>
 
 #include "sweep_tma.cuh"
@@ -279,21 +280,21 @@ __global__ void __launch_bounds__(kThreads, 1) grpC_kernel(GrpParams P, const Fa
                                                           int nsteps, int t) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar;
+  __shared__ double* s_out[kCBatch];
+  __shared__ double* s_out2[kCBatch];
+  __shared__ double s_g2[kCBatch];
+  __shared__ int s_act[kCBatch];
   const int J = blockIdx.x;
   const int grp = J / P.g;
   const bool has_inflow = kUpper ? (grp < P.NG - 1) : (grp > 0);
   if (!kUpper && !has_inflow) return;  // ytilde is already y in the first group
   const int nx = P.nx, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* Mj = sm;                       // kDense
-  double* In = sm + kDense;              // kCBatch x kLd
-  if (has_inflow) {
-    if (tid == 0) {
-      mbar_init(&bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    if (tid == 0)
-      tma_load(Mj, (kUpper ? P.Psi : P.Phi) + int64_t(J) * kDense, uint32_t(kDense) * 8u, &bar);
+  double* In = sm + kDense;              // kCBatch x kLd   (operand, then the product)
+  if (has_inflow && tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tma_load(Mj, (kUpper ? P.Psi : P.Phi) + int64_t(J) * kDense, uint32_t(kDense) * 8u, &bar);
   }
   const int src_grp = kUpper ? grp + 1 : grp - 1;
   const double* til = kUpper ? P.Xtil : P.Ytil;
@@ -301,27 +302,38 @@ __global__ void __launch_bounds__(kThreads, 1) grpC_kernel(GrpParams P, const Fa
   bool waited = false;
   for (int s0 = 0; s0 < P.Nd; s0 += kCBatch) {
     const int nb = min(kCBatch, P.Nd - s0);
+    if (tid < kCBatch) {
+      const int s = s0 + tid;
+      int act = 0;
+      double* o = nullptr;
+      double* o2 = nullptr;
+      double g2 = 0.0;
+      if (tid < nb) {
+        const FastStep st = steps[int64_t(s) * nsteps + t];
+        act = st.in != nullptr;
+        o = st.out;
+        o2 = st.out2;
+        g2 = (st.out2 && st.node2 > 0 && P.gam) ? P.gam[st.node2] : 0.0;
+      }
+      s_act[tid] = act;
+      s_out[tid] = o;
+      s_out2[tid] = o2;
+      s_g2[tid] = g2;
+    }
+    __syncthreads();
     if (has_inflow) {
       for (int i = tid; i < kCBatch * kLd; i += blockDim.x) {
         const int c = i / kLd, b = i - c * kLd;
-        const int s = s0 + c;
-        double v = 0.0;
-        if (c < nb && b < nx && steps[int64_t(s) * nsteps + t].in)
-          v = bv[(int64_t(s) * P.NG + src_grp) * kMaxNx + b];
-        In[i] = v;
+        In[i] = (c < nb && b < nx && s_act[c]) ? bv[(int64_t(s0 + c) * P.NG + src_grp) * kMaxNx + b] : 0.0;
       }
       if (!waited) {
         mbar_wait(&bar, 0);
         waited = true;
       }
       __syncthreads();
-    }
-    // 16 row tiles (8 rows) x 2 chain tiles (8 chains): warp w -> row tile w,
-    // both chain tiles; K = 128 in 32 steps of 4
-    const int mt = warp;  // kWarps == 16 row tiles of 8 rows = 128 rows
-    double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
-    if (has_inflow) {
-      const int ar = mt * 8 + (lane >> 2);
+      // 16 row tiles x 2 chain tiles: warp w -> row tile w; K = 128 in 32 steps of 4
+      double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+      const int ar = warp * 8 + (lane >> 2);
       const int kc = lane & 3;
 #pragma unroll 8
       for (int ks = 0; ks < kLd / 4; ++ks) {
@@ -331,26 +343,28 @@ __global__ void __launch_bounds__(kThreads, 1) grpC_kernel(GrpParams P, const Fa
         dmma(d00, d01, a, b0);
         dmma(d10, d11, a, b1);
       }
+      __syncthreads();  // In is overwritten with the product below
+      // D fragment: row = 8w + lane/4, chain = 2*(lane%4) + {0,1} (+8 for tile 1)
+      const int c0 = 2 * (lane & 3);
+      In[c0 * kLd + ar] = d00;
+      In[(c0 + 1) * kLd + ar] = d01;
+      In[(8 + c0) * kLd + ar] = d10;
+      In[(9 + c0) * kLd + ar] = d11;
+      __syncthreads();
     }
-    // D fragment: row = mt*8 + lane/4, chain col = 2*(lane%4) + {0,1} (+8 for tile 1)
-    const int a = mt * 8 + (lane >> 2);
-    if (a < nx) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = (q >> 1) * 8 + 2 * (lane & 3) + (q & 1);
-        const double d = q == 0 ? d00 : q == 1 ? d01 : q == 2 ? d10 : d11;
-        const int s = s0 + c;
-        if (c >= nb) continue;
-        const FastStep st = steps[int64_t(s) * nsteps + t];
-        if (!st.in) continue;
-        const int64_t p = int64_t(J) * nx + a;
-        if (!kUpper) {
-          P.Ytil[int64_t(s) * P.nsp + p] += d;
-        } else {
-          const double x = til[int64_t(s) * P.nsp + p] + d;
-          if (st.out) st.out[p] = x;
-          if (st.out2) st.out2[p] = x + ((st.node2 > 0 && P.gam) ? P.gam[st.node2] : 0.0);
-        }
+    // coalesced row updates: chain c, rows a
+    for (int i = tid; i < nb * nx; i += blockDim.x) {
+      const int c = i / nx, a = i - c * nx;
+      if (!s_act[c]) continue;
+      const int s = s0 + c;
+      const int64_t p = int64_t(J) * nx + a;
+      const double d = has_inflow ? In[c * kLd + a] : 0.0;
+      if (!kUpper) {
+        P.Ytil[int64_t(s) * P.nsp + p] += d;
+      } else {
+        const double x = til[int64_t(s) * P.nsp + p] + d;
+        if (s_out[c]) s_out[c][p] = x;
+        if (s_out2[c]) s_out2[c][p] = x + s_g2[c];
       }
     }
     __syncthreads();
@@ -587,15 +601,53 @@ void group_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, boo
   }
   const dim3 gA(c->grp_n, nchains);
   const size_t sA = smemA(c), sC = smemC();
-  c->tbegin(3);
-  for (int t = 0; t < nsteps; ++t) {
-    KKT_LAUNCH(c, grpA_L_kernel, gA, kThreads, sA, P, jobs_dev, nsteps, t, coarse_terms);
-    KKT_LAUNCH(c, grpB_kernel<false>, gA, kThreads, 0, P, jobs_dev, nsteps, t);
-    KKT_LAUNCH(c, grpC_kernel<false>, c->ny, kThreads, sC, P, jobs_dev, nsteps, t);
-    KKT_LAUNCH(c, grpA_U_kernel, gA, kThreads, sA, P, jobs_dev, nsteps, t);
-    KKT_LAUNCH(c, grpB_kernel<true>, gA, kThreads, 0, P, jobs_dev, nsteps, t);
-    KKT_LAUNCH(c, grpC_kernel<true>, c->ny, kThreads, sC, P, jobs_dev, nsteps, t);
+  auto sequence = [&]() {
+    for (int t = 0; t < nsteps; ++t) {
+      KKT_LAUNCH(c, grpA_L_kernel, gA, kThreads, sA, P, jobs_dev, nsteps, t, coarse_terms);
+      KKT_LAUNCH(c, grpB_kernel<false>, gA, kThreads, 0, P, jobs_dev, nsteps, t);
+      KKT_LAUNCH(c, grpC_kernel<false>, c->ny, kThreads, sC, P, jobs_dev, nsteps, t);
+      KKT_LAUNCH(c, grpA_U_kernel, gA, kThreads, sA, P, jobs_dev, nsteps, t);
+      KKT_LAUNCH(c, grpB_kernel<true>, gA, kThreads, 0, P, jobs_dev, nsteps, t);
+      KKT_LAUNCH(c, grpC_kernel<true>, c->ny, kThreads, sC, P, jobs_dev, nsteps, t);
+    }
+  };
+  // The 6*nsteps launches of one application are replayed from a CUDA graph:
+  // the job table is a fixed device buffer refreshed before each replay, so
+  // the captured kernel arguments stay valid.
+  static const bool no_graph = getenv("KKT_NO_GRAPH") != nullptr;
+  if (no_graph) {
+    c->tbegin(3);
+    sequence();
+    c->tend(3);
+    return;
   }
+  Ctx::Graph* gr = nullptr;
+  for (auto& e : c->graphs)
+    if (e.jobs == jobs_dev && e.nchains == nchains && e.nsteps == nsteps && e.coarse == coarse_terms &&
+        e.y == c->grp_y.p)
+      gr = &e;
+  if (!gr) {
+    Ctx::Graph e;
+    e.jobs = jobs_dev;
+    e.nchains = nchains;
+    e.nsteps = nsteps;
+    e.coarse = coarse_terms;
+    e.y = c->grp_y.p;
+    const int64_t l0 = c->launches;
+    cudaGraph_t graph;
+    KKT_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    sequence();
+    KKT_CUDA(cudaStreamEndCapture(c->stream, &graph));
+    KKT_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
+    KKT_CUDA(cudaGraphDestroy(graph));
+    e.nlaunch = c->launches - l0;
+    c->launches = l0;
+    c->graphs.push_back(e);
+    gr = &c->graphs.back();
+  }
+  c->tbegin(3);
+  KKT_CUDA(cudaGraphLaunch(gr->exec, c->stream));
+  c->launches += gr->nlaunch;
   c->tend(3);
 }
 
