@@ -6,6 +6,7 @@
 // reference's expressions, Ahat factorisation), build_time_partition
 // (time_partition.cpp:61-86) and make_schur_solver (schur.cpp:543-558).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -165,9 +166,16 @@ void setup(Ctx* c, const kkt_problem_desc& d, const kkt_runtime_opts* o) {
     c->owned.push_back({s == 0 ? 1 : s * c->m + 1, last});
   }
 
-  // ---- factor + preconditioner setup
-  build_factor(c);
-  if (c->mode == KKT_MODE_FAST) build_block_inverses(c);
+  // ---- factor + preconditioner setup: the reference's banded LU (bitwise) for
+  // STRICT mode and small grids; the block recursion for FAST mode on large
+  // grids (nx > 128), where the band's rank-1 updates do not scale
+  static const bool force_rec = getenv("KKT_FORCE_BLOCK_RECURSION") != nullptr;  // testing
+  if (c->mode == KKT_MODE_FAST && (c->nx > 128 || force_rec)) {
+    build_block_recursion(c);
+  } else {
+    build_factor(c);
+    if (c->mode == KKT_MODE_FAST) build_block_inverses(c);
+  }
   if (d.precond == KKT_PRECOND_TWO_LEVEL) build_coarse(c);
   KKT_CUDA(cudaStreamSynchronize(c->stream));
 }

@@ -170,6 +170,7 @@ struct Ctx {
 // ---- builders (ctx.cu / factor.cu / coarse.cu)
 void build_factor(Ctx* c);
 void build_block_inverses(Ctx* c);
+void build_block_recursion(Ctx* c);
 void build_coarse(Ctx* c);
 
 // ---- operators (stencil.cu)

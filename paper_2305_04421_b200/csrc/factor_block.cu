@@ -1,0 +1,155 @@
+// factor_block.cu — K6 for large grids (FAST mode, nx > 128: configs 2-4).
+//
+// The reference's banded LU (linalg.cpp:69-125) of Ahat is pivot-free on these
+// problems, and an unpivoted LU is unique, so its block form
+// can be computed by the block recursion on the nx-by-nx diagonal blocks
+//     D_0 = T,   D_J = T - cy^2 D_{J-1}^{-1},   D_J = L_JJ U_JJ,
+// with T = tridiag(-cx, diag(Ahat), -cx) and D_{J-1}^{-1} = Ui_{J-1} Li_{J-1}.
+// It produces the sweep operators Li_J = L_JJ^{-1}, Ui_J = U_JJ^{-1} directly
+// (the same factors as the banded LU up to rounding) with dense, L2-resident
+// work per block instead of ny*nx rank-1 updates over the whole band.
+// A pivot below 1e-14 ||Ahat||_inf (linalg.cpp:10,98-103) raises
+// SingularMatrixError with the global row index, as the banded LU would.
+#include <cmath>
+
+#include "ctx.cuh"
+
+namespace kkt {
+namespace {
+
+constexpr int kLuThreads = 1024;
+
+// D = T - cy^2 * S   (S == nullptr: D = T)
+__global__ void form_d_kernel(int n, double diag, double mcx, double cy2, const double* __restrict__ S,
+                              double* __restrict__ D) {
+  const int64_t nn = int64_t(n) * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nn;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int a = int(e / n), b = int(e - int64_t(a) * n);
+    double v = a == b ? diag : ((a - b == 1 || b - a == 1) ? mcx : 0.0);
+    if (S) v -= cy2 * S[e];
+    D[e] = v;
+  }
+}
+
+// Unpivoted right-looking LU in place, one CTA (the matrix is L2-resident).
+__global__ void __launch_bounds__(kLuThreads) dense_lu_nopiv_kernel(int n, double tol, double* A,
+                                                                    int* status) {
+  for (int j = 0; j < n; ++j) {
+    const double d = A[int64_t(j) * n + j];
+    if (!(fabs(d) > tol)) {
+      if (threadIdx.x == 0) *status = j;
+      return;
+    }
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) A[int64_t(i) * n + j] /= d;
+    __syncthreads();
+    const int rows = n - j - 1;
+    const int64_t pairs = int64_t(rows) * rows;
+    for (int64_t t = threadIdx.x; t < pairs; t += blockDim.x) {
+      const int i = j + 1 + int(t / rows);
+      const int c = j + 1 + int(t % rows);
+      A[int64_t(i) * n + c] = fma(-A[int64_t(i) * n + j], A[int64_t(j) * n + c], A[int64_t(i) * n + c]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *status = -1;
+}
+
+// Li = (unit lower of A)^{-1}, Ui = (upper of A)^{-1}; one thread per column,
+// columns spread over CTAs.
+__global__ void tri_inverse_kernel(int n, const double* __restrict__ A, double* __restrict__ Li,
+                                   double* __restrict__ Ui) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  for (int a = 0; a < n; ++a) {
+    double acc = (a == b) ? 1.0 : 0.0;
+    if (a > b)
+      for (int k = b; k < a; ++k) acc = fma(-A[int64_t(a) * n + k], Li[int64_t(k) * n + b], acc);
+    Li[int64_t(a) * n + b] = acc;
+  }
+  for (int a = n - 1; a >= 0; --a) {
+    double acc = 0.0;
+    if (a <= b) {
+      acc = (a == b) ? 1.0 : 0.0;
+      for (int k = a + 1; k <= b; ++k) acc = fma(-A[int64_t(a) * n + k], Ui[int64_t(k) * n + b], acc);
+      acc /= A[int64_t(a) * n + a];
+    }
+    Ui[int64_t(a) * n + b] = acc;
+  }
+}
+
+// C = A * B (n x n, row-major), 32x32 tiles through shared memory.
+__global__ void gemm_kernel(int n, const double* __restrict__ A, const double* __restrict__ B,
+                            double* __restrict__ C) {
+  __shared__ double As[32][33], Bs[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  const int row0 = blockIdx.y * 32, col = blockIdx.x * 32 + tx;
+  double acc[4] = {0, 0, 0, 0};
+  for (int k0 = 0; k0 < n; k0 += 32) {
+    for (int r = ty; r < 32; r += 8) {
+      const int ar = row0 + r, ac = k0 + tx;
+      As[r][tx] = (ar < n && ac < n) ? A[int64_t(ar) * n + ac] : 0.0;
+      const int br = k0 + r;
+      Bs[r][tx] = (br < n && col < n) ? B[int64_t(br) * n + col] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const double bv = Bs[k][tx];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(As[ty + 8 * q][k], bv, acc[q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = row0 + ty + 8 * q;
+    if (r < n && col < n) C[int64_t(r) * n + col] = acc[q];
+  }
+}
+
+}  // namespace
+
+void build_block_recursion(Ctx* c) {
+  const int nx = c->nx, ny = c->ny;
+  const int64_t nn = int64_t(nx) * nx;
+  // ||Ahat||_inf as in build_factor (linalg.cpp:35-43 order)
+  double anorm = 0.0;
+  for (int j = 1; j <= ny; ++j)
+    for (int i = 1; i <= nx; ++i) {
+      double row = 0.0;
+      if (j > 1) row += std::abs(c->Ahat.mcy);
+      if (i > 1) row += std::abs(c->Ahat.mcx);
+      row += std::abs(c->Ahat.diag);
+      if (i < nx) row += std::abs(c->Ahat.mcx);
+      if (j < ny) row += std::abs(c->Ahat.mcy);
+      anorm = std::max(anorm, row);
+    }
+  const double tol = 1e-14 * anorm;
+  c->Li.alloc(size_t(ny) * nn);
+  c->Ui.alloc(size_t(ny) * nn);
+  DBuf<double> D(nn), S(nn);
+  DBuf<int> st(1);
+  const double cy2 = c->cy * c->cy;
+  const dim3 gg((nx + 31) / 32, (nx + 31) / 32), gb(32, 8);
+  for (int J = 0; J < ny; ++J) {
+    KKT_LAUNCH(c, form_d_kernel, kSmCount * 2, 256, 0, nx, c->Ahat.diag, c->Ahat.mcx, cy2,
+               J > 0 ? S.p : nullptr, D.p);
+    KKT_LAUNCH(c, dense_lu_nopiv_kernel, 1, kLuThreads, 0, nx, tol, D.p, st.p);
+    double* Li = c->Li.p + J * nn;
+    double* Ui = c->Ui.p + J * nn;
+    KKT_LAUNCH(c, tri_inverse_kernel, (nx + 127) / 128, 128, 0, nx, D.p, Li, Ui);
+    if (J + 1 < ny) KKT_LAUNCH(c, gemm_kernel, gg, gb, 0, nx, Ui, Li, S.p);
+    int hs = -1;
+    KKT_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+    if (hs >= 0)
+      throw Error(KKT_ESINGULAR,
+                  "block LU: pivot below tolerance " + std::to_string(tol) + " at index " +
+                      std::to_string(J * nx + hs),
+                  J * nx + hs);
+  }
+  c->pivoted = false;
+}
+
+}  // namespace kkt
