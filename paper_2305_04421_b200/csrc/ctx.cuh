@@ -21,6 +21,7 @@ template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool own = true;  // false: a view into another allocation (e.g. the L2-persisting arena)
   DBuf() = default;
   explicit DBuf(size_t count) { alloc(count); }
   void alloc(size_t count) {
@@ -28,17 +29,24 @@ struct DBuf {
     n = count;
     if (count) KKT_CUDA(cudaMalloc(&p, count * sizeof(T)));
   }
+  void view(T* q, size_t count) {
+    release();
+    p = q;
+    n = count;
+    own = false;
+  }
   void release() {
-    if (p) cudaFree(p);
+    if (p && own) cudaFree(p);
     p = nullptr;
     n = 0;
+    own = true;
   }
   ~DBuf() { release(); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), own(o.own) { o.p = nullptr; o.n = 0; }
   DBuf& operator=(DBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    if (this != &o) { release(); p = o.p; n = o.n; own = o.own; o.p = nullptr; o.n = 0; }
     return *this;
   }
 };
@@ -106,6 +114,7 @@ struct Ctx {
     cudaGraphExec_t exec = nullptr;
   };
   std::vector<Graph> graphs;
+  DBuf<double> arena;              // one allocation for the sweep operators (L2-persisting window)
 
   // ---- coarse space (scalar variant)
   bool has_coarse = false;
