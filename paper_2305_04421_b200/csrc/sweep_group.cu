@@ -222,6 +222,9 @@ __host__ __device__ inline int tri_index(int g, int i) { return g * (g - 1) / 2 
 template <bool kUpper>
 __global__ void __launch_bounds__(kThreads, 1) grpB_kernel(GrpParams P, const FastStep* steps,
                                                           int nsteps, int t) {
+  // let phase C launch now: its prologue (TMA of Phi_J / Psi_J) does not
+  // depend on this kernel and overlaps it (programmatic dependent launch)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   __shared__ double ov[kMaxNx];
   const int grp = blockIdx.x, s = blockIdx.y;
   const FastStep st = steps[int64_t(s) * nsteps + t];
@@ -296,6 +299,8 @@ __global__ void __launch_bounds__(kThreads, 1) grpC_kernel(GrpParams P, const Fa
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     tma_load(Mj, (kUpper ? P.Psi : P.Phi) + int64_t(J) * kDense, uint32_t(kDense) * 8u, &bar);
   }
+  // everything below reads phase B's outputs
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int src_grp = kUpper ? grp + 1 : grp - 1;
   const double* til = kUpper ? P.Xtil : P.Ytil;
   const double* bv = kUpper ? P.F : P.E;
@@ -461,6 +466,25 @@ size_t smemA(const Ctx* c) {
   return sizeof(double) * (size_t(kSlots) * c->Lpk_stride + size_t(5 + kWarps) * kMaxNx);
 }
 size_t smemC() { return sizeof(double) * (size_t(kDense) + size_t(kCBatch) * kLd); }
+
+// Launch with programmatic stream serialization: the kernel may start while
+// its predecessor runs and must call griddepcontrol.wait before reading it.
+template <class K>
+void launch_pdl(Ctx* c, K kernel, int grid, size_t smem, const GrpParams& P, const FastStep* jobs,
+                int nsteps, int t) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KKT_CUDA(cudaLaunchKernelEx(&cfg, kernel, P, jobs, nsteps, t));
+  c->launches++;
+}
 
 }  // namespace
 
@@ -640,10 +664,10 @@ void group_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, boo
     for (int t = 0; t < nsteps; ++t) {
       KKT_LAUNCH(c, grpA_L_kernel, gA, kThreads, sA, P, jobs_dev, nsteps, t, coarse_terms);
       KKT_LAUNCH(c, grpB_kernel<false>, gA, kThreads, 0, P, jobs_dev, nsteps, t);
-      KKT_LAUNCH(c, grpC_kernel<false>, c->ny, kThreads, sC, P, jobs_dev, nsteps, t);
+      launch_pdl(c, grpC_kernel<false>, c->ny, sC, P, jobs_dev, nsteps, t);
       KKT_LAUNCH(c, grpA_U_kernel, gA, kThreads, sA, P, jobs_dev, nsteps, t);
       KKT_LAUNCH(c, grpB_kernel<true>, gA, kThreads, 0, P, jobs_dev, nsteps, t);
-      KKT_LAUNCH(c, grpC_kernel<true>, c->ny, kThreads, sC, P, jobs_dev, nsteps, t);
+      launch_pdl(c, grpC_kernel<true>, c->ny, sC, P, jobs_dev, nsteps, t);
     }
   };
   // The 6*nsteps launches of one application are replayed from a CUDA graph:
