@@ -188,6 +188,10 @@ int kkt_phase_times(const kkt_ctx* ctx, double* ms4, int64_t* counts4);
  * (BandedLU::ab_, linalg.hpp:65-74; (kl + ku_ + 1) rows per column) and its
  * pivot vector to HOST buffers (either may be NULL). */
 int kkt_debug_ahat_factor(kkt_ctx* ctx, int32_t* kl, int32_t* ku, double* ab_host, int32_t* piv_host);
+/* Same for the per-dof coarse operator's banded LU (SparseLU -> BandedLU,
+ * linalg.cpp:312-331; entry (i,j) at j*(kl+ku+1) + i-j+ku with ku = the
+ * fill-extended upper bandwidth).  KKT_ECONFIG without a per-dof coarse space. */
+int kkt_debug_coarse_factor(kkt_ctx* ctx, int32_t* kl, int32_t* ku, double* ab_host, int32_t* piv_host);
 
 /* Multi-rank bring-up (time-slab sharding).  Rank g of G owns
  * subdomains [g*Nd/G, (g+1)*Nd/G) and their nodes; every vector argument is

@@ -401,6 +401,9 @@ int kkt_coarse_prolong_add(kkt_ctx* ctx, const double* cvec, double* out) {
 int kkt_coarse_matrix(kkt_ctx* ctx, double* host_out) {
   return kkt::guard(ctx, [&](Ctx* c) {
     kkt::need(c->has_coarse && host_out, "no coarse space");
+    if (c->h_S0.empty() || (c->cdim > 4096 && !std::getenv("KKT_KEEP_S0")))
+      throw kkt::Error(KKT_ECONFIG, "coarse_matrix_dense: dimension " + std::to_string(c->cdim) +
+                                        " exceeds the dense limit 4096");
     std::memcpy(host_out, c->h_S0.data(), sizeof(double) * c->h_S0.size());
   });
 }
@@ -463,9 +466,26 @@ int kkt_debug_ahat_factor(kkt_ctx* ctx, int32_t* kl, int32_t* ku, double* ab_hos
     if (kl) *kl = c->kl;
     if (ku) *ku = c->kuf;
     if (ab_host)
-      KKT_CUDA(cudaMemcpy(ab_host, c->ab.p, sizeof(double) * c->ab.n, cudaMemcpyDeviceToHost));
+      KKT_CUDA(cudaMemcpyAsync(ab_host, c->ab.p, sizeof(double) * c->ab.n, cudaMemcpyDeviceToHost, c->stream));
+      KKT_CUDA(cudaStreamSynchronize(c->stream));
     if (piv_host)
-      KKT_CUDA(cudaMemcpy(piv_host, c->piv.p, sizeof(int) * c->piv.n, cudaMemcpyDeviceToHost));
+      KKT_CUDA(cudaMemcpyAsync(piv_host, c->piv.p, sizeof(int) * c->piv.n, cudaMemcpyDeviceToHost, c->stream));
+      KKT_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int kkt_debug_coarse_factor(kkt_ctx* ctx, int32_t* kl, int32_t* ku, double* ab_host,
+                            int32_t* piv_host) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(c->has_coarse && c->perdof, "no per-dof coarse space");
+    if (kl) *kl = c->cb_kl;
+    if (ku) *ku = c->cb_kuf;
+    if (ab_host)
+      KKT_CUDA(cudaMemcpyAsync(ab_host, c->cb_ab.p, sizeof(double) * c->cb_ab.n, cudaMemcpyDeviceToHost, c->stream));
+      KKT_CUDA(cudaStreamSynchronize(c->stream));
+    if (piv_host)
+      KKT_CUDA(cudaMemcpyAsync(piv_host, c->cb_piv.p, sizeof(int) * c->cb_piv.n, cudaMemcpyDeviceToHost, c->stream));
+      KKT_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

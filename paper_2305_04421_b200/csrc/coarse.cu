@@ -311,8 +311,10 @@ void h2d(Ctx* c, DBuf<T>& d, const std::vector<T>& h) {
 // ---------------------------------------------------------------------------
 void build_coarse(Ctx* c) {
   const int Nd = c->Nd, nsp = c->nsp, Nt = c->Nt;
-  if (c->desc.coarse_variant != KKT_COARSE_SCALAR)
-    throw Error(KKT_EUNSUPPORTED, "per-dof coarse variant is not implemented on the device path");
+  if (c->desc.coarse_variant != KKT_COARSE_SCALAR) {
+    build_coarse_perdof(c);
+    return;
+  }
   c->phi_const.clear();
   c->phi_lin.clear();
   for (int s = 0; s < Nd; ++s) {
@@ -482,6 +484,7 @@ static const double* gather_all(Ctx* c, double* local) {
 }
 
 void coarse_restrict(Ctx* c, const double* r, double* cdev) {
+  if (c->perdof) return perdof_restrict(c, r, cdev);
   node_sums(c, r);
   KKT_LAUNCH(c, coarse_restrict_kernel, 1, kCoarseThreads, 0, tables(c), c->nodesum.p,
              c->nranks > 1 ? c->cvec.p : cdev);
@@ -490,10 +493,12 @@ void coarse_restrict(Ctx* c, const double* r, double* cdev) {
 }
 
 void coarse_solve(Ctx* c, double* cdev) {
+  if (c->perdof) return perdof_solve(c, cdev);
   KKT_LAUNCH(c, coarse_solve_kernel, 1, kCoarseThreads, sizeof(double) * c->cdim, tables(c), cdev);
 }
 
 void coarse_prolong_add(Ctx* c, const double* cdev, double* out) {
+  if (c->perdof) return perdof_prolong_add(c, cdev, out);
   KKT_LAUNCH(c, prolong_add_kernel, grid_for(c->B), 256, 0, tables(c), c->ntl, c->nsp, cdev, out);
 }
 
@@ -516,16 +521,24 @@ static void ensure_tmp(Ctx* c) {
 // apply_two_level (schur.cpp:415-444).
 void two_level_apply(Ctx* c, const double* r, double* out, int form) {
   if (!c->has_coarse) throw Error(KKT_ECONFIG, "two-level apply: no coarse space");
-  coarse_gamma(c, r);
-  const bool fast = c->mode == KKT_MODE_FAST && c->has_fast();
-  if (form == KKT_FORM_MULTIPLICATIVE && fast) {
-    rasq_apply(c, r, out, true);
-    return;
-  }
   ensure_tmp(c);
   double* yc = c->tmpB1.p;
   const int g = grid_for(c->B);
-  KKT_LAUNCH(c, broadcast_gamma_kernel, g, 256, 0, c->ntl, c->nsp, c->n0, c->gam.p, yc);
+  if (c->perdof) {
+    // y_c = prolong_add(S0^{-1} restrict(r)) into zeros (schur.cpp:421-424)
+    coarse_restrict(c, r, c->cvec.p);
+    perdof_solve(c, c->cvec.p);
+    KKT_CUDA(cudaMemsetAsync(yc, 0, sizeof(double) * c->B, c->stream));
+    perdof_prolong_add(c, c->cvec.p, yc);
+  } else {
+    coarse_gamma(c, r);
+    const bool fast = c->mode == KKT_MODE_FAST && c->has_fast();
+    if (form == KKT_FORM_MULTIPLICATIVE && fast) {
+      rasq_apply(c, r, out, true);
+      return;
+    }
+    KKT_LAUNCH(c, broadcast_gamma_kernel, g, 256, 0, c->ntl, c->nsp, c->n0, c->gam.p, yc);
+  }
   switch (form) {
     case KKT_FORM_LITERAL:
       rasq_apply(c, yc, out, false);

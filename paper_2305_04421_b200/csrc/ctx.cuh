@@ -124,6 +124,11 @@ struct Ctx {
   std::vector<double> h_S0;       // dense S0 row-major (coarse_matrix_dense)
   DBuf<double> S0lu;              // dense LU factors (DenseLU, linalg.cpp:199-234)
   DBuf<int> S0piv;
+  // per-dof variant (coarse_dof.cu): banded LU with partial pivoting of S0
+  bool perdof = false;
+  int cb_kl = 0, cb_kuf = 0, cb_ld = 0;
+  DBuf<double> cb_ab;             // factor, entry(i,j) at j*cb_ld + i-j+cb_kuf
+  DBuf<int> cb_piv;
   // per-node coarse tables: for node n (1..Nt): column ids and profile values
   DBuf<int> node_col;             // 2 per node: column of (owner, kind 0/1), -1 if absent
   DBuf<double> node_phi;          // 2 per node
@@ -207,7 +212,11 @@ void rasq_apply(Ctx* c, const double* r, double* out, bool with_coarse_residual)
 void coarse_restrict(Ctx* c, const double* r, double* cdev);
 void coarse_solve(Ctx* c, double* cdev);
 void coarse_prolong_add(Ctx* c, const double* cdev, double* out);
-void coarse_gamma(Ctx* c, const double* r);   // restrict + solve -> gam (per-node y_c values)
+void coarse_gamma(Ctx* c, const double* r);
+void build_coarse_perdof(Ctx* c);                 // coarse_dof.cu
+void perdof_restrict(Ctx* c, const double* r, double* cdev);
+void perdof_solve(Ctx* c, double* cdev);
+void perdof_prolong_add(Ctx* c, const double* cdev, double* out);   // restrict + solve -> gam (per-node y_c values)
 void two_level_apply(Ctx* c, const double* r, double* out, int form);
 void schur_apply(Ctx* c, const double* r, double* out);
 void pinv_apply(Ctx* c, const double* r, double* out);
