@@ -174,6 +174,34 @@ int kkt_gmres_solve(kkt_ctx* ctx, const double* b, double* x, kkt_gmres_result* 
 int kkt_gmres_solve_host(kkt_ctx* ctx, const double* b_host, double* x_host,
                          kkt_gmres_result* res, double* history, int32_t history_cap);
 
+/* ---- the end-to-end run record (experiments.hpp:14-31) ------------------ */
+/* evaluate_objective (kkt.cpp:88-108): 0.5 ms sum (u - target)^2 +
+ * 0.5 omega ms sum z^2.  u, z, target: DEVICE blocks (rank-local slab when
+ * sharded); target holds the caller's SpaceTimeFn sampled at the layout's
+ * nodes (t = n dt, x = i dx, y = j dy). */
+int kkt_evaluate_objective(kkt_ctx* ctx, const double* u, const double* z, const double* target,
+                           double* objective);
+/* assemble_rhs(ops, model_initial_condition, model_target).to_kkt()
+ * (kkt.cpp:21-48, model_problem.hpp:11-18) for this context's slab, into HOST
+ * buffers: b (3 x local block) and the target samples (local block; may be NULL). */
+int kkt_model_rhs(kkt_ctx* ctx, double* b_host, double* target_host);
+
+typedef struct kkt_run_record {
+  int32_t iterations;
+  int32_t converged;
+  double true_final_relres;
+  double objective;
+  double setup_seconds;     /* context + preconditioner setup + model RHS */
+  double solve_seconds;     /* GMRES on the device, b and x resident in HBM */
+} kkt_run_record;
+
+/* run_single(cfg) (experiments.cpp:33-69): set up, solve the model problem,
+ * evaluate the objective.  Non-convergence is recorded, not an error.
+ * x_host (3 x local block, may be NULL) receives the solution.  On failure the
+ * message is in kkt_create_error(). */
+int kkt_run_single(const kkt_problem_desc* desc, const kkt_runtime_opts* opts,
+                   kkt_run_record* rec, double* x_host);
+
 /* ---- instrumentation ---------------------------------------------------- */
 /* Number of kernels this context launched since creation (or last reset). */
 int kkt_launch_count(const kkt_ctx* ctx, int64_t* count);

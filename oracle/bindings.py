@@ -21,7 +21,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(_HERE))
-from paper_2305_04421_b200._abi import GmresResult, desc_from_problem  # noqa: E402
+from paper_2305_04421_b200._abi import GmresResult, RunRecordC, desc_from_problem  # noqa: E402
 from paper_2305_04421_b200.problems import Problem  # noqa: E402
 
 REF_SO = os.path.join(_HERE, "_ref", "libkktdd_ref.so")
@@ -212,6 +212,42 @@ class Ref(_Base):
     prefix = "ref_"
     path = REF_SO
     _lib = None
+
+    # -- the f1 record (experiments.cpp:33-69, :179-208) ------------------
+    @classmethod
+    def run_single(cls, problem: Problem, want_x=False):
+        """The reference's own run_single(cfg): (record dict, JSON text, x or None)."""
+        desc = desc_from_problem(problem)
+        rec = RunRecordC()
+        B = problem.block
+        x = np.empty(3 * B) if want_x else None
+        buf = C.create_string_buffer(1 << 14)
+        lib = cls.lib()
+        st = lib.ref_run_single(C.byref(desc), C.byref(rec), _arr(x) if want_x else None, buf,
+                                C.c_int(len(buf)))
+        if st != 0:
+            raise OracleError(st, lib.ref_error().decode(), lib.ref_error_index())
+        d = {k: getattr(rec, k) for k, _ in RunRecordC._fields_}
+        d["converged"] = bool(d["converged"])
+        return d, buf.value.decode(), x
+
+    def model_rhs(self):
+        """(b, target samples) of assemble_rhs(ops, model_initial_condition, model_target)."""
+        b = np.empty(3 * self.block)
+        t = np.empty(self.block)
+        self._call("model_rhs", self.h, _arr(b), _arr(t))
+        return b, t
+
+    def evaluate_objective(self, u, z):
+        out = C.c_double()
+        self._call("evaluate_objective", self.h, _arr(np.ascontiguousarray(u, dtype=np.float64)),
+                   _arr(np.ascontiguousarray(z, dtype=np.float64)), C.byref(out))
+        return out.value
+
+    def zero_control_objective(self):
+        out = C.c_double()
+        self._call("zero_control_objective", self.h, C.byref(out))
+        return out.value
 
 
 class Orc(_Base):

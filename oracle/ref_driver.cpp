@@ -9,6 +9,7 @@
 // make_schur_solver, then gmres_solve with the apply_K / apply_P_inv lambdas —
 // except that the right-hand side is supplied by the caller (the harness's
 // seeded generator) instead of model_problem.hpp.
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <optional>
@@ -23,6 +24,8 @@
 #include "kktdd/linalg.hpp"
 #undef private
 #include "kktdd/config.hpp"
+#include "kktdd/experiments.hpp"
+#include "kktdd/model_problem.hpp"
 #include "kktdd/gmres.hpp"
 #include "kktdd/heat_operators.hpp"
 #include "kktdd/kkt.hpp"
@@ -326,6 +329,72 @@ int ref_gmres_dense(int n, const double* A, const double* M, const double* b, do
     const int nh = std::min<int>(history_cap, static_cast<int>(r.residual_history.size()));
     res->history_len = nh;
     if (history) std::memcpy(history, r.residual_history.data(), sizeof(double) * nh);
+  });
+}
+
+// run_single itself (experiments.cpp:33-69) and its JSON record
+// (experiments.cpp:179-208): the f1 record the device's kkt_run_single mirrors.
+int ref_run_single(const kkt_problem_desc* d, kkt_run_record* rec, double* x, char* json,
+                   int json_cap) {
+  return guarded([&] {
+    ProblemConfig cfg = to_cfg(d);
+    GmresResult res;
+    RunRecord r = run_single(cfg, &res);
+    rec->iterations = r.iterations;
+    rec->converged = r.converged ? 1 : 0;
+    rec->true_final_relres = r.true_final_relres;
+    rec->objective = r.objective;
+    rec->setup_seconds = r.setup_seconds;
+    rec->solve_seconds = r.solve_seconds;
+    if (x) std::memcpy(x, res.solution.data(), sizeof(double) * res.solution.size());
+    if (json && json_cap > 0) {
+      const std::string js = to_json_string(r);
+      std::snprintf(json, static_cast<std::size_t>(json_cap), "%s", js.c_str());
+    }
+  });
+}
+
+// assemble_rhs(ops, model_initial_condition, model_target).to_kkt() and the
+// target samples evaluate_objective uses (kkt.cpp:88-108).
+int ref_model_rhs(void* vc, double* b, double* target) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    const HeatOperators& ops = *c->ops;
+    const KKTVector kb = assemble_rhs(ops, model_initial_condition, model_target).to_kkt();
+    std::memcpy(b, kb.data.data(), sizeof(double) * kb.data.size());
+    const auto& L = ops.layout;
+    for (int n = 1; n <= L.nt; ++n)
+      for (int j = 1; j <= L.ny_int; ++j)
+        for (int i = 1; i <= L.nx_int; ++i)
+          target[L.index(n, i, j)] = model_target(i * c->cfg.dx(), j * c->cfg.dy(), n * ops.dt);
+  });
+}
+
+int ref_evaluate_objective(void* vc, const double* u, const double* z, double* out) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] { *out = evaluate_objective(*c->ops, cin(u, nb(c)), cin(z, nb(c)), model_target); });
+}
+
+// The acceptance suite's zero-control comparison (acceptance_main.cpp:70-84,
+// :443-448): objective of the state driven by f alone, z = 0.
+int ref_zero_control_objective(void* vc, double* out) {
+  auto* c = static_cast<RefCtx*>(vc);
+  return guarded([&] {
+    const HeatOperators& ops = *c->ops;
+    const RhsBundle rhs = assemble_rhs(ops, model_initial_condition, model_target);
+    const int nsp = ops.layout.n_sp();
+    SpaceTimeVector u = ops.layout.zeros();
+    std::vector<double> step(nsp);
+    for (int n = 1; n <= ops.layout.nt; ++n) {
+      const std::size_t off = ops.layout.node_offset(n);
+      for (int p = 0; p < nsp; ++p) {
+        step[p] = rhs.f[off + p];
+        if (n > 1) step[p] += u[ops.layout.node_offset(n - 1) + p];
+      }
+      ops.A_factors.solve_in_place(step);
+      std::copy(step.begin(), step.end(), u.begin() + off);
+    }
+    *out = evaluate_objective(ops, u, ops.layout.zeros(), model_target);
   });
 }
 

@@ -47,6 +47,14 @@ class GmresResult(C.Structure):
     ]
 
 
+class RunRecordC(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int32), ("converged", C.c_int32),
+        ("true_final_relres", C.c_double), ("objective", C.c_double),
+        ("setup_seconds", C.c_double), ("solve_seconds", C.c_double),
+    ]
+
+
 def desc_from_problem(p: Problem) -> ProblemDesc:
     return ProblemDesc(
         Lx=p.Lx, Ly=p.Ly, T=p.T, Nx=p.Nx, Ny=p.Ny, Nt=p.Nt, nu=p.nu, omega=p.omega, Nd=p.Nd,

@@ -5,10 +5,12 @@
 // HeatOperators (heat_operators.cpp:46-55: derived constants with the
 // reference's expressions, Ahat factorisation), build_time_partition
 // (time_partition.cpp:61-86) and make_schur_solver (schur.cpp:543-558).
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "ctx.cuh"
 
@@ -428,6 +430,84 @@ int kkt_gmres_solve_host(kkt_ctx* ctx, const double* b_host, double* x_host,
     KKT_CUDA(cudaMemcpyAsync(x_host, c->e2e_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
     KKT_CUDA(cudaStreamSynchronize(c->stream));
   });
+}
+
+namespace kkt {
+namespace {
+// assemble_rhs (kkt.cpp:29-48) with model_initial_condition / model_target
+// (model_problem.hpp:11-18), for the local slab; same expressions and order.
+void model_rhs(const Ctx* c, double* b, double* target) {
+  const double two_pi = 2.0 * 3.141592653589793;  // 2 * std::numbers::pi
+  const int64_t B = c->B;
+  for (int nl = 0; nl < c->ntl; ++nl) {
+    const int n = c->n0 + nl;
+    const double t = n * c->dt;
+    for (int j = 1; j <= c->ny; ++j) {
+      for (int i = 1; i <= c->nx; ++i) {
+        const double x = i * c->dx, y = j * c->dy;
+        const int64_t k = (int64_t(nl) * c->ny + (j - 1)) * c->nx + (i - 1);
+        const double tv = std::sin(two_pi * t) * std::sin(two_pi * x) * std::sin(two_pi * y);
+        b[k] = c->ms * tv;
+        b[B + k] = 0.0;
+        b[2 * B + k] = n == 1 ? -x * y * (x - 1.0) * (y - 2.0) : 0.0;
+        if (target) target[k] = tv;
+      }
+    }
+  }
+}
+}  // namespace
+}  // namespace kkt
+
+int kkt_evaluate_objective(kkt_ctx* ctx, const double* u, const double* z, const double* target,
+                           double* objective) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(u && z && target && objective, "evaluate_objective: bad arguments");
+    *objective = kkt::kkt_objective(c, u, z, target);
+  });
+}
+
+int kkt_model_rhs(kkt_ctx* ctx, double* b_host, double* target_host) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(b_host != nullptr, "model_rhs: bad arguments");
+    kkt::model_rhs(c, b_host, target_host);
+  });
+}
+
+int kkt_run_single(const kkt_problem_desc* desc, const kkt_runtime_opts* opts, kkt_run_record* rec,
+                   double* x_host) {
+  if (!desc || !rec) return KKT_EINVAL;
+  using clock = std::chrono::steady_clock;
+  auto secs = [](clock::time_point a) { return std::chrono::duration<double>(clock::now() - a).count(); };
+  const auto t_setup = clock::now();
+  kkt_ctx* ctx = nullptr;
+  int st = kkt_ctx_create(desc, opts, &ctx);
+  if (st != KKT_OK) return st;
+  st = kkt::guard(ctx, [&](Ctx* c) {
+    const size_t B = size_t(c->B);
+    std::vector<double> b(3 * B), tgt(B);
+    kkt::model_rhs(c, b.data(), tgt.data());
+    kkt::DBuf<double> db{3 * B}, dx{3 * B}, dt{B};
+    KKT_CUDA(cudaMemcpyAsync(db.p, b.data(), sizeof(double) * 3 * B, cudaMemcpyHostToDevice, c->stream));
+    KKT_CUDA(cudaMemcpyAsync(dt.p, tgt.data(), sizeof(double) * B, cudaMemcpyHostToDevice, c->stream));
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+    rec->setup_seconds = secs(t_setup);
+    const auto t_solve = clock::now();
+    kkt_gmres_result res{};
+    kkt::gmres(c, db.p, dx.p, &res, nullptr, 0);
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+    rec->solve_seconds = secs(t_solve);
+    rec->iterations = res.iterations;
+    rec->converged = res.converged;
+    rec->true_final_relres = res.true_final_relres;
+    rec->objective = kkt::kkt_objective(c, dx.p, dx.p + B, dt.p);
+    if (x_host) {
+      KKT_CUDA(cudaMemcpyAsync(x_host, dx.p, sizeof(double) * 3 * B, cudaMemcpyDeviceToHost, c->stream));
+      KKT_CUDA(cudaStreamSynchronize(c->stream));
+    }
+  });
+  if (st != KKT_OK) kkt::g_create_err = kkt_last_error(ctx);
+  kkt_ctx_destroy(ctx);
+  return st;
 }
 
 int kkt_launch_count(const kkt_ctx* ctx, int64_t* count) {

@@ -212,6 +212,7 @@ void rasq_apply(Ctx* c, const double* r, double* out, bool with_coarse_residual)
 void coarse_restrict(Ctx* c, const double* r, double* cdev);
 void coarse_solve(Ctx* c, double* cdev);
 void coarse_prolong_add(Ctx* c, const double* cdev, double* out);
+double kkt_objective(Ctx* c, const double* u, const double* z, const double* target);  // krylov.cu
 void coarse_gamma(Ctx* c, const double* r);
 void build_coarse_perdof(Ctx* c);                 // coarse_dof.cu
 void perdof_restrict(Ctx* c, const double* r, double* cdev);

@@ -383,6 +383,19 @@ double kkt_relres(Ctx* c, const double* v, const double* rhs) {
   return b2 > 0.0 ? r / std::sqrt(b2) : r;
 }
 
+// evaluate_objective (kkt.cpp:88-108): misfit = sum (u - target)^2 and
+// control = sum z^2, each in index order (STRICT) or by the fixed-shape tree
+// (FAST); the target is sampled by the caller (a SpaceTimeFn is a host callback).
+double kkt_objective(Ctx* c, const double* u, const double* z, const double* target) {
+  const int64_t n = c->B;
+  if (c->hbuf.n < 8) c->hbuf.alloc(8);
+  DotArgs A{kDotDiff, n, const_cast<double*>(u), nullptr, nullptr, target, c->hbuf.p + 2, nullptr};
+  launch_dot(c, A);
+  const double misfit = fetch(c, c->hbuf.p + 2);
+  const double control = dev_dot(c, z, z, n, c->hbuf.p + 3);
+  return 0.5 * c->ms * misfit + 0.5 * c->desc.omega * c->ms * control;
+}
+
 // gmres_solve (gmres.cpp:21-155) with apply_operator = apply_K and
 // apply_preconditioner = apply_P_inv (or none), as wired by run_single
 // (experiments.cpp:46-57).

@@ -291,6 +291,21 @@ class HeatKKT:
         self._call("kkt_residual", dptr(v), dptr(rhs), C.byref(out))
         return out.value
 
+    def evaluate_objective(self, u, z, target) -> float:
+        """evaluate_objective (kkt.cpp:88-108) with the target sampled at the nodes."""
+        u, z, target = (self._dev(a, self.block) for a in (u, z, target))
+        out = C.c_double()
+        self._call("kkt_evaluate_objective", dptr(u), dptr(z), dptr(target), C.byref(out))
+        return out.value
+
+    def model_rhs(self):
+        """assemble_rhs(ops, model_initial_condition, model_target).to_kkt() and the
+        target samples (kkt.cpp:21-48, model_problem.hpp) for this slab, on the host."""
+        b = np.empty(3 * self.block)
+        t = np.empty(self.block)
+        self._check(lib().kkt_model_rhs(self._h, b.ctypes.data_as(_P), t.ctypes.data_as(_P)))
+        return b, t
+
     # -- Schur level (schur.hpp) ------------------------------------------------
     def apply_shat(self, v, out=None): return self._unary("kkt_apply_shat", v, self.block, out)
     def apply_rasq(self, r, out=None): return self._unary("kkt_apply_rasq", r, self.block, out)

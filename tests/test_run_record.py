@@ -1,0 +1,59 @@
+"""CPU: the f1 run record (experiments.cpp:33-69, :179-208) on the reference
+side — the JSON layout our ``to_json_string`` must reproduce, the model
+problem's right-hand side, and the acceptance suite's objective criterion
+(acceptance_main.cpp:433-457) on the reference's own runs."""
+import json
+
+import numpy as np
+import pytest
+
+from oracle.bindings import Ref, available
+from paper_2305_04421_b200 import problems as P
+
+pytestmark = pytest.mark.skipif(not available("ref"), reason="oracle/_ref not built")
+
+SMALL = P.Problem(Lx=1.0, Ly=2.0, Nx=8, Ny=6, Nt=12, Nd=3, omega=1e-2, coarse_variant="scalar",
+                  tol=1e-10, restart=10, max_iters=200)
+
+
+def test_to_json_string_matches_reference_layout():
+    from paper_2305_04421_b200.experiments import RunRecord, to_json_string
+    for p in (SMALL, SMALL.replace(coarse_variant="per-dof", restart=None, precond="two-level"),
+              SMALL.replace(precond="one-level", jhat_sign="plus", two_level_form="additive")):
+        rec, text, _ = Ref.run_single(p)
+        mine = RunRecord(p, rec["iterations"], rec["converged"], rec["true_final_relres"],
+                         rec["objective"], rec["setup_seconds"], rec["solve_seconds"])
+        assert to_json_string(mine) == text
+        assert json.loads(text)["converged"] == rec["converged"]
+
+
+def test_model_rhs_restated():
+    """assemble_rhs with model_problem.hpp: f_u = ms*target, f(n=1) = u0, f_z = 0."""
+    p = SMALL
+    ref = Ref(p)
+    b, t = ref.model_rhs()
+    B, nx, ny = p.block, p.nx_int, p.ny_int
+    dx, dy, dt = p.Lx / p.Nx, p.Ly / p.Ny, p.T / p.Nt
+    n = np.arange(1, p.Nt + 1)[:, None, None]
+    j = np.arange(1, ny + 1)[None, :, None]
+    i = np.arange(1, nx + 1)[None, None, :]
+    tw = 2.0 * np.pi
+    tgt = (np.sin(tw * (n * dt)) * np.sin(tw * (i * dx)) * np.sin(tw * (j * dy))).reshape(-1)
+    assert np.allclose(t, tgt, rtol=0, atol=1e-15)
+    assert np.allclose(b[:B], (dt * dx * dy) * t, rtol=1e-15, atol=0)
+    assert not np.any(b[B:2 * B])
+    x, y = (i * dx)[0], (j * dy)[0]
+    u0 = (-x * y * (x - 1.0) * (y - 2.0)).reshape(-1)
+    assert np.allclose(b[2 * B:2 * B + p.n_sp], u0, rtol=1e-15, atol=0)
+    assert not np.any(b[2 * B + p.n_sp:])
+
+
+def test_reference_objective_below_zero_control():
+    """Criterion 10 (acceptance_main.cpp:433-457) on the reference's runs."""
+    for p in (SMALL, SMALL.replace(omega=1e-4)):
+        rec, _, x = Ref.run_single(p, want_x=True)
+        ref = Ref(p)
+        assert rec["converged"] and rec["true_final_relres"] <= 1e-5
+        B = p.block
+        assert ref.evaluate_objective(x[:B], x[B:2 * B]) == rec["objective"]
+        assert rec["objective"] <= ref.zero_control_objective() * (1.0 + 1e-8)
