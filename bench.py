@@ -60,14 +60,31 @@ def workload_desc(cfg, p):
             f"GMRES({p.restart}) rtol {p.tol}")
 
 
-def sweep_bytes(p, ranks=1):
-    """Algorithmic bytes of one RASQ sweep per GPU:
-    (2Nt + Nd - 1) * 5 planes * n_sp * 8 / G  +  (2m+1) * F,  F = 8 n_sp (2 nx + 1)
-    (the plane traffic splits over the G slabs; every GPU streams the factor)."""
-    m = p.Nt // p.Nd
-    planes = (2 * p.Nt + p.Nd - 1) * 5 * p.n_sp * 8
-    F = 8 * p.n_sp * (2 * p.nx_int + 1)
-    return planes // ranks + (2 * m + 1) * F
+def mgs_model(p, iters, ranks=1):
+    """Algorithmic bytes and launches of the modified Gram-Schmidt passes of one
+    solve: iteration j of a cycle runs h_0 = (w, v_0), j
+    fused axpy+dot passes and one fused axpy+norm = (4j + 5) vector passes of
+    3 * block * 8 bytes (per GPU: the vectors split over the G slabs)."""
+    m = p.restart or p.max_iters
+    vec = 3 * p.block * 8 // ranks
+    js = [k % m for k in range(iters)]
+    return sum((4 * j + 5) * vec for j in js), sum(j + 2 for j in js)
+
+
+def spectral_flops(p, ranks=1):
+    """fp64 FLOPs of the four sine-transform passes of one Schur apply
+    (spectral.cu): per plane X Sx (ny nx nx FMAs) and Sy Y (ny ny nx FMAs),
+    forward and inverse."""
+    ntl = p.Nt // ranks
+    return 2 * 2 * ntl * p.n_sp * (p.nx_int + p.ny_int)
+
+
+def fp64_peak():
+    path = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    try:
+        return float(json.load(open(path))["dmma_tflops"]), "measured (profiles/fp64_peak.json, scripts/fp64_peak.cu)"
+    except Exception:
+        return None, "unmeasured"
 
 
 class ClockSampler:
@@ -304,17 +321,23 @@ def run_ours(args, ws, rank, local):
     ms_e2e = max_over_ranks(e0.elapsed_time(e1) / e2e_steps, ws)
     e2e_value = ws * unknowns / (ms_e2e / 1000.0)
 
-    # ---- roofline of the dominant kernel (the RASQ sweep, K5)
+    # ---- roofline of the dominant kernel family: the Krylov MGS passes
+    # (dot_vec_kernel<0/1/2>, krylov.cu), HBM-bound; phase slot 2 brackets them
     peak, peak_src = hbm_peak()
-    sweep_ms = phase_ms[3] / max(1, phase_cnt[3])
-    achieved = sweep_bytes(p, ws) / (sweep_ms / 1000.0) / 1e9
+    mgs_bytes, mgs_launches = mgs_model(p, iters[-1], ws)
+    mgs_ms = phase_ms[2] / args.steps
+    achieved = mgs_bytes / (mgs_ms / 1000.0) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("sweep_dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get("mgs_axpy_dot_dram_bytes_per_launch")
         except Exception:
             traffic = None
+    # secondary: the spectral Schur apply (fp64 tensor cores), phase slot 3
+    tpk, tpk_src = fp64_peak()
+    sp_ms = phase_ms[3] / max(1, phase_cnt[3])
+    sp_tf = spectral_flops(p, ws) / (sp_ms / 1000.0) / 1e12 if sp_ms > 0 else None
 
     if rank != 0:
         return
@@ -335,12 +358,19 @@ def run_ours(args, ws, rank, local):
                                   "sweep_kernel": phase_ms[3] / args.steps},
         },
         "roofline": {
-            "kernel": "RASQ sweep K5 (grpA/grpB/grpC kernels, sweep_group.cu)", "bound": "hbm",
-            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "kernel": "Krylov MGS passes (dot_vec_kernel<0,1,2>: dot, fused axpy+dot, fused axpy+norm; krylov.cu)",
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": sweep_bytes(p, ws), "avg_launch_ms": sweep_ms,
-            "launches": phase_cnt[3],
-            "share_of_step": phase_ms[3] / max(1e-9, ms_total),
+            "algorithmic_bytes_per_launch": mgs_bytes / mgs_launches,
+            "avg_launch_ms": mgs_ms / mgs_launches, "launches": mgs_launches * args.steps,
+            "share_of_step": mgs_ms / max(1e-9, ms_step),
+        },
+        "roofline_schur": {
+            "kernel": "spectral RASQ: 4 sine-transform GEMM passes (gemm_f64_kernel, mma.sync m8n8k4 f64) + per-mode recurrences (spectral.cu)",
+            "bound": "tensor", "achieved": sp_tf, "peak": tpk, "unit": "TFLOP/s",
+            "frac": (sp_tf / tpk) if (sp_tf and tpk) else None, "peak_source": tpk_src,
+            "flops_per_apply": spectral_flops(p, ws), "avg_apply_ms": sp_ms,
+            "applies": phase_cnt[3], "share_of_step": phase_ms[3] / max(1e-9, ms_total),
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": ms_e2e, "wall_ms_per_step": 1000 * wall_e2e},

@@ -178,6 +178,9 @@ void setup(Ctx* c, const kkt_problem_desc& d, const kkt_runtime_opts* o) {
     build_factor(c);
     if (c->mode == KKT_MODE_FAST) build_block_inverses(c);
   }
+  // FAST RASQ in Ahat's eigenbasis (spectral.cu); KKT_NO_SPECTRAL keeps the
+  // block-LU chains (sweep_group.cu / sweep_tma.cu / sweep_fast.cu)
+  if (c->mode == KKT_MODE_FAST) build_spectral(c);
   if (d.precond == KKT_PRECOND_TWO_LEVEL) build_coarse(c);
   KKT_CUDA(cudaStreamSynchronize(c->stream));
 }

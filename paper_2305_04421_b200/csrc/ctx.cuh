@@ -115,6 +115,8 @@ struct Ctx {
   };
   std::vector<Graph> graphs;
   DBuf<double> arena;              // one allocation for the sweep operators (L2-persisting window)
+  // spectral FAST RASQ (spectral.cu): sine matrices, eigenvalues, T(1), scratch
+  DBuf<double> sp_x, sp_y, sp_lam, sp_chat, sp_halo, sp_w1, sp_w2;
 
   // ---- coarse space (scalar variant)
   bool has_coarse = false;
@@ -207,6 +209,10 @@ void op_shat(Ctx* c, const double* v, double* out, double* tmp);
 void band_solve(Ctx* c, double* b, int nrhs, bool transpose);
 void window_solve(Ctx* c, double* b, int len, bool adjoint);
 void rasq_apply(Ctx* c, const double* r, double* out, bool with_coarse_residual);
+// ---- spectral FAST RASQ (spectral.cu)
+void build_spectral(Ctx* c);
+bool spectral_enabled(const Ctx* c);
+void spectral_rasq(Ctx* c, const double* r, const double* halo_prev, double* out, bool fused);
 
 // ---- coarse (coarse.cu)
 void coarse_restrict(Ctx* c, const double* r, double* cdev);

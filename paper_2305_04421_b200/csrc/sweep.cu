@@ -90,6 +90,10 @@ void rasq_apply(Ctx* c, const double* r, double* out, bool fused_coarse) {
     return base + (n - c->n0) * nsp;
   };
   auto wplane = [&](double* base, int n) { return base + (n - c->n0) * nsp; };
+  if (c->mode == KKT_MODE_FAST && spectral_enabled(c)) {
+    spectral_rasq(c, r, c->s0 > 0 ? hr.prev : nullptr, out, fused_coarse);
+    return;
+  }
   if (c->mode == KKT_MODE_STRICT || !c->has_fast()) {
     // scratch: one plane per subdomain for the shared node's forward value
     const size_t need = size_t(Nd) * nsp;

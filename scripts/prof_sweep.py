@@ -35,3 +35,13 @@ for _ in range(a.reps):
 ev1.record()
 torch.cuda.synchronize()
 print(f"P_inv apply: {ev0.elapsed_time(ev1) / a.reps:.3f} ms")
+ev0.record()
+for _ in range(a.reps):
+    k.apply_K(r, out)
+ev1.record()
+torch.cuda.synchronize()
+print(f"K apply: {ev0.elapsed_time(ev1) / a.reps:.3f} ms")
+k.set_phase_timing(True)
+k.apply_P_inv(r, out)
+torch.cuda.synchronize()
+print("phase ms (0 K, 1 P_inv, 2 Krylov, 3 sweep kernel):", k.phase_times())

@@ -137,5 +137,10 @@ def test_bench_roofline_bytes():
     bench = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(bench)
     p = P.config(1)
-    # (2Nt + Nd - 1) * 5 * n_sp * 8 + (2m+1) * 8 n_sp (2 nx + 1)
-    assert bench.sweep_bytes(p) == (2 * 512 + 15) * 5 * 16129 * 8 + 65 * 8 * 16129 * 255
+    vec = 3 * 512 * 16129 * 8
+    # 44 iterations of GMRES(30): j = 0..29 then 0..13, (4j + 5) vector passes each
+    b, launches = bench.mgs_model(p, 44)
+    assert b == (4 * (435 + 91) + 5 * 44) * vec and launches == (435 + 91) + 2 * 44
+    assert bench.mgs_model(p, 44, ranks=2)[0] == b // 2
+    # four transform passes: 2 * 2 * Nt * n_sp * (nx + ny) FLOPs
+    assert bench.spectral_flops(p) == 4 * 512 * 16129 * 254
