@@ -60,15 +60,21 @@ def workload_desc(cfg, p):
             f"GMRES({p.restart}) rtol {p.tol}")
 
 
-def mgs_model(p, iters, ranks=1):
-    """Algorithmic bytes and launches of the modified Gram-Schmidt passes of one
-    solve: iteration j of a cycle runs h_0 = (w, v_0), j
-    fused axpy+dot passes and one fused axpy+norm = (4j + 5) vector passes of
-    3 * block * 8 bytes (per GPU: the vectors split over the G slabs)."""
+def mgs_model(p, iters, ranks=1, mode="fast"):
+    """Algorithmic bytes and launches of the Gram-Schmidt passes of one solve
+    (SURVEY.md §8d, K7), per GPU (the vectors split over the G slabs).
+    FAST (krylov.cu, one-reduction MGS): iteration j reads w and v_0..v_j once
+    for r = V^T w and the Gram row, then reads v_0..v_j and w and writes w for
+    w -= V h: 2j + 5 vector passes; launches: ceil((j+1)/16) dots + 1 solve +
+    ceil((j+1)/16) updates.  STRICT (reference MGS order): 4j + 5 passes, j + 2
+    launches."""
     m = p.restart or p.max_iters
     vec = 3 * p.block * 8 // ranks
     js = [k % m for k in range(iters)]
-    return sum((4 * j + 5) * vec for j in js), sum(j + 2 for j in js)
+    if mode == "strict":
+        return sum((4 * j + 5) * vec for j in js), sum(j + 2 for j in js)
+    return (sum((2 * j + 5) * vec for j in js),
+            sum(2 * -(-(j + 1) // 16) + 1 for j in js))
 
 
 def spectral_flops(p, ranks=1):
@@ -324,7 +330,7 @@ def run_ours(args, ws, rank, local):
     # ---- roofline of the dominant kernel family: the Krylov MGS passes
     # (dot_vec_kernel<0/1/2>, krylov.cu), HBM-bound; phase slot 2 brackets them
     peak, peak_src = hbm_peak()
-    mgs_bytes, mgs_launches = mgs_model(p, iters[-1], ws)
+    mgs_bytes, mgs_launches = mgs_model(p, iters[-1], ws, args.mode)
     mgs_ms = phase_ms[2] / args.steps
     achieved = mgs_bytes / (mgs_ms / 1000.0) / 1e9
     traffic = None
@@ -358,7 +364,8 @@ def run_ours(args, ws, rank, local):
                                   "sweep_kernel": phase_ms[3] / args.steps},
         },
         "roofline": {
-            "kernel": "Krylov MGS passes (dot_vec_kernel<0,1,2>: dot, fused axpy+dot, fused axpy+norm; krylov.cu)",
+            "kernel": ("Krylov Gram-Schmidt passes: one-reduction MGS (cgs_dots_kernel, icwy_solve_kernel, cgs_update_kernel; krylov.cu)"
+                       if args.mode == "fast" else "Krylov MGS passes (dot_seq_kernel, reference order; krylov.cu)"),
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": mgs_bytes / mgs_launches,

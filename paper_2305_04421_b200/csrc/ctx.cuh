@@ -180,6 +180,8 @@ struct Ctx {
   int err_index = -1;
 
   DBuf<double> red_all;            // all-gathered partial sums
+  DBuf<double*> bptr;              // device array of Krylov basis pointers (FAST ICWY-MGS)
+  DBuf<double> gram;               // FAST ICWY-MGS: the cycle's basis Gram rows
   ~Ctx();
 };
 

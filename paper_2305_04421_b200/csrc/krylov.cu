@@ -18,6 +18,7 @@
 //    per-CTA partials, last CTA sums the partials in index order).
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include "ctx.cuh"
@@ -272,6 +273,210 @@ __global__ void __launch_bounds__(kTreeThreads) dot_tree_kernel(DotArgs A, doubl
   }
 }
 
+// ---------------------------------------------------------------------------
+// FAST orthogonalisation: modified Gram-Schmidt in its one-reduction ("ICWY")
+// form (Swirydowicz et al., low-synchronisation Gram-Schmidt).  MGS's
+// coefficients satisfy h_i = (v_i, w) - sum_{k<i} (v_i, v_k) h_k, i.e.
+// h = (I + L)^{-1} r with r = V^T w and L the strictly lower part of V^T V,
+// so one pass over the basis forms r together with the new Gram row
+// (v_j, v_k), k < j; a one-warp kernel solves the small triangular system;
+// a second pass forms w -= V h and ||w||^2.  2j + 5 vector passes at
+// iteration j instead of MGS's 4j + 5, with MGS's coefficients to rounding
+// (and its orthogonality behaviour).  STRICT keeps the reference's MGS
+// order (gmres.cpp:92-96).
+// ---------------------------------------------------------------------------
+constexpr int kMD = 32;              // accumulators per launch
+constexpr int kMDH = kMD / 2;        // basis vectors per dots launch (r and Gram dots)
+constexpr int kMDS = kMD;
+constexpr int kCgsThreads = 128;
+constexpr int kCgsBlocks = kSmCount * 3;  // 3 CTAs/SM at ~140 registers (<= kTreeBlocks partials)
+
+struct CgsArgs {
+  int64_t n;
+  double* w;
+  const double* const* v;  // device array of basis pointers (this chunk)
+  int nb;                  // vectors in this chunk
+  const double* vj;        // dots: newest basis vector (Gram row), nullable
+  int ng;                  // dots: Gram dots in this chunk (v_i with i < j)
+  const double* h;         // update: coefficients of this chunk
+  double* dst;             // dots: kMD values (r at [0, nb), Gram at [kMDH, kMDH+ng)); update: ||w||^2
+  int* flag;               // non-finite w entries (nullable)
+};
+
+// block partial sums of `nv` accumulators -> partial[block * kMDS + i]; the
+// last block reduces the partials in block order (deterministic).
+__device__ void cgs_reduce(double (&acc)[kMDS], int nv, double* dst, double* partial, unsigned* counter) {
+  __shared__ double wsum[kCgsThreads / 32][kMDS];
+  __shared__ bool is_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < kMDS; ++i) {
+    if (i < nv) {
+      double a = acc[i];
+      for (int off = 16; off; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+      if (lane == 0) wsum[warp][i] = a;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double s = 0.0;
+    for (int w = 0; w < kCgsThreads / 32; ++w) s += wsum[w][threadIdx.x];
+    partial[int64_t(blockIdx.x) * kMDS + threadIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int i = warp; i < nv; i += kCgsThreads / 32) {
+    double s = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) s += ((volatile double*)partial)[int64_t(b) * kMDS + i];
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) dst[i] = s;
+  }
+  if (threadIdx.x == 0) *counter = 0;
+}
+
+// NB basis vectors (compile time: every load is issued ahead of its FMAs)
+template <int NB>
+__global__ void __launch_bounds__(kCgsThreads) cgs_dots_kernel(CgsArgs A, double* partial, unsigned* counter) {
+  double acc[kMDS];
+#pragma unroll
+  for (int i = 0; i < kMDS; ++i) acc[i] = 0.0;
+  const double* vp[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) vp[i] = A.v[i];
+  const double* vj = A.ng > 0 ? A.vj : A.w;  // ng == 0: Gram slots stay unused
+  bool bad = false;
+  const int64_t npair = A.n >> 1;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < npair; k += stride) {
+    const double2 w = ld2(A.w, k);
+    const double2 q = ld2(vj, k);
+    double2 v[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) v[i] = __ldg(reinterpret_cast<const double2*>(vp[i]) + k);
+    if (A.flag && !(isfinite(w.x) && isfinite(w.y))) bad = true;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      acc[i] = fma(w.x, v[i].x, fma(w.y, v[i].y, acc[i]));
+      acc[kMDH + i] = fma(q.x, v[i].x, fma(q.y, v[i].y, acc[kMDH + i]));
+    }
+  }
+  if ((A.n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const double w = A.w[A.n - 1];
+    if (A.flag && !isfinite(w)) bad = true;
+    const double q = vj[A.n - 1];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const double v = vp[i][A.n - 1];
+      acc[i] = fma(w, v, acc[i]);
+      acc[kMDH + i] = fma(q, v, acc[kMDH + i]);
+    }
+  }
+  if (bad) *A.flag = 1;
+  cgs_reduce(acc, kMDS, A.dst, partial, counter);
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kCgsThreads) cgs_update_kernel(CgsArgs A, double* partial, unsigned* counter) {
+  double acc[kMDS];
+#pragma unroll
+  for (int i = 0; i < kMDS; ++i) acc[i] = 0.0;
+  const double* vp[NB];
+  double nh[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    vp[i] = A.v[i];
+    nh[i] = -A.h[i];
+  }
+  const int64_t npair = A.n >> 1;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  auto step = [&](double2 w, const double2 (&v)[NB]) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      w.x = fma(nh[i], v[i].x, w.x);
+      w.y = fma(nh[i], v[i].y, w.y);
+    }
+    return w;
+  };
+  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  // two independent pair indices per trip: 2 (NB + 1) loads in flight
+  for (; k + stride < npair; k += 2 * stride) {
+    double2 v0[NB], v1[NB];
+    const double2 w0 = ld2(A.w, k), w1 = ld2(A.w, k + stride);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      v0[i] = __ldg(reinterpret_cast<const double2*>(vp[i]) + k);
+      v1[i] = __ldg(reinterpret_cast<const double2*>(vp[i]) + k + stride);
+    }
+    const double2 r0 = step(w0, v0), r1 = step(w1, v1);
+    st2(A.w, k, r0);
+    st2(A.w, k + stride, r1);
+    acc[0] = fma(r0.x, r0.x, fma(r0.y, r0.y, acc[0]));
+    acc[1] = fma(r1.x, r1.x, fma(r1.y, r1.y, acc[1]));
+  }
+  for (; k < npair; k += stride) {
+    double2 v0[NB];
+    const double2 w0 = ld2(A.w, k);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) v0[i] = __ldg(reinterpret_cast<const double2*>(vp[i]) + k);
+    const double2 r0 = step(w0, v0);
+    st2(A.w, k, r0);
+    acc[0] = fma(r0.x, r0.x, fma(r0.y, r0.y, acc[0]));
+  }
+  acc[0] += acc[1];
+  acc[1] = 0.0;
+  if ((A.n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    double w = A.w[A.n - 1];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) w = fma(nh[i], vp[i][A.n - 1], w);
+    A.w[A.n - 1] = w;
+    acc[0] = fma(w, w, acc[0]);
+  }
+  cgs_reduce(acc, 1, A.dst, partial, counter);
+}
+
+template <int NB>
+void launch_dots(Ctx* c, const CgsArgs& A) {
+  if constexpr (NB > 1) {
+    if (A.nb < NB) return launch_dots<NB - 1>(c, A);
+  }
+  KKT_LAUNCH(c, cgs_dots_kernel<NB>, kCgsBlocks, kCgsThreads, 0, A, c->red.p, c->red_count.p);
+}
+
+template <int NB>
+void launch_update(Ctx* c, const CgsArgs& A) {
+  if constexpr (NB > 1) {
+    if (A.nb < NB) return launch_update<NB - 1>(c, A);
+  }
+  KKT_LAUNCH(c, cgs_update_kernel<NB>, kTreeBlocks, kCgsThreads, 0, A, c->red.p, c->red_count.p);
+}
+
+// Gram row j and h = (I + L)^{-1} r (one thread; j < max_iters, O(j^2)).
+// chunks: kMD values per chunk of kMDH basis vectors (r first, Gram second).
+__global__ void icwy_solve_kernel(int j, const double* __restrict__ chunks, double* __restrict__ G,
+                                  int ldg, double* __restrict__ h) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int k = 0; k < j; ++k) G[int64_t(j) * ldg + k] = chunks[(k / kMDH) * kMD + kMDH + (k % kMDH)];
+  for (int i = 0; i <= j; ++i) {
+    double acc = chunks[(i / kMDH) * kMD + (i % kMDH)];
+    for (int k = 0; k < i; ++k) acc = fma(-G[int64_t(i) * ldg + k], h[k], acc);
+    h[i] = acc;
+  }
+}
+
+// rank-ordered sums of `cnt` all-gathered values per rank
+__global__ void sum_partials_multi_kernel(const double* __restrict__ parts, int nranks, int cnt,
+                                          double* __restrict__ dst) {
+  const int i = threadIdx.x;
+  if (i >= cnt) return;
+  double s = 0.0;
+  for (int r = 0; r < nranks; ++r) s += parts[r * cnt + i];
+  dst[i] = s;
+}
+
 // v = r / beta  (gmres.cpp:64-67) and v_{j+1} = w / h_{j+1} (:120-123).
 __global__ void div_kernel(int64_t n, const double* __restrict__ in, double* __restrict__ out,
                            double d) {
@@ -319,7 +524,7 @@ int grid_for(int64_t n) {
 
 void ensure_reduction(Ctx* c) {
   if (!c->red.p) {
-    c->red.alloc(kTreeBlocks);
+    c->red.alloc(size_t(kTreeBlocks) * kMDS);
     c->red_count.alloc(1);
     KKT_CUDA(cudaMemsetAsync(c->red_count.p, 0, sizeof(unsigned), c->stream));
   }
@@ -358,6 +563,37 @@ double fetch(Ctx* c, const double* d) {
   KKT_CUDA(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   KKT_CUDA(cudaStreamSynchronize(c->stream));
   return h;
+}
+
+void cgs_allreduce(Ctx* c, double* dst, int nv) {
+  if (c->nranks <= 1) return;
+  if (c->red_all.n < size_t(c->nranks) * kMDS) c->red_all.alloc(size_t(c->nranks) * kMDS);
+  c->comm->allgather(dst, c->red_all.p, size_t(nv), c->stream);
+  KKT_LAUNCH(c, sum_partials_multi_kernel, 1, 64, 0, c->red_all.p, c->nranks, nv, dst);
+}
+
+// h (device, j+1 values) = MGS coefficients of w against v_0..v_j, then
+// w -= V h and ||w||^2 -> h[j+1].  `scratch` holds kMD values per chunk; G is
+// the cycle's Gram matrix (ldg x ldg, rows filled as the basis grows).
+void icwy_orthogonalise(Ctx* c, double* w, const double* const* bptr, const double* vj, int j, double* h,
+                        double* scratch, double* G, int ldg) {
+  const int nb = j + 1;
+  const int64_t n = 3 * c->B;
+  for (int c0 = 0, ci = 0; c0 < nb; c0 += kMDH, ++ci) {
+    const int cnt = std::min(kMDH, nb - c0);
+    const int ng = std::max(0, std::min(cnt, j - c0));
+    CgsArgs A{n, w, bptr + c0, cnt, ng > 0 ? vj : nullptr, ng, nullptr, scratch + ci * kMD,
+              c0 == 0 ? c->flag.p : nullptr};
+    launch_dots<kMDH>(c, A);
+    cgs_allreduce(c, A.dst, kMD);
+  }
+  KKT_LAUNCH(c, icwy_solve_kernel, 1, 32, 0, j, scratch, G, ldg, h);
+  for (int c0 = 0; c0 < nb; c0 += kMDH) {
+    const int cnt = std::min(kMDH, nb - c0);
+    CgsArgs A{n, w, bptr + c0, cnt, nullptr, 0, h + c0, h + nb, nullptr};
+    launch_update<kMDH>(c, A);
+    cgs_allreduce(c, A.dst, 1);
+  }
 }
 
 }  // namespace
@@ -406,7 +642,15 @@ int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* his
   const int64_t n = 3 * c->B;
   const bool have_prec = P.precond != KKT_PRECOND_NONE;
   ensure_reduction(c);
-  if (c->hbuf.n < size_t(P.max_iters) + 8) c->hbuf.alloc(size_t(P.max_iters) + 8);
+  // FAST: two-pass classical Gram-Schmidt with selective reorthogonalisation
+  // (cgs_pass); KKT_MGS=1 keeps MGS in FAST mode too
+  static const bool force_mgs = std::getenv("KKT_MGS") != nullptr;
+  const bool cgs = c->mode == KKT_MODE_FAST && !force_mgs;
+  const size_t hstride = size_t(P.max_iters) + 8 + kMD;
+  if (c->hbuf.n < 2 * hstride + size_t(kMD) * (P.max_iters / kMDH + 2))
+    c->hbuf.alloc(2 * hstride + size_t(kMD) * (P.max_iters / kMDH + 2));
+  const int ldg = (P.restart > 0 ? std::min(P.restart, P.max_iters) : P.max_iters) + 1;
+  if (cgs && c->gram.n < size_t(ldg) * ldg) c->gram.alloc(size_t(ldg) * ldg);
   if (c->g_r.n < size_t(n)) c->g_r.alloc(n);
   if (c->g_w.n < size_t(n)) c->g_w.alloc(n);
   if (have_prec && c->g_z.n < size_t(n)) c->g_z.alloc(n);
@@ -451,13 +695,20 @@ int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* his
       c->basis.back().alloc(n);
     }
     KKT_LAUNCH(c, div_kernel, g, 256, 0, n, r, c->basis[0].p, beta);
+    if (cgs) {
+      std::vector<double*> ptrs(cycle + 1);
+      for (int i = 0; i <= cycle; ++i) ptrs[i] = c->basis[i].p;
+      if (c->bptr.n < ptrs.size()) c->bptr.alloc(std::max<size_t>(ptrs.size(), 64));
+      KKT_CUDA(cudaMemcpyAsync(c->bptr.p, ptrs.data(), sizeof(double*) * ptrs.size(),
+                               cudaMemcpyHostToDevice, c->stream));
+    }
     std::vector<std::vector<double>> H;
     std::vector<double> gv(cycle + 1, 0.0), cs(cycle, 0.0), sn(cycle, 0.0);
     gv[0] = beta;
     int k = 0;
     double* w = c->g_w.p;
     double* z = c->g_z.p;
-    std::vector<double> hh(cycle + 2);
+    std::vector<double> hh(cycle + 3);
     for (int j = 0; j < cycle; ++j) {
       if (have_prec) {
         c->tbegin(1);
@@ -472,6 +723,20 @@ int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* his
         c->tend(0);
       }
       c->tbegin(2);
+      if (cgs) {
+        icwy_orthogonalise(c, w, c->bptr.p, c->basis[j].p, j, hd, hd + hstride, c->gram.p, ldg);
+        c->tend(2);
+        int bad = 0;
+        KKT_CUDA(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c->stream));
+        KKT_CUDA(cudaMemcpyAsync(&bad, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        KKT_CUDA(cudaStreamSynchronize(c->stream));
+        if (bad) {
+          throw Error(KKT_EDIVERGED,
+                      "gmres: non-finite values in Krylov vector at iteration " +
+                          std::to_string(total_iters + 1),
+                      total_iters + 1);
+        }
+      } else {
       // ---- modified Gram-Schmidt, fused (gmres.cpp:92-96)
       {
         DotArgs A{kDotPlain, n, w, nullptr, nullptr, c->basis[0].p, hd + 0, c->flag.p};
@@ -490,13 +755,14 @@ int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* his
       KKT_CUDA(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c->stream));
       KKT_CUDA(cudaMemcpyAsync(&bad, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       KKT_CUDA(cudaStreamSynchronize(c->stream));
-      c->tcollect();
       if (bad) {
         throw Error(KKT_EDIVERGED,
                     "gmres: non-finite values in Krylov vector at iteration " +
                         std::to_string(total_iters + 1),
                     total_iters + 1);
       }
+      }
+      c->tcollect();
       H.emplace_back(j + 2, 0.0);
       auto& h = H[j];
       for (int i = 0; i <= j; ++i) h[i] = hh[i];

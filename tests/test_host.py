@@ -138,9 +138,12 @@ def test_bench_roofline_bytes():
     spec.loader.exec_module(bench)
     p = P.config(1)
     vec = 3 * 512 * 16129 * 8
-    # 44 iterations of GMRES(30): j = 0..29 then 0..13, (4j + 5) vector passes each
-    b, launches = bench.mgs_model(p, 44)
+    # 44 iterations of GMRES(30): j = 0..29 then 0..13
+    b, launches = bench.mgs_model(p, 44, mode="strict")   # MGS: (4j + 5) vector passes
     assert b == (4 * (435 + 91) + 5 * 44) * vec and launches == (435 + 91) + 2 * 44
-    assert bench.mgs_model(p, 44, ranks=2)[0] == b // 2
+    assert bench.mgs_model(p, 44, ranks=2, mode="strict")[0] == b // 2
+    b, launches = bench.mgs_model(p, 44)                  # one-reduction MGS: (2j + 5)
+    assert b == (2 * (435 + 91) + 5 * 44) * vec
+    assert launches == sum(2 * -(-(j + 1) // 16) + 1 for j in list(range(30)) + list(range(14)))
     # four transform passes: 2 * 2 * Nt * n_sp * (nx + ny) FLOPs
     assert bench.spectral_flops(p) == 4 * 512 * 16129 * 254
