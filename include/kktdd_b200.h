@@ -64,7 +64,13 @@ enum { KKT_SIGN_PLUS = 0, KKT_SIGN_MINUS = 1 };
  *  FAST:   the performance path: FMA, deterministic tree reductions, blocked
  *          triangular solves with inverted diagonal blocks, fused two-level
  *          residual.  Rounding-level differences only. */
-enum { KKT_MODE_FAST = 0, KKT_MODE_STRICT = 1 };
+enum { KKT_MODE_FAST = 0, KKT_MODE_STRICT = 1, KKT_MODE_SPECTRAL = 2 };
+/*  SPECTRAL: FAST arithmetic, but the spatial solves inside RASQ use Ahat's
+ *          sine eigenbasis (fp64 tensor-core transforms + one scalar time
+ *          recurrence per eigenmode) instead of the reference's banded-LU
+ *          substitution.  Same linear operator to rounding, but NOT the
+ *          reference's method (north_star asks for the LU method), so it is
+ *          opt-in and reported separately; FAST is the headline path. */
 
 /* POD mirror of ProblemConfig (config.hpp:35-68) + GmresParams (:23-28).
  * Field meanings and defaults are the reference's. */

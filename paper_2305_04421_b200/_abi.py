@@ -16,6 +16,8 @@ KKT_EUNSUPPORTED = 7
 
 MODE_FAST = 0
 MODE_STRICT = 1
+MODE_SPECTRAL = 2
+MODES = {"fast": MODE_FAST, "strict": MODE_STRICT, "spectral": MODE_SPECTRAL}
 
 
 class ProblemDesc(C.Structure):

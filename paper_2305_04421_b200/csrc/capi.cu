@@ -91,6 +91,11 @@ void setup(Ctx* c, const kkt_problem_desc& d, const kkt_runtime_opts* o) {
   validate(d);
   c->desc = d;
   c->mode = o ? o->mode : KKT_MODE_FAST;
+  if (c->mode == KKT_MODE_SPECTRAL) {  // FAST arithmetic + eigenbasis spatial solves
+    c->mode = KKT_MODE_FAST;
+    c->spectral = true;
+  }
+  if (c->mode != KKT_MODE_FAST && c->mode != KKT_MODE_STRICT) throw Error(KKT_EINVAL, "unknown mode");
   c->rank = o ? o->rank : 0;
   c->nranks = o ? o->nranks : 1;
   if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks)
@@ -178,9 +183,9 @@ void setup(Ctx* c, const kkt_problem_desc& d, const kkt_runtime_opts* o) {
     build_factor(c);
     if (c->mode == KKT_MODE_FAST) build_block_inverses(c);
   }
-  // FAST RASQ in Ahat's eigenbasis (spectral.cu); KKT_NO_SPECTRAL keeps the
-  // block-LU chains (sweep_group.cu / sweep_tma.cu / sweep_fast.cu)
-  if (c->mode == KKT_MODE_FAST) build_spectral(c);
+  // SPECTRAL mode only: RASQ in Ahat's eigenbasis (spectral.cu).  FAST keeps
+  // the reference's LU method (sweep_group.cu / sweep_tma.cu / sweep_fast.cu).
+  if (c->spectral) build_spectral(c);
   if (d.precond == KKT_PRECOND_TWO_LEVEL) build_coarse(c);
   KKT_CUDA(cudaStreamSynchronize(c->stream));
 }

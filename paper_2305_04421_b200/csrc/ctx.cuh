@@ -64,6 +64,7 @@ struct CoarseColumn {
 struct Ctx {
   kkt_problem_desc desc{};
   int mode = KKT_MODE_FAST;
+  bool spectral = false;           // KKT_MODE_SPECTRAL: eigenbasis RASQ (spectral.cu)
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;

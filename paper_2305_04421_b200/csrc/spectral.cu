@@ -1,4 +1,4 @@
-// spectral.cu — FAST-mode RASQ (K5) in Ahat's eigenbasis.
+// spectral.cu — SPECTRAL-mode RASQ (K5) in Ahat's eigenbasis (opt-in).
 //
 // Ahat = A - sigma*dt*I (heat_operators.cpp:16-20, :24-44) is the constant-
 // coefficient 5-point operator on the nx-by-ny interior grid with homogeneous
@@ -21,7 +21,10 @@
 // resident nx x nx / ny x ny sine matrices.  No sequential chain of spatial
 // solves remains: the dependency depth per apply is 2m scalar steps.
 //
-// STRICT mode keeps the reference-order banded substitution (sweep_strict.cu).
+// This is NOT the reference's spatial-solve method (banded LU, linalg.cpp:
+// 127-162), so it runs only in the opt-in KKT_MODE_SPECTRAL; FAST keeps the
+// LU block substitution (sweep_group.cu), STRICT the reference-order banded
+// substitution (sweep_strict.cu).
 #include <cmath>
 #include <cstdlib>
 #include <vector>
@@ -205,7 +208,6 @@ __global__ void rasq_modes_kernel(RecParams P) {
 bool spectral_enabled(const Ctx* c) { return c->sp_x.p != nullptr; }
 
 void build_spectral(Ctx* c) {
-  if (std::getenv("KKT_NO_SPECTRAL")) return;
   const int nx = c->nx, ny = c->ny, nsp = c->nsp;
   auto sine = [](int n) {
     std::vector<double> S(size_t(n) * n);

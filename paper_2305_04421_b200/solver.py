@@ -155,7 +155,9 @@ class HeatKKT:
             stream = torch.cuda.Stream(device=self.device)
         self.stream = stream
         self._nccl_id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        opts = RuntimeOpts(mode=_abi.MODE_STRICT if mode == "strict" else _abi.MODE_FAST,
+        if mode not in _abi.MODES:
+            raise ValueError(f"mode must be one of {sorted(_abi.MODES)}, got {mode!r}")
+        opts = RuntimeOpts(mode=_abi.MODES[mode],
                            device=device, rank=rank, nranks=nranks,
                            nccl_unique_id=C.cast(self._nccl_id, C.c_void_p) if self._nccl_id else None,
                            stream=C.c_void_p(stream.cuda_stream),

@@ -147,3 +147,13 @@ def test_bench_roofline_bytes():
     assert launches == sum(2 * -(-(j + 1) // 16) + 1 for j in list(range(30)) + list(range(14)))
     # four transform passes: 2 * 2 * Nt * n_sp * (nx + ny) FLOPs
     assert bench.spectral_flops(p) == 4 * 512 * 16129 * 254
+    # RASQ sweep: (2Nt + Nd - 1) * 5 planes + (2m+1) * F
+    F = 8 * 16129 * (2 * 127 + 1)
+    assert bench.sweep_bytes(p) == (2 * 512 + 15) * 5 * 16129 * 8 + 65 * F
+
+
+def test_mode_names():
+    assert _abi.MODES == {"fast": 0, "strict": 1, "spectral": 2}
+    txt = open(HEADER).read()
+    assert "KKT_MODE_SPECTRAL = 2" in txt
+
