@@ -38,5 +38,9 @@ bool group_supported(const Ctx* c);
 void build_group_operators(Ctx* c);
 void group_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms);
 void tma_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms);
+bool v4_supported(const Ctx* c);
+int v4_group_size(const Ctx* c);
+void build_v4(Ctx* c, const double* G, const double* H, const double* Li, const double* dinv);
+void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms);
 
 }  // namespace kkt

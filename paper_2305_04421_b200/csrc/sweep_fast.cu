@@ -162,6 +162,10 @@ __global__ void __launch_bounds__(kFastThreads) fast_chain_kernel(FastParams P,
 
 void fast_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms) {
   if (nchains <= 0 || nsteps <= 0) return;
+  if (c->v4_ops.p) {
+    v4_chains(c, jobs_dev, nchains, nsteps, coarse_terms);
+    return;
+  }
   if (c->Phi.p) {
     group_chains(c, jobs_dev, nchains, nsteps, coarse_terms);
     return;

@@ -529,9 +529,11 @@ void build_group_operators(Ctx* c) {
   const int nx = c->nx, ny = c->ny;
   // group size: balance phase A (g steps) against phase B (NG-1 steps), keeping
   // NG * Nd phase-A CTAs within one wave of the 148 SMs
+  const bool v4 = v4_supported(c);
   int g = 16;
   while (g > 4 && (ny + g - 1) / g * c->Nd <= kSmCount / 2) g /= 2;
   while ((ny + g - 1) / g * c->Nd > kSmCount && g < ny) g *= 2;
+  if (v4) g = v4_group_size(c);  // v4: one wave of 8-CTA clusters per chain set
   if (g > ny) g = ny;
   c->grp_g = g;
   c->grp_n = (ny + g - 1) / g;
@@ -626,6 +628,15 @@ void build_group_operators(Ctx* c) {
         KKT_CUDA(cudaStreamSynchronize(c->stream));
       }
     }
+  }
+  if (v4) {
+    build_v4(c, G.p, H.p, c->Li.p, dinv.p);
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+    c->Phi.release();
+    c->Psi.release();
+    c->grp_tl.release();
+    c->grp_tu.release();
+    return;
   }
   pin_operators_in_l2(c);
   c->grp_y.alloc(size_t(c->Nd) * c->nsp);
