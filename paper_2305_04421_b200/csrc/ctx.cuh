@@ -118,8 +118,8 @@ struct Ctx {
   DBuf<double> arena;              // one allocation for the sweep operators (L2-persisting window)
   // fast v4 (sweep_v4.cu): fragment-ordered operators, chain state, B-phase items
   DBuf<double> v4_ops, v4_state, v4_zero, v4_la;
-  DBuf<int2> v4_items;
-  int v4_maxp = 0, v4_nitemsL = 0, v4_nitemsU = 0, v4_nsets = 0;
+  DBuf<unsigned> v4_flags;
+  int v4_nsets = 0;
   // spectral FAST RASQ (spectral.cu): sine matrices, eigenvalues, T(1), scratch
   DBuf<double> sp_x, sp_y, sp_lam, sp_chat, sp_halo, sp_w1, sp_w2;
 

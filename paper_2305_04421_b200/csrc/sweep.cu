@@ -23,6 +23,20 @@ namespace {
 // Job descriptors go to a per-context device arena.  The H2D copy from
 // pageable memory returns only after the data is staged, and the stream
 // orders it after every kernel still reading the previous descriptors.
+// The fast chains fold the previous step's inflow correction into the next
+// step (sweep_v4.cu), which needs every step's `add` to be the same chain's
+// previous `out` (or null).  All job builders below satisfy this; check it.
+void check_fast_jobs(const std::vector<FastStep>& jobs, int nchains, int nsteps) {
+  for (int s = 0; s < nchains; ++s)
+    for (int t = 0; t < nsteps; ++t) {
+      const FastStep& j = jobs[size_t(s) * nsteps + t];
+      if (!j.in || !j.add) continue;
+      const FastStep* pv = t > 0 ? &jobs[size_t(s) * nsteps + t - 1] : nullptr;
+      if (!pv || !pv->in || pv->out != j.add)
+        throw Error(KKT_EINVAL, "fast chain step: add is not the previous step's out");
+    }
+}
+
 template <class T>
 const T* upload(Ctx* c, DBuf<char>& buf, const std::vector<T>& v) {
   const size_t bytes = v.size() * sizeof(T);
@@ -45,6 +59,7 @@ void band_solve(Ctx* c, double* b, int nrhs, bool transpose) {
   } else {
     std::vector<FastStep> jobs(nrhs);
     for (int k = 0; k < nrhs; ++k) jobs[k] = {b + k * nsp, nullptr, b + k * nsp, nullptr, 1.0, 0, 0};
+    check_fast_jobs(jobs, nrhs, 1);
     fast_chains(c, upload(c, c->jobs_fast, jobs), nrhs, 1, false);
   }
 }
@@ -71,6 +86,7 @@ void window_solve(Ctx* c, double* b, int len, bool adjoint) {
       if (adjoint && k < len - 1) add = b + (k + 1) * nsp;
       jobs.push_back({b + k * nsp, add, b + k * nsp, nullptr, 1.0, 0, 0});
     }
+    check_fast_jobs(jobs, 1, len);
     fast_chains(c, upload(c, c->jobs_fast, jobs), 1, len, false);
   }
 }
@@ -150,6 +166,7 @@ void rasq_apply(Ctx* c, const double* r, double* out, bool fused_coarse) {
                       fused_coarse ? n : 0};
     }
   }
+  check_fast_jobs(jobs, Nd, nsteps);
   fast_chains(c, upload(c, c->jobs_fast, jobs), Nd, nsteps, fused_coarse);
 }
 

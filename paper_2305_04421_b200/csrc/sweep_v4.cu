@@ -14,23 +14,31 @@
 // corrections y_J += Phi_J e_{G-1} / x_J += Psi_J f_{G+1}) exactly as in v3.
 // What changes is the mapping onto the machine:
 //
-//  * A (the chain of g block steps of one group) runs on a cluster of 8 CTAs.
-//    CTA r owns block rows 16r..16r+15 of every step and computes them for
-//    ALL 16 chains of a chain set at once as 2x2 m8n8k4 fp64 DMMA tiles, so
-//    each factor element read from shared memory serves 16 right-hand sides.
-//    Matrix row slices arrive by TMA bulk copies (a 3-stage ring, fetched
-//    steps ahead); the 16-row result slice of step q goes to the 7 peer CTAs
-//    with st.async (DSMEM, mbarrier transaction counts), double-buffered.
-//    The off-chain term (c_J or d_J) is computed before waiting for the
-//    peers' slices, so it overlaps the exchange.
-//  * The inflow correction of the previous sweep direction is folded into the
-//    start of the next A kernel (C-part), so a time step is 4 kernels:
-//    A_L(+C_U of the previous step) -> B_L -> A_U(+C_L) -> B_U.
-//  * B (group-boundary values) is split into chunks of kBT propagator
-//    products per CTA; the chunk partials are summed in a fixed order by the
-//    consumer, so every result is deterministic.
-//  * Kernels are chained with programmatic dependent launch and the whole
-//    RASQ application (4*(2m+1)+1 launches) is replayed from a CUDA graph.
+//  * A time step is two kernels, one per sweep direction (A_L, A_U); one
+//    RASQ application is 2(2m+1)+1 launches, chained with programmatic
+//    dependent launch and replayed from a CUDA graph.
+//  * Each group's chain of g block steps runs on a cluster of 8 CTAs.  CTA r
+//    owns block rows 16r..16r+15 of every step and computes them for ALL 16
+//    chains of a chain set at once as 2x2 m8n8k4 fp64 DMMA tiles, so each
+//    operator element read from shared memory serves 16 right-hand sides.
+//    The 16-row result slice of a step goes to the 7 peer CTAs with st.async
+//    (DSMEM, mbarrier transaction counts), double-buffered.
+//  * Warp specialisation: warps 0-3 run the dependent chain (one tile each);
+//    warps 4-7 compute the off-chain term of the rows ahead (c_J / d_J),
+//    handed over through shared memory (mbarriers cready/cfree), write the
+//    previous step's outputs and keep two TMA rings of operator slices full.
+//  * The inflow correction of the previous direction is folded into the
+//    off-chain term through precomputed products: the L sweep's right-hand
+//    side x_{t-1} = x~_{t-1} + Psi f enters as Li x~ + (Li Psi) f, the U
+//    sweep's y = y~ + Phi e as Ut y~ + (Ut Phi) e, so no correction pass
+//    sits between the chains.
+//  * B (group-boundary values from precomputed propagator products) runs at
+//    the tail of each A kernel: each cluster multiplies its own group-end
+//    vector (exchanged to all its CTAs) into its targets' partials, pairs of
+//    clusters i <-> NG-1-i balance the work, and a release/acquire flag
+//    publishes the vector a partner borrows.  The consumer sums the partials
+//    in a fixed order: deterministic.  All clusters of the grid are
+//    co-resident (v4_group_size), so the cross-cluster waits cannot deadlock.
 //
 // Layouts.  Matrices (128x128, zero padded) are stored "fragment ordered":
 // slice r (rows 16r..16r+15) = [ks 32][rt 2][lane 32] with element
@@ -57,8 +65,6 @@ constexpr int kSlice = kRows * kN;   // doubles per matrix slice (16 KB)
 constexpr int kMat = kN * kN;        // doubles per matrix
 constexpr int kVec = kN * kCs;       // doubles per block vector of a chain set
 constexpr int kThr4 = 256;
-constexpr int kRing = 3;
-constexpr int kBT = 2;               // propagator products per B-phase CTA
 constexpr int kCMax = 9;             // C-part operator slices in flight (the slab aliases ring + X + V)
 
 __host__ __device__ inline int tri_idx(int g, int i) { return g * (g - 1) / 2 + i; }  // i < g
@@ -100,9 +106,6 @@ __device__ __forceinline__ void bulk_g2s(double* dst, const double* src, uint32_
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
-}
-__device__ __forceinline__ void l2_prefetch(const double* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void dmma4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -152,28 +155,46 @@ __device__ __forceinline__ void cta_mma(const double* A, const double* B, int kb
 }
 
 // One warp: tile (rt, ct) of D[16 rows x 16 chains] (+)= A_slice x B over
-// k-steps [kb, ke), 4 independent accumulators.
+// k-steps [kb, ke): 4 independent accumulators, operands of the next 4
+// k-steps loaded while the current ones are in the tensor pipe.
 __device__ __forceinline__ void warp_mma(const double* A, const double* B, int kb, int ke, int rt, int ct,
                                          double& d0, double& d1) {
   const int lane = threadIdx.x & 31;
-  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
-  const int boff = ct * 32 + (lane & 3) * 8 + (lane >> 2);
+  double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  const double* Ap = A + rt * 32 + lane;                               // + ks * 64
+  const double* Bp = B + ct * 32 + (lane & 3) * 8 + (lane >> 2);      // + ks * 64
   int ks = kb;
-  for (; ks + 4 <= ke; ks += 4) {
+  const int n4 = (ke - kb) >> 2;
+  if (n4 > 0) {
     double av[4], bv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      av[u] = A[((ks + u) * 2 + rt) * 32 + lane];
-      bv[u] = B[(ks + u) * 64 + boff];
+      av[u] = Ap[(ks + u) * 64];
+      bv[u] = Bp[(ks + u) * 64];
     }
-    dmma4(a0, a1, av[0], bv[0]);
-    dmma4(b0, b1, av[1], bv[1]);
-    dmma4(c0, c1, av[2], bv[2]);
-    dmma4(e0, e1, av[3], bv[3]);
+    for (int it = 1; it < n4; ++it) {
+      double an[4], bn[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        an[u] = Ap[(ks + 4 + u) * 64];
+        bn[u] = Bp[(ks + 4 + u) * 64];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma4(acc[u][0], acc[u][1], av[u], bv[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        av[u] = an[u];
+        bv[u] = bn[u];
+      }
+      ks += 4;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma4(acc[u][0], acc[u][1], av[u], bv[u]);
+    ks += 4;
   }
-  for (; ks < ke; ++ks) dmma4(a0, a1, A[(ks * 2 + rt) * 32 + lane], B[ks * 64 + boff]);
-  d0 += (a0 + b0) + (c0 + e0);
-  d1 += (a1 + b1) + (c1 + e1);
+  for (; ks < ke; ++ks) dmma4(acc[0][0], acc[0][1], Ap[ks * 64], Bp[ks * 64]);
+  d0 += (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+  d1 += (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
@@ -189,8 +210,9 @@ struct V4Params {
   const double* OffL;  // Li_J
   const double* OnU;   // H_J
   const double* OffU;  // Ut_J
-  const double* Phi;   // L inflow propagators (C-part of the U kernel)
-  const double* Psi;   // U inflow propagators (C-part of the L kernel)
+  const double* UPhi;  // Ut_J Phi_J: L inflow propagators seen by the U sweep's d_J
+  const double* Psi;   // U inflow propagators (outputs of the L kernel)
+  const double* LPsi;  // Li_J Psi_J: U inflow propagators seen by the L sweep's c_J
   const double* TL;    // L boundary products
   const double* TU;    // U boundary products (mirrored indices)
   // state
@@ -198,11 +220,10 @@ struct V4Params {
   double* Xt;          // per chain n_sp: xtilde
   double* Yend;        // [set][NG][kVec]: ytilde at each group's last row
   double* Xend;        // [set][NG][kVec]: xtilde at each group's first row
-  double* EP;          // [set][NG][maxp][kVec]: partial sums of e_G - Yend(G)
-  double* FP;          // [set][NG][maxp][kVec]: partial sums of f_G - Xend(G)
-  const int2* bitemsL; // B-phase work items (G, part)
-  const int2* bitemsU;
-  int nitemsL, nitemsU, maxp;
+  double* EP;          // [set][NG target][NG source][kVec]: TL products (L)
+  double* FP;          // [set][NG target][NG source][kVec]: TU products (U)
+  unsigned* flagL;     // [set][NG]: group-end vector published (L kernel)
+  unsigned* flagU;     // [set][NG] (U kernel)
   // problem
   const double* a1;
   const double* a2;
@@ -216,85 +237,92 @@ struct V4Params {
   const double* zeros; // kN zeros: load target of masked-out lanes (branch-free loads)
   const double* LA;    // [J][3][kN]: Li_J a2, Li_J a1, Li_J 1 (two-level residual term)
   int empty;           // debug: KKT_V4_EMPTY=1 kernels return at once (launch floor)
-  int no_l2pf;         // debug: KKT_V4_NO_L2PF disables the L2 prefetch of the next kernels' operators
 };
 
-__device__ __forceinline__ int nparts_L(int G) { return (G + kBT - 1) / kBT; }
 
 // ---------------------------------------------------------------------------
-// A kernel: [C-part of the other direction] then the zero-inflow chain.
-//   L (kU = false), time step t:  C-part  x_{t-1,J} = xt_J + Psi_J f_{G+1}
-//                                 (outputs of step t-1), then y~ chain.
-//   U (kU = true):                C-part  y_J = y~_J + Phi_J e_{G-1} (in place),
-//                                 then x~ chain.
-// `final_only`: the C-part of the last step only (after the last U sweep).
+// A kernel: the zero-inflow chain of one group for one chain set on one 8-CTA
+// cluster (CTA r: block rows 16r..16r+15).  Time step t:
+//   L (kU = false):  y~_J = c_J + G_J y~_{J-1},
+//        c_J = Li_J (in*scale + x~_{t-1,J}) + (Li Psi)_J f_{G+1} - coarse_J
+//     The add operand x_{t-1} = x~_{t-1} + Psi f_{G+1} (the inflow correction
+//     of the previous U sweep) enters through the precomputed Li_J Psi_J, and
+//     the outputs of step t-1, x_{t-1,J} = x~_{t-1,J} + Psi_J f_{G+1}, are
+//     written here by the off-chain warps.  (FastStep.add is the previous
+//     step's out or null, sweep.cu.)
+//   U (kU = true):   x~_J = d_J + H_J x~_{J+1},
+//        d_J = Ut_J y~_J + (Ut Phi)_J e_{G-1}      (y_J = y~_J + Phi_J e_{G-1})
+// `final_only` (L): the outputs of the last step only.
+// Warps 0-3 run the dependent chain (one output tile each): wait for the
+// peers' slices of the previous row, + G_J y~_{J-1} (H_J x~_{J+1}), + the
+// off-chain tile, send the slice to the peers.  Warps 4-7 compute the
+// off-chain tiles of the rows ahead and the outputs, load the operands and
+// refill the operator rings.
 // ---------------------------------------------------------------------------
 template <bool kU>
 __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int final_only) {
   extern __shared__ __align__(128) double sm[];
-  // [ring 3x2 slices | X 2 vectors | V] doubles as the C-part slab of up to
-  // kCMax operator slices (all fetched at once); EV and part follow.
-  double* ring = sm;                      // kRing stages x 2 slices
-  double* X = ring + kRing * 2 * kSlice;  // 2 exchange buffers
-  double* V = X + 2 * kVec;               // 2 off-chain operands (b_J or y_J)
-  double* EV = V + 2 * kVec;              // inflow vector of the C-part
-  double* part = EV + kVec;               // 4 tiles x 32 lanes x 2
-  double* Cb = part + 4 * 32 * 2;         // 2 x (4 tiles x 32 lanes x 2): off-chain tiles
-  double* cslab = sm;
-  __shared__ __align__(8) uint64_t tbar[kRing];
+  double* ringC = sm;                    // 3 on-chain slices
+  double* ringO = ringC + 3 * kSlice;    // 2 x (triangle, M1, M2) off-chain slices
+  double* X = ringO + 6 * kSlice;        // 2 exchange buffers
+  double* V = X + 2 * kVec;              // off-chain operand
+  double* EV = V + kVec;                 // inflow vector f_{G+1} (L) / e_{G-1} (U)
+  double* Cb = EV + kVec;                // 2 x 256: off-chain tiles
+  double* part = Cb + 2 * 256;           // k-half partials (final_only)
+  double* cslab = sm;                    // final_only: kCMax Psi slices (aliases the rings)
+  __shared__ __align__(8) uint64_t tbarC[3], tbarO[2], sfreeC[3], sfreeO[2], xbar[2], cready[2], cfree[2];
   __shared__ __align__(8) uint64_t cbar[kCMax];
-  __shared__ __align__(8) uint64_t xbar[2];
-  __shared__ __align__(8) uint64_t cready[2], cfree[2], sfree[kRing];
-  __shared__ FastStep sj[kCs];   // jobs of step t (chain)
-  __shared__ FastStep sp[kCs];   // jobs of step t-1 (C-part of the L kernel)
+  __shared__ FastStep sj[kCs];   // jobs of step t
+  __shared__ FastStep sp[kCs];   // jobs of step t-1 (outputs written by the L kernel)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = int(cta_rank());
   const int cid = blockIdx.x / kCl;
   const int G = cid % P.NG, set = cid / P.NG;
   const int J0 = G * P.g, J1 = min(P.ny, J0 + P.g) - 1, len = J1 - J0 + 1;
   const int NG = P.NG;
-  const bool cpart = kU ? (!final_only) : (t > 0);
-  const bool cinflow = kU ? (G > 0) : (G < NG - 1);
+  const bool inflow = kU ? (G > 0) : (G < NG - 1);
+  const bool prev = !kU && t > 0;  // this L kernel writes the outputs of step t-1
   const bool chain = !final_only;
-  const double* Cm = kU ? P.Phi : P.Psi;
   const double* On = kU ? P.OnU : P.OnL;
   const double* Off = kU ? P.OffU : P.OffL;
+  const double* M1 = kU ? P.UPhi : P.LPsi;
   // off-chain triangle: Li lower (ks < 4r+4), Ut upper (ks >= 4r)
   const int okb = kU ? 4 * r : 0, oke = kU ? 32 : 4 * r + 4;
-  auto rowC = [&](int i) { return J0 + i; };
   auto rowQ = [&](int q) { return kU ? J1 - q : J0 + q; };
-  // chain stage q: on-chain slice (q > 0) and off-chain triangle
-  auto issue_any = [&](int q) {  // by any one thread
+  const uint32_t tri_bytes = uint32_t(oke - okb) * 64 * 8;
+  // on-chain stage u = row u+1 (row 0 has no inflow), slot u % 3
+  auto issue_on = [&](int u) {
+    if (u + 1 >= len) return;
+    const int J = rowQ(u + 1);
+    mbar_expect_tx(&tbarC[u % 3], kSlice * 8);
+    bulk_g2s(ringC + (u % 3) * kSlice, On + (size_t(J) * kCl + r) * kSlice, kSlice * 8, &tbarC[u % 3]);
+  };
+  // off-chain stage q = row q, slot q % 2: triangle (+ M1, + Psi for prev)
+  const bool use_m1 = inflow && (kU || prev);
+  const bool use_psi = !kU && prev && inflow;
+  auto issue_off = [&](int q) {
     if (q >= len) return;
-    double* dst = ring + (q % kRing) * 2 * kSlice;
-    uint64_t* bar = &tbar[q % kRing];
     const int J = rowQ(q);
-    const uint32_t offb = uint32_t(oke - okb) * 64 * 8;
-    mbar_expect_tx(bar, (q > 0 ? kSlice * 8 : 0) + offb);
-    if (q > 0) bulk_g2s(dst, On + (size_t(J) * kCl + r) * kSlice, kSlice * 8, bar);
-    bulk_g2s(dst + kSlice + okb * 64, Off + (size_t(J) * kCl + r) * kSlice + okb * 64, offb, bar);
-  };
-  auto issue = [&](int q) {
-    if (tid == 0) issue_any(q);
-  };
-  // C-part slices i0 .. i0+n-1, all in flight at once
-  auto issue_c = [&](int i0, int n) {
-    if (tid != 0) return;
-    for (int i = 0; i < n; ++i) {
-      mbar_expect_tx(&cbar[i], kSlice * 8);
-      bulk_g2s(cslab + i * kSlice, Cm + (size_t(rowC(i0 + i)) * kCl + r) * kSlice, kSlice * 8, &cbar[i]);
-    }
+    double* dst = ringO + (q & 1) * 3 * kSlice;
+    const size_t sl = (size_t(J) * kCl + r) * kSlice;
+    mbar_expect_tx(&tbarO[q & 1], tri_bytes + (use_m1 ? kSlice * 8 : 0) + (use_psi ? kSlice * 8 : 0));
+    bulk_g2s(dst + okb * 64, Off + sl + okb * 64, tri_bytes, &tbarO[q & 1]);
+    if (use_m1) bulk_g2s(dst + kSlice, M1 + sl, kSlice * 8, &tbarO[q & 1]);
+    if (use_psi) bulk_g2s(dst + 2 * kSlice, P.Psi + sl, kSlice * 8, &tbarO[q & 1]);
   };
   if (tid == 0) {
-    for (int i = 0; i < kRing; ++i) mbar_init(&tbar[i], 1);
-    for (int i = 0; i < kCMax; ++i) mbar_init(&cbar[i], 1);
-    mbar_init(&xbar[0], 1);
-    mbar_init(&xbar[1], 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&tbarC[i], 1);
+      mbar_init(&sfreeC[i], 128);
+    }
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&tbarO[i], 1);
+      mbar_init(&sfreeO[i], 128);
+      mbar_init(&xbar[i], 1);
       mbar_init(&cready[i], 128);
       mbar_init(&cfree[i], 128);
     }
-    for (int i = 0; i < kRing; ++i) mbar_init(&sfree[i], 256);
+    for (int i = 0; i < kCMax; ++i) mbar_init(&cbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // the job table and the operators are constant during the graph: load them
@@ -303,77 +331,64 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     const int c = set * kCs + tid;
     FastStep z{nullptr, nullptr, nullptr, nullptr, 1.0, 0, 0};
     sj[tid] = (chain && c < P.nchains) ? P.jobs[int64_t(c) * P.nsteps + t] : z;
-    sp[tid] = (!kU && cpart && c < P.nchains) ? P.jobs[int64_t(c) * P.nsteps + (t - 1)] : z;
+    sp[tid] = (prev && c < P.nchains) ? P.jobs[int64_t(c) * P.nsteps + (t - 1)] : z;
   }
-  __syncthreads();
   if (P.empty == 1) {  // debug: launch-overhead floor
     pdl_wait();
     pdl_launch();
     cluster_sync_all();
     return;
   }
-  const bool use_slab = cpart && cinflow;
-  if (use_slab) {
-    issue_c(0, min(len, kCMax));
-  } else if (chain) {
-    issue(0);
-    issue(1);
-  }
-  // Pull the operators of the next two kernels into L2 while this one runs
-  // (the operator set of all four kernels exceeds the L2, so a cyclic sweep
-  // would miss every time): the B kernel of this direction (its propagator
-  // products of group G, slice r) and the A kernel of the other direction
-  // (C-part, on- and off-chain slices of the same group and slice).
-  if (warp == 1 && chain && !P.no_l2pf) {
-    const double* Cn = kU ? P.Psi : P.Phi;
-    const double* Onn = kU ? P.OnL : P.OnU;
-    const double* Offn = kU ? P.OffL : P.OffU;
-    const int nkb = kU ? 0 : 4 * r, nke = kU ? 4 * r + 4 : 32;  // the other triangle
-    for (int i = lane; i < len; i += 32) {
-      const size_t base = (size_t(J0 + i) * kCl + r) * kSlice;
-      l2_prefetch(Cn + base, kSlice * 8);
-      l2_prefetch(Onn + base, kSlice * 8);
-      l2_prefetch(Offn + base + nkb * 64, uint32_t(nke - nkb) * 64 * 8);
-    }
-    const double* T = kU ? P.TU : P.TL;
-    const int nterms = kU ? NG - 1 - G : G;
-    for (int j = lane; j < nterms; j += 32) {
-      const int m = kU ? tri_idx(NG - 1 - G, NG - 1 - (G + 1 + j)) : tri_idx(G, j);
-      l2_prefetch(T + (size_t(m) * kCl + r) * kSlice, kSlice * 8);
+  if (tid == 0) {
+    if (chain) {
+      issue_on(0);
+      issue_on(1);
+      issue_on(2);
+      issue_off(0);
+      issue_off(1);
+    } else if (inflow) {
+      for (int i = 0; i < min(len, kCMax); ++i) {
+        mbar_expect_tx(&cbar[i], kSlice * 8);
+        bulk_g2s(cslab + i * kSlice, P.Psi + (size_t(J0 + i) * kCl + r) * kSlice, kSlice * 8, &cbar[i]);
+      }
     }
   }
+  __syncthreads();
+
   long long* tim = (P.tim && tid == 0) ? P.tim + (size_t(kU) * gridDim.x + blockIdx.x) * 32 : nullptr;
   if (tim) tim[0] = clock64();
   pdl_wait();  // everything below reads the predecessors' outputs
+  // (dependents launch only after every CTA of this grid has started and
+  // triggered, so the cross-cluster waits below cannot be starved by them)
   pdl_launch();
   if (tim) tim[1] = clock64();
 
   const int t4 = warp & 3, rt = t4 >> 1, ct = t4 & 1;
-  const bool owner = warp < 4;  // kh == 0 warps hold the reduced tiles
   const int krow = r * kRows + rt * 8 + (lane >> 2);  // this lane's block row
   const int nch = ct * 8 + 2 * (lane & 3);            // this lane's chain pair
   const int cpair = set * kCs + nch;                  // global chain of the pair's first
 
-  // ---------------- C-part -------------------------------------------------
-  // inflow vector e_{G-1} (U kernel) or f_{G+1} (L kernel): group-end value
-  // plus the chunk partials, summed in a fixed order
-  if (use_slab) {
+  // inflow vector e_{G-1} (U) / f_{G+1} (L): the group-end value plus the
+  // products T y~_end(src) written by the previous kernel of the other
+  // direction, one partial per source group, summed in a fixed order
+  if (inflow && (prev || kU || final_only)) {
     const int Gs = kU ? G - 1 : G + 1;
     const double* endv = (kU ? P.Yend : P.Xend) + (size_t(set) * NG + Gs) * kVec;
-    const double* pp = (kU ? P.EP : P.FP) + (size_t(set) * NG + Gs) * P.maxp * kVec;
-    const int np = kU ? nparts_L(Gs) : nparts_L(NG - 1 - Gs);
+    const double* pp = (kU ? P.EP : P.FP) + (size_t(set) * NG + Gs) * NG * kVec;
+    // sources: L (e_Gs): 0 .. Gs-1; U (f_Gs): Gs+1 .. NG-1
+    const int s0 = kU ? 0 : Gs + 1, s1 = kU ? Gs : NG;
     constexpr int kU8 = kVec / kThr4;
     double v[kU8];
 #pragma unroll
     for (int u = 0; u < kU8; ++u) v[u] = endv[tid + u * kThr4];
-    for (int p0 = 0; p0 < np; p0 += 4) {  // 4 partials' loads in flight at once
+    for (int p0 = s0; p0 < s1; p0 += 4) {  // 4 partials' loads in flight at once
       double w[4][kU8];
 #pragma unroll
       for (int p = 0; p < 4; ++p) {
-        const double* src = p0 + p < np ? pp + size_t(p0 + p) * kVec : P.zeros;
-        const int stride = p0 + p < np ? kThr4 : 0;
+        const bool ok = p0 + p < s1;
+        const double* src = ok ? pp + size_t(p0 + p) * kVec : P.zeros;
 #pragma unroll
-        for (int u = 0; u < kU8; ++u) w[p][u] = src[(p0 + p < np ? tid : 0) + u * stride];
+        for (int u = 0; u < kU8; ++u) w[p][u] = src[ok ? tid + u * kThr4 : 0];
       }
 #pragma unroll
       for (int p = 0; p < 4; ++p)
@@ -383,109 +398,82 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
 #pragma unroll
     for (int u = 0; u < kU8; ++u) EV[tid + u * kThr4] = v[u];
   }
-  // base values of the C-part rows (x~ for L, y~ for U), kCMax rows per batch
-  double base0[kCMax], base1[kCMax];
-  const bool rowok = owner && krow < P.nx;
-  auto load_base = [&](int i0) {
-    const double* src = kU ? P.Yt : P.Xt;
-    const int kr = krow < P.nx ? krow : 0;
-#pragma unroll
-    for (int u = 0; u < kCMax; ++u) {
-      const int ii = i0 + u < len ? i0 + u : 0;
-      const size_t p = size_t(rowC(ii)) * P.nx + kr;
-      base0[u] = src[size_t(cpair) * P.nsp + p];
-      base1[u] = src[size_t(cpair + 1) * P.nsp + p];
-    }
-  };
-  if (cpart) load_base(0);
-  // peer exchange buffers are armed before anyone can send (cluster barrier)
-  if (tid == 0 && chain) {
+  // the other direction's publish flags were last used by the previous
+  // kernel (complete): reset them for its next launch
+  if (tid < NG && r == 0 && G == 0) (kU ? P.flagL : P.flagU)[set * NG + tid] = 0u;
+  if (tid == 0 && chain) {  // peer exchange buffers armed before anyone can send
     mbar_expect_tx(&xbar[0], (kCl - 1) * kRows * kCs * 8);
     mbar_expect_tx(&xbar[1], (kCl - 1) * kRows * kCs * 8);
   }
-  cluster_sync_all();
+  cluster_sync_all();  // also: EV complete, every CTA's barriers armed
   if (tim) tim[2] = clock64();
 
-  if (cpart) {
+  // ---------------- final_only: outputs of the last step --------------------
+  if (final_only) {
     double g2[2] = {0.0, 0.0};
-    if (!kU && P.gam) {
+    if (P.gam) {
 #pragma unroll
       for (int u = 0; u < 2; ++u)
         if (sp[nch + u].out2 && sp[nch + u].node2 > 0) g2[u] = P.gam[sp[nch + u].node2];
     }
-    uint32_t cph = 0;
     for (int i0 = 0; i0 < len; i0 += kCMax) {
-      if (i0 > 0) {
-        load_base(i0);
-        if (use_slab) issue_c(i0, min(len - i0, kCMax));  // the previous batch's reads are done
+      if (i0 > 0 && inflow && tid == 0) {
+        for (int i = 0; i < min(len - i0, kCMax); ++i) {
+          mbar_expect_tx(&cbar[i], kSlice * 8);
+          bulk_g2s(cslab + i * kSlice, P.Psi + (size_t(J0 + i0 + i) * kCl + r) * kSlice, kSlice * 8, &cbar[i]);
+        }
       }
-#pragma unroll
-      for (int u = 0; u < kCMax; ++u) {
-        const int i = i0 + u;
-        if (i >= len) break;
-        const int J = rowC(i);
-        double d0 = base0[u], d1 = base1[u];
-        if (use_slab) {
-          mbar_wait(&cbar[u], cph);
+      for (int u = 0; u < kCMax && i0 + u < len; ++u) {
+        const int J = J0 + i0 + u;
+        double d0 = 0.0, d1 = 0.0;
+        if (inflow) {
+          mbar_wait(&cbar[u], uint32_t(i0 / kCMax) & 1u);
           cta_mma(cslab + u * kSlice, EV, 0, 32, part, d0, d1);
         }
-        if (rowok) {
+        if (warp < 4 && krow < P.nx) {
           const int p = J * P.nx + krow;
 #pragma unroll
           for (int w = 0; w < 2; ++w) {
-            const double x = w ? d1 : d0;
-            if (kU) {
-              if (cinflow && sj[nch + w].in) P.Yt[size_t(cpair + w) * P.nsp + p] = x;
-            } else {
-              const FastStep& st = sp[nch + w];
-              if (st.in) {
-                if (st.out) st.out[p] = x;
-                if (st.out2) st.out2[p] = x + g2[w];
-              }
+            const FastStep& st = sp[nch + w];
+            if (st.in) {
+              const double x = P.Xt[size_t(cpair + w) * P.nsp + p] + (w ? d1 : d0);
+              if (st.out) st.out[p] = x;
+              if (st.out2) st.out2[p] = x + g2[w];
             }
           }
         }
       }
-      cph ^= 1u;
     }
-    // the slab is free (cta_mma ends with __syncthreads): start the chain's ring
-    if (use_slab && chain) {
-      issue(0);
-      issue(1);
-    }
-    cluster_sync_all();  // the group's rows are complete for every CTA of the cluster
+    cluster_sync_all();
+    return;
   }
-  if (tim) tim[3] = clock64();
-  if (!chain) return;
 
   // ---------------- the zero-inflow chain (warp-specialised) -----------------
-  // warps 0-3: the dependent chain, one output tile each:
-  //     wait for the peers' slices of the previous row, + G_J y_{J-1}
-  //     (H_J x_{J+1}), + the off-chain tile, send the slice to the peers.
-  // warps 4-7: the off-chain term of the rows ahead, c_J = Li_J b_J
-  //     (d_J = Ut_J y_J), one tile each, handed over through Cb[q&1]
-  //     (cready/cfree), plus the operand loads and the TMA ring refills.
-  // Ring stage q (on slice + off triangle) is freed by all 256 threads (sfree).
   const uint32_t xb_base = smem_u32(&xbar[0]);  // xbar[1] at +8
   double* ybase = kU ? P.Xt : P.Yt;
   if (warp < 4) {
     for (int q = 0; q < len; ++q) {
       const int J = rowQ(q);
-      const int st = q % kRing;
-      long long m0 = tim ? clock64() : 0;
-      mbar_wait(&tbar[st], uint32_t(q / kRing) & 1u);
+      long long m0 = tim ? clock64() : 0, m1 = m0, m2 = m0;
       double y0 = 0.0, y1 = 0.0;
-      long long m1 = tim ? clock64() : 0, m2 = m1;
       if (q > 0) {
+        const int u = q - 1;
+        // refill: the slot of stage u-1 (row q-1, consumed last step) gets stage u+2
+        if (tid == 0 && u >= 1) {
+          mbar_wait(&sfreeC[(u - 1) % 3], uint32_t((u - 1) / 3) & 1u);
+          issue_on(u + 2);
+        }
+        mbar_wait(&tbarC[u % 3], uint32_t(u / 3) & 1u);
+        if (tim) m1 = clock64();
         const int xb = (q - 1) & 1;
         mbar_wait_cluster(&xbar[xb], uint32_t((q - 1) >> 1) & 1u);
         if (tim) m2 = clock64();
         // re-arm for the next use (peers refill it only after receiving this
         // CTA's next slices, sent below after every chain warp read it)
         if (tid == 0) mbar_expect_tx(&xbar[xb], (kCl - 1) * kRows * kCs * 8);
-        warp_mma(ring + st * 2 * kSlice, X + xb * kVec, 0, 32, rt, ct, y0, y1);
+        warp_mma(ringC + (u % 3) * kSlice, X + xb * kVec, 0, 32, rt, ct, y0, y1);
+        mbar_arrive(&sfreeC[u % 3]);
       }
-      mbar_arrive(&sfree[st]);
       long long m3 = tim ? clock64() : 0;
       mbar_wait(&cready[q & 1], uint32_t(q >> 1) & 1u);
       long long m4 = tim ? clock64() : 0;
@@ -493,7 +481,7 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
       y1 += Cb[(q & 1) * 256 + (t4 * 32 + lane) * 2 + 1];
       mbar_arrive(&cfree[q & 1]);
       const int xi = vidx(krow, nch);
-      if (q + 1 < len) {
+      {  // the last row too: every CTA gets the whole group-end vector (B below)
         double* xs = X + (q & 1) * kVec + xi;
         *reinterpret_cast<double2*>(xs) = make_double2(y0, y1);
         const uint32_t loc = smem_u32(xs);
@@ -506,7 +494,8 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
               "d"(y0), "d"(y1), "r"(mapa_u32(xb_base + 8u * uint32_t(q & 1), peer))
               : "memory");
         }
-      } else {
+      }
+      if (q + 1 == len) {
         // group-end value for the B phase: L -> last row J1, U -> first row J0
         double* ev = (kU ? P.Xend : P.Yend) + (size_t(set) * NG + G) * kVec + xi;
         *reinterpret_cast<double2*>(ev) = make_double2(y0, y1);
@@ -532,17 +521,21 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     const int vn = 4 * (warp - 4) + (lane >> 3), vk0 = lane & 7;
     const FastStep vst = sj[vn];
     const bool vact = vst.in != nullptr;
+    // add = x_{t-1} = x~_{t-1} + Psi f (sweep.cu: add is the previous out); the
+    // adjoint turn step's in is the previous out too (in = out(t-1))
+    const bool vadd = !kU && vact && vst.add != nullptr;
+    const bool vinp = !kU && vact && prev && sp[vn].in && vst.in == sp[vn].out;
+    const double* xsrc = kU ? P.Yt : P.Xt;
     double xin[16], xad[16];
     auto load_v = [&](int J) {
       // every address valid (masked lanes read `zeros`), so all loads issue at once
       const double* pin;
-      const double* padd;
+      const double* padd = P.zeros;
       if (kU) {
-        pin = vact ? P.Yt + size_t(set * kCs + vn) * P.nsp + size_t(J) * P.nx : P.zeros;
-        padd = P.zeros;
+        pin = vact ? xsrc + size_t(set * kCs + vn) * P.nsp + size_t(J) * P.nx : P.zeros;
       } else {
-        pin = vact ? vst.in + size_t(J) * P.nx : P.zeros;
-        padd = (vact && vst.add) ? vst.add + size_t(J) * P.nx : P.zeros;
+        pin = vact ? (vinp ? xsrc + size_t(set * kCs + vn) * P.nsp : vst.in) + size_t(J) * P.nx : P.zeros;
+        if (vadd) padd = xsrc + size_t(set * kCs + vn) * P.nsp + size_t(J) * P.nx;
       }
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
@@ -551,155 +544,182 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
         if (!kU) xad[u] = padd[k];
       }
     };
-    auto store_v = [&](int b) {
+    auto store_v = [&]() {
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int k = vk0 + 8 * u;
         const double v = kU ? xin[u] : fma(xin[u], vst.scale, xad[u]);
-        V[b * kVec + vidx(k, vn)] = (vact && k < P.nx) ? v : 0.0;
+        V[vidx(k, vn)] = (vact && k < P.nx) ? v : 0.0;
       }
     };
-    // the two-level residual term of the L right-hand side, b -= (Shat y_c)_node / ms,
-    // enters after the product: Li_J (Shat y_c) = al*Li a2 - be*Li a1 + ga*Li 1
-    // with per-chain scalars from the coarse values gamma (sweep.cu jobs, node)
-    const bool lacoef = !kU && P.coarse;
+    // per-chain scalars of this lane's chain pair
     double al[2] = {0.0, 0.0}, be[2] = {0.0, 0.0}, ga[2] = {0.0, 0.0};
-    if (lacoef) {
+    double addm[2] = {0.0, 0.0};
+    const bool lacoef = !kU && P.coarse;
 #pragma unroll
-      for (int w = 0; w < 2; ++w) {
-        const FastStep& sw = sj[nch + w];
-        if (sw.in && sw.node > 0) {
-          const double gn = P.gam[sw.node], gp = P.gam[sw.node + 1];
-          const bool d = sw.node != 1;
-          const double gm = d ? P.gam[sw.node - 1] : 0.0;
-          al[w] = gn * P.inv_ms;
-          be[w] = (gp + gm) * P.inv_ms;
-          ga[w] = d ? gn * P.inv_ms : 0.0;
-        }
+    for (int w = 0; w < 2; ++w) {
+      const FastStep& sw = sj[nch + w];
+      // coefficient of (Li Psi)_J f: the add operand, plus in*scale when in is
+      // the previous out
+      const bool inp = !kU && prev && sw.in && sp[nch + w].in && sw.in == sp[nch + w].out;
+      addm[w] = (!kU && sw.in) ? ((sw.add ? 1.0 : 0.0) + (inp ? sw.scale : 0.0)) : 0.0;
+      // the two-level residual term, b -= (Shat y_c)_node / ms, after the
+      // product: Li_J (Shat y_c) = al*Li a2 - be*Li a1 + ga*Li 1
+      if (lacoef && sw.in && sw.node > 0) {
+        const double gn = P.gam[sw.node], gp = P.gam[sw.node + 1];
+        const bool d = sw.node != 1;
+        const double gm = d ? P.gam[sw.node - 1] : 0.0;
+        al[w] = gn * P.inv_ms;
+        be[w] = (gp + gm) * P.inv_ms;
+        ga[w] = d ? gn * P.inv_ms : 0.0;
       }
     }
-    double la2 = 0.0, la1 = 0.0, la0 = 0.0;
-    auto load_la = [&](int J) {
-      if (!lacoef) return;
-      const double* la = P.LA + size_t(J) * 3 * kN + (krow < kN ? krow : 0);  // Li a2, Li a1, Li 1
-      la2 = la[0];
-      la1 = la[kN];
-      la0 = la[2 * kN];
+    double og2[2] = {0.0, 0.0};
+#pragma unroll
+    for (int w = 0; w < 2; ++w)
+      if (prev && sp[nch + w].out2 && sp[nch + w].node2 > 0 && P.gam) og2[w] = P.gam[sp[nch + w].node2];
+    double la2 = 0.0, la1 = 0.0, la0 = 0.0, nx0 = 0.0, nx1 = 0.0;
+    auto load_row = [&](int J) {  // per-lane row data: the LA terms, x~_{t-1} of the outputs
+      const int kr = krow < P.nx ? krow : 0;
+      if (prev) {
+        const size_t p = size_t(J) * P.nx + kr;
+        nx0 = P.Xt[size_t(cpair) * P.nsp + p];
+        nx1 = P.Xt[size_t(cpair + 1) * P.nsp + p];
+      }
+      if (lacoef) {
+        const double* la = P.LA + size_t(J) * 3 * kN + kr;  // Li a2, Li a1, Li 1
+        la2 = la[0];
+        la1 = la[kN];
+        la0 = la[2 * kN];
+      }
     };
     load_v(rowQ(0));
-    load_la(rowQ(0));
-    store_v(0);
+    load_row(rowQ(0));
+    store_v();
     if (len > 1) load_v(rowQ(1));
     named_bar_sync(1, 128);
+    long long* otim = (P.tim && ot == 0) ? P.tim + (size_t(kU) * gridDim.x + blockIdx.x) * 32 : nullptr;
     for (int q = 0; q < len; ++q) {
-      const int st = q % kRing;
-      const double cl2 = la2, cl1 = la1, cl0 = la0;
-      if (q + 1 < len) load_la(rowQ(q + 1));
-      mbar_wait(&tbar[st], uint32_t(q / kRing) & 1u);
+      const int J = rowQ(q);
+      const double cl2 = la2, cl1 = la1, cl0 = la0, ox0 = nx0, ox1 = nx1;
+      if (q + 1 < len) load_row(rowQ(q + 1));
+      long long n0 = otim ? clock64() : 0;
+      mbar_wait(&tbarO[q & 1], uint32_t(q >> 1) & 1u);
+      long long n1 = otim ? clock64() : 0;
+      const double* so = ringO + (q & 1) * 3 * kSlice;
       double c0 = 0.0, c1 = 0.0;
-      warp_mma(ring + st * 2 * kSlice + kSlice, V + (q & 1) * kVec, okb, oke, rt, ct, c0, c1);
-      mbar_arrive(&sfree[st]);
+      warp_mma(so, V, okb, oke, rt, ct, c0, c1);  // Li_J b / Ut_J y~
+      if (use_m1) {
+        double m0v = 0.0, m1v = 0.0;
+        warp_mma(so + kSlice, EV, 0, 32, rt, ct, m0v, m1v);  // (Li Psi)_J f / (Ut Phi)_J e
+        if (kU) {
+          c0 += m0v;
+          c1 += m1v;
+        } else {
+          c0 += addm[0] * m0v;
+          c1 += addm[1] * m1v;
+        }
+      }
       if (lacoef && krow < P.nx) {
         c0 -= al[0] * cl2 - be[0] * cl1 + ga[0] * cl0;
         c1 -= al[1] * cl2 - be[1] * cl1 + ga[1] * cl0;
       }
+      long long n2 = otim ? clock64() : 0;
       if (q >= 2) mbar_wait(&cfree[q & 1], uint32_t((q >> 1) - 1) & 1u);
+      long long n3 = otim ? clock64() : 0;
       Cb[(q & 1) * 256 + (t4 * 32 + lane) * 2] = c0;
       Cb[(q & 1) * 256 + (t4 * 32 + lane) * 2 + 1] = c1;
       mbar_arrive(&cready[q & 1]);
-      // refill: stage q+kRing-1 goes to the slot of stage q-1 once both
-      // groups are done with it
-      if (ot == 0 && q + kRing - 1 < len) {
-        if (q >= 1) mbar_wait(&sfree[(q - 1) % kRing], uint32_t((q - 1) / kRing) & 1u);
-        issue_any(q + kRing - 1);
+      if (prev) {  // outputs of step t-1: x_{t-1,J} = x~_{t-1,J} + Psi_J f
+        double o0 = ox0, o1 = ox1;
+        if (use_psi) warp_mma(so + 2 * kSlice, EV, 0, 32, rt, ct, o0, o1);
+        if (krow < P.nx) {
+          const int p = J * P.nx + krow;
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            const FastStep& st = sp[nch + w];
+            if (st.in) {
+              const double x = w ? o1 : o0;
+              if (st.out) st.out[p] = x;
+              if (st.out2) st.out2[p] = x + og2[w];
+            }
+          }
+        }
       }
+      named_bar_sync(1, 128);  // every off warp is done with V and off stage q
+      if (ot == 0) issue_off(q + 2);
+      long long n4 = otim ? clock64() : 0;
       if (q + 1 < len) {
-        named_bar_sync(1, 128);  // every off warp is done reading V[(q+1)&1] (row q-1)
-        store_v((q + 1) & 1);
+        store_v();
         if (q + 2 < len) load_v(rowQ(q + 2));
-        named_bar_sync(1, 128);  // V[(q+1)&1] complete
+        named_bar_sync(1, 128);  // V complete
+      }
+      if (otim) {
+        const long long n5 = clock64();
+        otim[25] += n1 - n0;  // off: ring wait
+        otim[26] += n2 - n1;  // off: products
+        otim[27] += n3 - n2;  // off: cfree wait
+        otim[28] += n4 - n3;  // off: handoff + barrier + refill
+        otim[29] += n5 - n4;  // off: operand stage
       }
     }
   }
   if (tim) tim[31] = clock64();
-  cluster_sync_all();  // no CTA exits while a peer may still address its shared memory
-}
 
-// ---------------------------------------------------------------------------
-// B kernel: chunk partials of the boundary values
-//   L: e_G - Yend(G) = sum_{i<G} TL_{G,i} Yend(i)
-//   U: f_G - Xend(G) = sum_{i>G} TU_{m(G),m(i)} Xend(i),  m(x) = NG-1-x
-// one CTA per (set, item = (G, chunk), row slice r); up to kBT products.
-// ---------------------------------------------------------------------------
-template <bool kU>
-__global__ void __launch_bounds__(kThr4) v4B_kernel(V4Params P) {
-  extern __shared__ __align__(128) double sm[];
-  double* ring = sm;                 // 2 stages x (T slice + vector)
-  double* part = ring + 2 * (kSlice + kVec);
-  __shared__ __align__(8) uint64_t bar[2];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int nitems = kU ? P.nitemsU : P.nitemsL;
-  const int r = blockIdx.x % kCl;
-  const int it = (blockIdx.x / kCl) % nitems;
-  const int set = blockIdx.x / (kCl * nitems);
-  const int2 item = (kU ? P.bitemsU : P.bitemsL)[it];
-  const int G = item.x, chunk = item.y;
-  const int NG = P.NG;
-  const int nterms = kU ? NG - 1 - G : G;
-  const int i0 = chunk * kBT, i1 = min(nterms, i0 + kBT);
-  const double* T = kU ? P.TU : P.TL;
+  // ---------------- B: products for the boundary values ---------------------
+  //   L: e_G = y~_end(G) + sum_{i<G} TL_{G,i} y~_end(i)
+  //   U: f_G = x~_first(G) + sum_{i>G} TU_{m(G),m(i)} x~_first(i),  m(x) = NG-1-x
+  // The cluster of source group i computes the products with its own
+  // group-end vector (in X after the last exchange) for its targets; pairs
+  // i <-> NG-1-i share the work so no cluster computes more than
+  // ceil((NG-1)/2) products (the borrowed ones wait for the partner's
+  // published vector).  Results: one partial per (target, source).
+  unsigned* flags = (kU ? P.flagU : P.flagL) + set * NG;
   const double* endv = (kU ? P.Xend : P.Yend) + size_t(set) * NG * kVec;
-  auto src_group = [&](int j) { return kU ? G + 1 + j : j; };
-  auto tmat = [&](int j) { return kU ? tri_idx(NG - 1 - G, NG - 1 - src_group(j)) : tri_idx(G, j); };
-  if (P.empty) {  // debug: launch-overhead floor
-    pdl_wait();
-    pdl_launch();
-    return;
-  }
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
+  if (tid == 0) __threadfence();  // this CTA's group-end slice before the flag
   __syncthreads();
-  auto issue_T = [&](int j) {  // operator slice: independent of the predecessors
-    if (tid == 0 && j < i1) {
-      double* dst = ring + ((j - i0) & 1) * (kSlice + kVec);
-      mbar_expect_tx(&bar[(j - i0) & 1], (kSlice + kVec) * 8);
-      bulk_g2s(dst, T + (size_t(tmat(j)) * kCl + r) * kSlice, kSlice * 8, &bar[(j - i0) & 1]);
+  cluster_sync_all();
+  if (tid == 0 && r == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(flags + G), "r"(1u) : "memory");
+  const int half = NG / 2;  // ceil((NG-1)/2)
+  const int pg = NG - 1 - G;
+  // targets of source x: L -> x+1 .. NG-1, U -> 0 .. x-1 (count NG-1-x / x)
+  auto ntarg = [&](int x) { return kU ? x : NG - 1 - x; };
+  auto targ = [&](int x, int k) { return kU ? x - 1 - k : x + 1 + k; };
+  const int nown = min(ntarg(G), half);
+  const int nbor = (pg != G && ntarg(pg) > half) ? ntarg(pg) - half : 0;
+  const double* T = kU ? P.TU : P.TL;
+  auto tm = [&](int tg, int src) { return kU ? tri_idx(NG - 1 - tg, NG - 1 - src) : tri_idx(tg, src); };
+  double* stage = sm;  // the rings are free now (9 slices)
+  if (tid == 0) {
+    for (int k = 0; k < nown + nbor; ++k) {
+      const int src = k < nown ? G : pg;
+      const int tg = k < nown ? targ(G, k) : targ(pg, half + (k - nown));
+      mbar_expect_tx(&cbar[k], kSlice * 8 + (k == nown ? kVec * 8 : 0));
+      bulk_g2s(stage + k * kSlice, T + (size_t(tm(tg, src)) * kCl + r) * kSlice, kSlice * 8, &cbar[k]);
     }
-  };
-  auto issue_v = [&](int j) {
-    if (tid == 0 && j < i1) {
-      double* dst = ring + ((j - i0) & 1) * (kSlice + kVec) + kSlice;
-      bulk_g2s(dst, endv + size_t(src_group(j)) * kVec, kVec * 8, &bar[(j - i0) & 1]);
+    if (nbor > 0) {  // the partner's vector, once it is published
+      unsigned v = 0;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flags + pg) : "memory");
+      } while (v == 0u);
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      bulk_g2s(stage + 8 * kSlice, endv + size_t(pg) * kVec, kVec * 8, &cbar[nown]);
     }
-  };
-  issue_T(i0);
-  issue_T(i0 + 1);
-  pdl_wait();
-  pdl_launch();
-
-  issue_v(i0);
-  issue_v(i0 + 1);
-  double d0 = 0.0, d1 = 0.0;
-  uint32_t ph = 0;
-  for (int j = i0; j < i1; ++j) {
-    const int b = (j - i0) & 1;
-    mbar_wait(&bar[b], (ph >> b) & 1u);
-    ph ^= 1u << b;
-    const double* st = ring + b * (kSlice + kVec);
-    cta_mma(st, st + kSlice, 0, 32, part, d0, d1);  // ends with __syncthreads: stage free
-    issue_T(j + 2);
-    issue_v(j + 2);
   }
-  if (threadIdx.x < 128) {
-    const int warp = threadIdx.x >> 5, t4 = warp & 3, rt = t4 >> 1, ct = t4 & 1;
-    const int krow = r * kRows + rt * 8 + (lane >> 2);
-    const int nch = ct * 8 + 2 * (lane & 3);
-    double* out = (kU ? P.FP : P.EP) + ((size_t(set) * NG + G) * P.maxp + chunk) * kVec + vidx(krow, nch);
-    *reinterpret_cast<double2*>(out) = make_double2(d0, d1);
+  const double* ownv = X + ((len - 1) & 1) * kVec;
+  mbar_wait_cluster(&xbar[(len - 1) & 1], uint32_t((len - 1) >> 1) & 1u);  // last exchange complete
+  for (int k = 0; k < nown + nbor; ++k) {
+    const int src = k < nown ? G : pg;
+    const int tg = k < nown ? targ(G, k) : targ(pg, half + (k - nown));
+    mbar_wait(&cbar[k], 0u);
+    double e0 = 0.0, e1 = 0.0;
+    cta_mma(stage + k * kSlice, k < nown ? ownv : stage + 8 * kSlice, 0, 32, part, e0, e1);
+    if (warp < 4) {
+      double* out = (kU ? P.FP : P.EP) + ((size_t(set) * NG + tg) * NG + src) * kVec + vidx(krow, nch);
+      *reinterpret_cast<double2*>(out) = make_double2(e0, e1);
+    }
   }
+  cluster_sync_all();  // no CTA exits while a peer may still address its shared memory
 }
 
 // ---------------------------------------------------------------------------
@@ -743,6 +763,27 @@ __global__ void la_kernel(const double* __restrict__ OffL, const double* __restr
   LA[(size_t(J) * 3 + 2) * kN + a] = s0;
 }
 
+// C_J = A_J B_J (kN x kN, zero padded), A_J = Li_J (mode 0) or Li_J^T D_J^{-1}
+// (mode 1) from the square inverse blocks (nx x nx), B_J dense kN x kN (setup)
+__global__ void lmul_kernel(const double* __restrict__ Li, const double* __restrict__ dinv, int nx, int mode,
+                            const double* __restrict__ B, double* __restrict__ C) {
+  const int J = blockIdx.x;
+  const double* L = Li + size_t(J) * nx * nx;
+  const double* Bj = B + size_t(J) * kMat;
+  for (int e = threadIdx.x; e < kMat; e += blockDim.x) {
+    const int a = e / kN, b = e % kN;
+    double acc = 0.0;
+    if (a < nx) {
+      if (mode == 0) {
+        for (int k = 0; k <= a; ++k) acc = fma(L[a * nx + k], Bj[k * kN + b], acc);
+      } else {
+        for (int k = a; k < nx; ++k) acc = fma(L[k * nx + a] * dinv[J * nx + k], Bj[k * kN + b], acc);
+      }
+    }
+    C[size_t(J) * kMat + e] = acc;
+  }
+}
+
 void launch_ex(Ctx* c, const void* fn, int grid, size_t smem, bool cluster, void** args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -767,8 +808,7 @@ void launch_ex(Ctx* c, const void* fn, int grid, size_t smem, bool cluster, void
   c->launches++;
 }
 
-size_t smemA() { return sizeof(double) * (size_t(kRing) * 2 * kSlice + 5 * size_t(kVec) + 3 * 4 * 32 * 2); }
-size_t smemB() { return sizeof(double) * (2 * size_t(kSlice + kVec) + 4 * 32 * 2); }
+size_t smemA() { return sizeof(double) * (9 * size_t(kSlice) + 4 * size_t(kVec) + 3 * 4 * 32 * 2); }
 
 }  // namespace
 
@@ -779,8 +819,6 @@ void set_v4_attributes() {
   if (done) return;
   KKT_CUDA(cudaFuncSetAttribute(v4A_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemA())));
   KKT_CUDA(cudaFuncSetAttribute(v4A_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemA())));
-  KKT_CUDA(cudaFuncSetAttribute(v4B_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemB())));
-  KKT_CUDA(cudaFuncSetAttribute(v4B_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smemB())));
   done = true;
 }
 
@@ -822,66 +860,33 @@ void build_v4(Ctx* c, const double* G, const double* H, const double* Li, const 
   const int nx = c->nx, ny = c->ny, NG = c->grp_n;
   const int ntri = std::max(1, NG * (NG - 1) / 2);
   const size_t per = size_t(ny) * kMat;
-  c->v4_ops.alloc(6 * per + 2 * size_t(ntri) * kMat);
+  c->v4_ops.alloc(7 * per + 2 * size_t(ntri) * kMat);
   double* base = c->v4_ops.p;
   auto pack = [&](const double* src, int64_t sstride, int ld, int n, int mode, int count, double* dst) {
     const dim3 grid(16, count);
     KKT_LAUNCH(c, frag_pack_kernel, grid, 256, 0, src, sstride, ld, n, mode, dinv, nx, dst);
   };
-  pack(G, kMat, kN, nx, 0, ny, base + 0 * per);                    // OnL
-  pack(Li, int64_t(nx) * nx, nx, nx, 0, ny, base + 1 * per);       // OffL
-  pack(H, kMat, kN, nx, 0, ny, base + 2 * per);                    // OnU
-  pack(Li, int64_t(nx) * nx, nx, nx, 1, ny, base + 3 * per);       // OffU = Li^T D^{-1}
-  pack(c->Phi.p, kMat, kN, nx, 0, ny, base + 4 * per);
-  pack(c->Psi.p, kMat, kN, nx, 0, ny, base + 5 * per);
+  pack(G, kMat, kN, nx, 0, ny, base + 0 * per);                    // OnL  = G_J
+  pack(Li, int64_t(nx) * nx, nx, nx, 0, ny, base + 1 * per);       // OffL = Li_J
+  pack(H, kMat, kN, nx, 0, ny, base + 2 * per);                    // OnU  = H_J
+  pack(Li, int64_t(nx) * nx, nx, nx, 1, ny, base + 3 * per);       // OffU = Li_J^T D_J^{-1}
+  {
+    // the inflow propagators as the other sweep sees them: Ut_J Phi_J, Li_J Psi_J
+    DBuf<double> tmp(per);
+    KKT_LAUNCH(c, lmul_kernel, ny, 256, 0, Li, dinv, nx, 1, c->Phi.p, tmp.p);
+    pack(tmp.p, kMat, kN, nx, 0, ny, base + 4 * per);              // UPhi
+    KKT_LAUNCH(c, lmul_kernel, ny, 256, 0, Li, dinv, nx, 0, c->Psi.p, tmp.p);
+    pack(tmp.p, kMat, kN, nx, 0, ny, base + 6 * per);              // LPsi
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  pack(c->Psi.p, kMat, kN, nx, 0, ny, base + 5 * per);             // Psi
   if (NG > 1) {
-    pack(c->grp_tl.p, kMat, kN, nx, 0, NG * (NG - 1) / 2, base + 6 * per);
-    pack(c->grp_tu.p, kMat, kN, nx, 0, NG * (NG - 1) / 2, base + 6 * per + size_t(ntri) * kMat);
+    pack(c->grp_tl.p, kMat, kN, nx, 0, NG * (NG - 1) / 2, base + 7 * per);
+    pack(c->grp_tu.p, kMat, kN, nx, 0, NG * (NG - 1) / 2, base + 7 * per + size_t(ntri) * kMat);
   }
-  static_assert(kCMax * kSlice <= kRing * 2 * kSlice + 3 * kVec, "C slab exceeds ring + X + V");
-  // The operators are re-read every time step (131 MB at config 1, more than
-  // the L2 holds, so a cyclic sweep would miss every time): mark as much of
-  // them as the persisting carve-out allows as L2-persisting.
-  if (!getenv("KKT_NO_L2PIN")) {
-    int max_persist = 0, max_window = 0;
-    KKT_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device));
-    KKT_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device));
-    if (max_persist > 0 && max_window > 0) {
-      const size_t bytes = std::min(sizeof(double) * c->v4_ops.n, size_t(max_window));
-      const size_t carve = std::min(bytes, size_t(max_persist));
-      KKT_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
-      cudaStreamAttrValue attr{};
-      attr.accessPolicyWindow.base_ptr = c->v4_ops.p;
-      attr.accessPolicyWindow.num_bytes = bytes;
-      attr.accessPolicyWindow.hitRatio = float(std::min(1.0, double(carve) / double(bytes)));
-      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      KKT_CUDA(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
-      if (getenv("KKT_V4_TIM"))
-        fprintf(stderr, "v4: L2 persisting carve %zu of window %zu (max persist %d, max window %d)\n", carve, bytes,
-                max_persist, max_window);
-    }
-  }
-  // B-phase work items
-  std::vector<int2> iL, iU;
-  int maxp = 1;
-  for (int Gg = 0; Gg < NG; ++Gg) {
-    const int nl = (Gg + kBT - 1) / kBT, nu = (NG - 1 - Gg + kBT - 1) / kBT;
-    for (int p = 0; p < nl; ++p) iL.push_back(make_int2(Gg, p));
-    for (int p = 0; p < nu; ++p) iU.push_back(make_int2(Gg, p));
-    maxp = std::max(maxp, std::max(nl, nu));
-  }
-  c->v4_maxp = maxp;
+  static_assert(kCMax <= 9, "the C slab aliases the 9 ring slices");
   c->v4_zero.alloc(kN);
   KKT_CUDA(cudaMemsetAsync(c->v4_zero.p, 0, sizeof(double) * kN, c->stream));
-  c->v4_nitemsL = int(iL.size());
-  c->v4_nitemsU = int(iU.size());
-  c->v4_items.alloc(iL.size() + iU.size() + 1);
-  if (!iL.empty())
-    KKT_CUDA(cudaMemcpyAsync(c->v4_items.p, iL.data(), sizeof(int2) * iL.size(), cudaMemcpyHostToDevice, c->stream));
-  if (!iU.empty())
-    KKT_CUDA(cudaMemcpyAsync(c->v4_items.p + iL.size(), iU.data(), sizeof(int2) * iU.size(),
-                             cudaMemcpyHostToDevice, c->stream));
   KKT_CUDA(cudaStreamSynchronize(c->stream));
   set_v4_attributes();
 }
@@ -899,8 +904,10 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
       if (e.exec) cudaGraphExecDestroy(e.exec);
     c->graphs.clear();
     const size_t nvec = size_t(nsets) * NG * kVec;
-    c->v4_state.alloc(size_t(2 * nsets * kCs) * c->nsp + 2 * nvec * (1 + c->v4_maxp));
+    c->v4_state.alloc(size_t(2 * nsets * kCs) * c->nsp + 2 * nvec + 2 * nvec * NG);
     KKT_CUDA(cudaMemsetAsync(c->v4_state.p, 0, sizeof(double) * c->v4_state.n, c->stream));
+    c->v4_flags.alloc(size_t(2) * nsets * NG);
+    KKT_CUDA(cudaMemsetAsync(c->v4_flags.p, 0, sizeof(unsigned) * c->v4_flags.n, c->stream));
     c->v4_nsets = nsets;
   }
   const int nsets_alloc = c->v4_nsets;
@@ -913,10 +920,11 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.OffL = ops + per;
   P.OnU = ops + 2 * per;
   P.OffU = ops + 3 * per;
-  P.Phi = ops + 4 * per;
+  P.UPhi = ops + 4 * per;
   P.Psi = ops + 5 * per;
-  P.TL = ops + 6 * per;
-  P.TU = ops + 6 * per + size_t(ntri) * kMat;
+  P.LPsi = ops + 6 * per;
+  P.TL = ops + 7 * per;
+  P.TU = ops + 7 * per + size_t(ntri) * kMat;
   double* st = c->v4_state.p;
   P.Yt = st;
   P.Xt = st + size_t(nsets_alloc * kCs) * c->nsp;
@@ -924,12 +932,9 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.Yend = vb;
   P.Xend = vb + nveca;
   P.EP = vb + 2 * nveca;
-  P.FP = vb + 2 * nveca + nveca * c->v4_maxp;
-  P.bitemsL = c->v4_items.p;
-  P.bitemsU = c->v4_items.p + c->v4_nitemsL;
-  P.nitemsL = c->v4_nitemsL;
-  P.nitemsU = c->v4_nitemsU;
-  P.maxp = c->v4_maxp;
+  P.FP = vb + 2 * nveca + nveca * NG;
+  P.flagL = c->v4_flags.p;
+  P.flagU = c->v4_flags.p + size_t(nsets_alloc) * NG;
   P.a1 = c->a1.p;
   P.a2 = c->a2.p;
   P.gam = c->gam.p;
@@ -950,7 +955,6 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
     KKT_LAUNCH(c, la_kernel, c->ny, kN, 0, P.OffL, c->a1.p, c->a2.p, c->nx, c->v4_la.p);
   }
   P.LA = c->v4_la.p;
-  P.no_l2pf = getenv("KKT_V4_NO_L2PF") ? 1 : 0;
   P.empty = getenv("KKT_V4_EMPTY") ? atoi(getenv("KKT_V4_EMPTY")) : 0;
   static const bool tim_on = getenv("KKT_V4_TIM") != nullptr;
   P.tim = nullptr;
@@ -961,7 +965,7 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
     P.tim = timbuf.p;
   }
   const int gridA = nsets * NG * kCl;
-  const size_t sA = smemA(), sB = smemB();
+  const size_t sA = smemA();
   auto sequence = [&]() {
     for (int t = 0; t <= nsteps; ++t) {
       int fin = t == nsteps ? 1 : 0;
@@ -970,18 +974,10 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
         launch_ex(c, reinterpret_cast<const void*>(&v4A_kernel<false>), gridA, sA, true, args);
       }
       if (fin) break;
-      if (P.nitemsL > 0) {
-        void* args[] = {&P};
-        launch_ex(c, reinterpret_cast<const void*>(&v4B_kernel<false>), nsets * P.nitemsL * kCl, sB, false, args);
-      }
       {
         int zero = 0;
         void* args[] = {&P, &t, &zero};
         launch_ex(c, reinterpret_cast<const void*>(&v4A_kernel<true>), gridA, sA, true, args);
-      }
-      if (P.nitemsU > 0) {
-        void* args[] = {&P};
-        launch_ex(c, reinterpret_cast<const void*>(&v4B_kernel<true>), nsets * P.nitemsU * kCl, sB, false, args);
       }
     }
   };
@@ -1004,7 +1000,7 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
           ++cnt;
           long long prev = m[0];
           for (int i = 1; i < 32; ++i) {
-            if (i >= 20 && i <= 25) {
+            if (i >= 20 && i <= 29) {
               acc[i] += double(m[i]);
               continue;
             }
@@ -1015,8 +1011,10 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
                 acc[1] / cnt, acc[2] / cnt, acc[3] / cnt);
         for (int i = 4; i < 16; ++i)
           if (acc[i] > 0) fprintf(stderr, " %.0f", acc[i] / cnt);
-        fprintf(stderr, " | tail %.0f | sums: tma %.0f xwait %.0f on %.0f cwait %.0f send %.0f (unused %.0f)\n", acc[31] / cnt,
-                acc[20] / cnt, acc[21] / cnt, acc[22] / cnt, acc[23] / cnt, acc[24] / cnt, acc[25] / cnt);
+        const double ns = 65.0 * 9.0 * cnt;  // per step (config-1 shape)
+        fprintf(stderr, " | tail %.0f | per step: chain tma %.0f xwait %.0f on %.0f cwait %.0f send %.0f | off ring %.0f mma %.0f cfree %.0f hand %.0f stage %.0f\n",
+                acc[31] / cnt, acc[20] / ns, acc[21] / ns, acc[22] / ns, acc[23] / ns, acc[24] / ns, acc[25] / ns,
+                acc[26] / ns, acc[27] / ns, acc[28] / ns, acc[29] / ns);
       }
     }
     return;
