@@ -642,8 +642,8 @@ int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* his
   const int64_t n = 3 * c->B;
   const bool have_prec = P.precond != KKT_PRECOND_NONE;
   ensure_reduction(c);
-  // FAST: two-pass classical Gram-Schmidt with selective reorthogonalisation
-  // (cgs_pass); KKT_MGS=1 keeps MGS in FAST mode too
+  // FAST: MGS in its one-reduction (ICWY) form, icwy_orthogonalise above;
+  // KKT_MGS=1 keeps the reference-order MGS in FAST mode too
   static const bool force_mgs = std::getenv("KKT_MGS") != nullptr;
   const bool cgs = c->mode == KKT_MODE_FAST && !force_mgs;
   const size_t hstride = size_t(P.max_iters) + 8 + kMD;
