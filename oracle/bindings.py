@@ -231,6 +231,24 @@ class Ref(_Base):
         d["converged"] = bool(d["converged"])
         return d, buf.value.decode(), x
 
+    # -- the f3 sweeps (experiments.cpp:97-177) ----------------------------
+    @classmethod
+    def sweep_csv(cls, base: Problem, kind: str, omegas, preconds, steps=0, nts=(), nt=0, nd=0):
+        """to_csv(weak_scaling_sweep(...)) (kind "weak") or to_csv(omega_sweep(...))
+        (kind "omega") of the reference itself."""
+        from paper_2305_04421_b200.problems import PRECOND
+        desc = desc_from_problem(base)
+        ia = (C.c_int * max(1, len(nts)))(*nts)
+        oa = (C.c_double * max(1, len(omegas)))(*omegas)
+        pa = (C.c_int * max(1, len(preconds)))(*[PRECOND[p] for p in preconds])
+        buf = C.create_string_buffer(1 << 16)
+        lib = cls.lib()
+        st = lib.ref_sweep_csv(0 if kind == "weak" else 1, C.byref(desc), steps, nt, nd, ia, len(nts), oa,
+                               len(omegas), pa, len(preconds), buf, C.c_int(len(buf)))
+        if st != 0:
+            raise OracleError(st, lib.ref_error().decode(), lib.ref_error_index())
+        return buf.value.decode()
+
     def model_rhs(self):
         """(b, target samples) of assemble_rhs(ops, model_initial_condition, model_target)."""
         b = np.empty(3 * self.block)

@@ -354,6 +354,26 @@ int ref_run_single(const kkt_problem_desc* d, kkt_run_record* rec, double* x, ch
   });
 }
 
+// The reference's own sweeps (experiments.cpp:97-142) and their CSV
+// (experiments.cpp:144-177): the f3 records the device sweeps mirror.
+// kind 0: weak_scaling_sweep(base, steps, nts, omegas, preconds)
+// kind 1: omega_sweep(base, nt, nd, omegas, preconds)
+int ref_sweep_csv(int kind, const kkt_problem_desc* d, int steps, int nt, int nd, const int* nts,
+                  int n_nts, const double* omegas, int n_omegas, const int* preconds, int n_preconds,
+                  char* csv, int csv_cap) {
+  return guarded([&] {
+    ProblemConfig base = to_cfg(d);
+    std::vector<int> ntl(nts, nts + n_nts);
+    std::vector<double> oml(omegas, omegas + n_omegas);
+    std::vector<PrecondKind> pl;
+    for (int i = 0; i < n_preconds; ++i) pl.push_back(static_cast<PrecondKind>(preconds[i]));
+    const SweepResult sw = kind == 0 ? weak_scaling_sweep(base, steps, ntl, oml, pl)
+                                     : omega_sweep(base, nt, nd, oml, pl);
+    const std::string text = to_csv(sw);
+    std::snprintf(csv, static_cast<std::size_t>(csv_cap), "%s", text.c_str());
+  });
+}
+
 // assemble_rhs(ops, model_initial_condition, model_target).to_kkt() and the
 // target samples evaluate_objective uses (kkt.cpp:88-108).
 int ref_model_rhs(void* vc, double* b, double* target) {

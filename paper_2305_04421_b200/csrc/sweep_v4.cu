@@ -517,8 +517,10 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     }
   } else {
     const int ot = tid - 128;  // 0..127
-    // operand loads: warp (w-4) -> chains 4(w-4) + lane/8, rows (lane&7) + 8u
-    const int vn = 4 * (warp - 4) + (lane >> 3), vk0 = lane & 7;
+    // operand loads in fragment order: thread ot owns V[ot + 128u], u < 16,
+    // i.e. chain vn and rows vk0 + 8u (conflict-free shared stores; a warp's
+    // loads cover 8 chains x 4 consecutive rows, whole 32-byte sectors)
+    const int vn = 8 * ((warp - 4) & 1) + (lane & 7), vk0 = 4 * ((warp - 4) >> 1) + ((lane >> 3) & 3);
     const FastStep vst = sj[vn];
     const bool vact = vst.in != nullptr;
     // add = x_{t-1} = x~_{t-1} + Psi f (sweep.cu: add is the previous out); the
@@ -549,7 +551,7 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
       for (int u = 0; u < 16; ++u) {
         const int k = vk0 + 8 * u;
         const double v = kU ? xin[u] : fma(xin[u], vst.scale, xad[u]);
-        V[vidx(k, vn)] = (vact && k < P.nx) ? v : 0.0;
+        V[ot + 128 * u] = (vact && k < P.nx) ? v : 0.0;  // == V[vidx(k, vn)]
       }
     };
     // per-chain scalars of this lane's chain pair
