@@ -13,11 +13,13 @@
 #include <vector>
 
 #include "ctx.cuh"
+#include "sweep.cuh"
 
 namespace kkt {
 
 Ctx::~Ctx() {
   if (stream) cudaStreamSynchronize(stream);
+  v4_unregister(this);
   delete comm;
   for (auto& g : graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);

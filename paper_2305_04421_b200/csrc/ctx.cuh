@@ -120,6 +120,7 @@ struct Ctx {
   DBuf<double> v4_ops, v4_state, v4_zero, v4_la;
   DBuf<unsigned> v4_flags;
   int v4_nsets = 0;
+  bool v4_coop = false, v4_registered = false;
   // spectral FAST RASQ (spectral.cu): sine matrices, eigenvalues, T(1), scratch
   DBuf<double> sp_x, sp_y, sp_lam, sp_chat, sp_halo, sp_w1, sp_w2;
 

@@ -42,5 +42,6 @@ bool v4_supported(const Ctx* c);
 int v4_group_size(const Ctx* c);
 void build_v4(Ctx* c, const double* G, const double* H, const double* Li, const double* dinv);
 void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms);
+void v4_unregister(Ctx* c);
 
 }  // namespace kkt

@@ -47,6 +47,7 @@
 // [ks 32][ct 2][kl 4][nl 8] (row 4ks+kl, chain 8ct+nl): the B operand reads
 // 32 consecutive doubles, the D fragment writes chain pairs as double2, and
 // the rows of CTA r are the contiguous doubles [256r, 256r+256).
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tbarO[i], 1);
-      mbar_init(&sfreeO[i], use_m1 ? 256 : 128);  // chain warps read the M1 slice
+      mbar_init(&sfreeO[i], 128);
       mbar_init(&xbar[i], 1);
       mbar_init(&cready[i], 128);
       mbar_init(&cfree[i], 128);
@@ -452,38 +453,10 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
   const uint32_t xb_base = smem_u32(&xbar[0]);  // xbar[1] at +8
   double* ybase = kU ? P.Xt : P.Yt;
   if (warp < 4) {
-    // coefficient of the inflow term per chain: (Ut Phi) e for every active
-    // chain (U); (Li Psi) f for the add operand plus in*scale when in is the
-    // previous out (L)
-    double addm[2] = {0.0, 0.0};
-#pragma unroll
-    for (int w = 0; w < 2; ++w) {
-      const FastStep& sw = sj[nch + w];
-      if (kU) {
-        addm[w] = sw.in ? 1.0 : 0.0;
-      } else {
-        const bool inp = prev && sw.in && sp[nch + w].in && sw.in == sp[nch + w].out;
-        addm[w] = sw.in ? ((sw.add ? 1.0 : 0.0) + (inp ? sw.scale : 0.0)) : 0.0;
-      }
-    }
-    // the inflow term M1_J * EV of row q (M1 slice in the off ring, stage q):
-    // computed one row ahead, while this row's slices are in flight
-    double mi0 = 0.0, mi1 = 0.0;
-    auto inflow_term = [&](int q) {
-      mi0 = 0.0;
-      mi1 = 0.0;
-      if (!use_m1 || q >= len) return;
-      mbar_wait(&tbarO[q & 1], uint32_t(q >> 1) & 1u);
-      warp_mma(ringO + (q & 1) * 3 * kSlice + kSlice, EV, 0, 32, rt, ct, mi0, mi1);
-      mi0 *= addm[0];
-      mi1 *= addm[1];
-      mbar_arrive(&sfreeO[q & 1]);
-    };
-    inflow_term(0);
     for (int q = 0; q < len; ++q) {
       const int J = rowQ(q);
       long long m0 = tim ? clock64() : 0, m1 = m0, m2 = m0;
-      double y0 = mi0, y1 = mi1;
+      double y0 = 0.0, y1 = 0.0;
       if (q > 0) {
         const int u = q - 1;
         // refill: the slot of stage u-1 (row q-1, consumed last step) gets stage u+2
@@ -533,7 +506,6 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
         if (sj[nch].in) ybase[size_t(cpair) * P.nsp + p] = y0;
         if (sj[nch + 1].in) ybase[size_t(cpair + 1) * P.nsp + p] = y1;
       }
-      inflow_term(q + 1);
       if (tim) {
         const long long m5 = clock64();
         tim[20] += m1 - m0;  // TMA ring wait
@@ -585,10 +557,19 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     };
     // per-chain scalars of this lane's chain pair
     double al[2] = {0.0, 0.0}, be[2] = {0.0, 0.0}, ga[2] = {0.0, 0.0};
+    double addm[2] = {0.0, 0.0};
     const bool lacoef = !kU && P.coarse;
 #pragma unroll
     for (int w = 0; w < 2; ++w) {
       const FastStep& sw = sj[nch + w];
+      // coefficient of the inflow term: (Ut Phi) e for every active chain (U);
+      // (Li Psi) f for the add operand plus in*scale when in is the previous out (L)
+      if (kU) {
+        addm[w] = sw.in ? 1.0 : 0.0;
+      } else {
+        const bool inp = prev && sw.in && sp[nch + w].in && sw.in == sp[nch + w].out;
+        addm[w] = sw.in ? ((sw.add ? 1.0 : 0.0) + (inp ? sw.scale : 0.0)) : 0.0;
+      }
       // the two-level residual term, b -= (Shat y_c)_node / ms, after the
       // product: Li_J (Shat y_c) = al*Li a2 - be*Li a1 + ga*Li 1
       if (lacoef && sw.in && sw.node > 0) {
@@ -635,6 +616,12 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
       const double* so = ringO + (q & 1) * 3 * kSlice;
       double c0 = 0.0, c1 = 0.0;
       warp_mma(so, V, okb, oke, rt, ct, c0, c1);  // Li_J b / Ut_J y~
+      if (use_m1) {
+        double m0v = 0.0, m1v = 0.0;
+        warp_mma(so + kSlice, EV, 0, 32, rt, ct, m0v, m1v);  // (Li Psi)_J f / (Ut Phi)_J e
+        c0 += addm[0] * m0v;
+        c1 += addm[1] * m1v;
+      }
       if (lacoef && krow < P.nx) {
         c0 -= al[0] * cl2 - be[0] * cl1 + ga[0] * cl0;
         c1 -= al[1] * cl2 - be[1] * cl1 + ga[1] * cl0;
@@ -661,12 +648,8 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
           }
         }
       }
-      mbar_arrive(&sfreeO[q & 1]);
       named_bar_sync(1, 128);  // every off warp is done with V and off stage q
-      if (ot == 0 && q + 2 < len) {  // the chain warps read the stage's M1 slice too
-        mbar_wait(&sfreeO[q & 1], uint32_t(q >> 1) & 1u);
-        issue_off(q + 2);
-      }
+      if (ot == 0) issue_off(q + 2);
       long long n4 = otim ? clock64() : 0;
       if (q + 1 < len) {
         store_v();
@@ -809,11 +792,19 @@ void launch_ex(Ctx* c, const void* fn, int grid, size_t smem, bool cluster, void
   cfg.blockDim = dim3(kThr4);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c->stream;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int na = 0;
   attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[na].val.programmaticStreamSerializationAllowed = 1;
   ++na;
+  // the A kernels wait across clusters (B tail): a cooperative launch makes
+  // the driver guarantee that every CTA of the grid is co-resident when other
+  // v4 contexts share the device (v4_register)
+  if (c->v4_coop) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
   if (cluster) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
     attr[na].val.clusterDim.x = kCl;
@@ -832,6 +823,24 @@ size_t smemA() { return sizeof(double) * (9 * size_t(kSlice) + 4 * size_t(kVec) 
 }  // namespace
 
 bool v4_supported(const Ctx* c) { return c->nx <= kN && c->ny >= 2 && !getenv("KKT_SWEEP_V3"); }
+
+// Live v4 contexts per device (this process).  The A kernels wait across
+// clusters, so a grid must not be starved of SMs by another such grid.  One
+// non-cooperative grid alone is safe (cooperative grids are guaranteed their
+// own residency and finish); every context after the first on a device
+// launches cooperatively.  KKT_V4_COOP=0/1 forces the choice.
+static std::atomic<int> g_live_v4[64];
+void v4_register(Ctx* c) {
+  const int d = c->device & 63;
+  const int before = g_live_v4[d].fetch_add(1);
+  c->v4_registered = true;
+  c->v4_coop = before > 0;
+  if (const char* e = getenv("KKT_V4_COOP")) c->v4_coop = atoi(e) != 0;
+}
+void v4_unregister(Ctx* c) {
+  if (c->v4_registered) g_live_v4[c->device & 63].fetch_sub(1);
+  c->v4_registered = false;
+}
 
 void set_v4_attributes() {
   static bool done = false;
@@ -908,6 +917,7 @@ void build_v4(Ctx* c, const double* G, const double* H, const double* Li, const 
   KKT_CUDA(cudaMemsetAsync(c->v4_zero.p, 0, sizeof(double) * kN, c->stream));
   KKT_CUDA(cudaStreamSynchronize(c->stream));
   set_v4_attributes();
+  v4_register(c);
 }
 
 // Run `nsteps` lock-step spatial solves of `nchains` chains (chain-major job

@@ -305,3 +305,21 @@ def test_config1_against_golden():
         e_ref = np.linalg.norm(xs[sel] - xstar[i])
         e_fast = np.linalg.norm(xf[i] - xstar[i])
         assert e_fast <= 2.0 * e_ref + 1e-14 * np.linalg.norm(xstar[i]), ("uzw"[k], e_fast, e_ref)
+
+
+def test_fast_config1_deterministic():
+    """FAST at config-1 size: P^-1 is bitwise reproducible run to run (fixed
+    reduction orders, no atomics) and the full solve takes the reference's 44
+    iterations every time — a race in the sweep's shared-memory pipelines shows
+    up here as drifting iteration counts."""
+    import torch
+    p = P.config(1)
+    k = _kkt(p, "fast")
+    r = torch.from_numpy(P.random_vec(3 * p.block, 5)).cuda()
+    o1 = k.apply_P_inv(r).clone()
+    o2 = k.apply_P_inv(r).clone()
+    assert torch.equal(o1, o2)
+    b = torch.from_numpy(P.kkt_rhs(1, p)).cuda()
+    x = torch.empty_like(b)
+    its = [k.gmres_solve(b, x).iterations for _ in range(2)]
+    assert its == [44, 44], its
