@@ -63,6 +63,17 @@ struct Stencil {
 // bitwise neutral for finite x, so they are skipped.
 // A is symmetric, so band_matvec_transpose (:56-67) yields the same terms in
 // the same order.
+__device__ __forceinline__ double band_row_strict_ij(const Stencil& s, const double* __restrict__ x,
+                                                     int p, int i, int j) {
+  double acc = 0.0;
+  if (j > 0) acc = sadd(acc, smul(s.mcy, x[p - s.nx]));
+  if (i > 0) acc = sadd(acc, smul(s.mcx, x[p - 1]));
+  acc = sadd(acc, smul(s.diag, x[p]));
+  if (i < s.nx - 1) acc = sadd(acc, smul(s.mcx, x[p + 1]));
+  if (j < s.ny - 1) acc = sadd(acc, smul(s.mcy, x[p + s.nx]));
+  return acc;
+}
+
 __device__ __forceinline__ double band_row_strict(const Stencil& s, const double* __restrict__ x,
                                                   int p) {
   const int i = p % s.nx;

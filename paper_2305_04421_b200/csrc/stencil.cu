@@ -5,6 +5,8 @@
 // order in BOTH modes (band_row_strict, common.cuh): for a bandwidth-bound
 // 5-point stencil the unfused mul/add costs nothing, and it makes K v bitwise
 // equal to apply_K (kkt.cpp:50-65) — SURVEY.md §8a-5.
+#include <algorithm>
+
 #include "ctx.cuh"
 
 namespace kkt {
@@ -65,28 +67,32 @@ __global__ void __launch_bounds__(kThreads) scale_kernel(int64_t n, const double
 // With `bm` non-null the kernel writes bm - K v instead (the restart
 // residual r = b - A x of gmres.cpp:50-51, same rounding as a separate pass).
 __global__ void __launch_bounds__(kThreads) apply_K_kernel(Stencil s, int nt, int nsp, double ms,
-                                                           double oms, double dt,
+                                                           double oms, double dt, float inv_nx,
                                                            const double* __restrict__ v,
                                                            double* __restrict__ out,
                                                            const double* __restrict__ bm,
                                                            const double* __restrict__ u_prev,
                                                            const double* __restrict__ w_next) {
+  // grid: x over the points of a plane, y over planes (no 64-bit division);
+  // j = p / nx from a float reciprocal, exact for p < 2^20, nx < 2^11
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nsp) return;
+  const int j = int((float(p) + 0.5f) * inv_nx);
+  const int i = p - j * s.nx;
   const int64_t B = int64_t(nt) * nsp;
   const double* u = v;
   const double* z = v + B;
   const double* w = v + 2 * B;
-  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < B;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const int n0 = int(idx / nsp);
-    const int p = int(idx - int64_t(n0) * nsp);
+  for (int n0 = blockIdx.y; n0 < nt; n0 += gridDim.y) {
     const int64_t off = int64_t(n0) * nsp;
+    const int64_t idx = off + p;
     const double uu = u[idx], zz = z[idx], ww = w[idx];
-    double ou = band_row_strict(s, w + off, p);
+    double ou = band_row_strict_ij(s, w + off, p, i, j);
     if (n0 < nt - 1) ou = ssub(ou, w[idx + nsp]);
     else if (w_next) ou = ssub(ou, w_next[p]);
     ou = sadd(ou, smul(ms, uu));
     const double oz = ssub(smul(oms, zz), smul(dt, ww));
-    double ow = band_row_strict(s, u + off, p);
+    double ow = band_row_strict_ij(s, u + off, p, i, j);
     if (n0 > 0) ow = ssub(ow, u[idx - nsp]);
     else if (u_prev) ow = ssub(ow, u_prev[p]);
     ow = ssub(ow, smul(dt, zz));
@@ -189,8 +195,9 @@ void op_apply_K(Ctx* c, const double* v, double* out, const double* b_minus) {
     if (c->rank > 0) h.prev = hp;
     if (c->rank + 1 < c->nranks) h.next = hn;
   }
-  KKT_LAUNCH(c, apply_K_kernel, grid_for(c->B), kThreads, 0, c->A, c->ntl, c->nsp, c->ms, c->oms,
-             c->dt, v, out, b_minus, h.prev, h.next);
+  const dim3 gK((c->nsp + kThreads - 1) / kThreads, std::min(c->ntl, 128));  // a few planes per thread
+  KKT_LAUNCH(c, apply_K_kernel, gK, kThreads, 0, c->A, c->ntl, c->nsp, c->ms, c->oms, c->dt,
+             1.0f / float(c->nx), v, out, b_minus, h.prev, h.next);
 }
 
 void op_pinv_uz(Ctx* c, const double* r, double* out) {
