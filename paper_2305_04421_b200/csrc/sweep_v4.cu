@@ -217,8 +217,8 @@ struct V4Params {
   const double* TL;    // L boundary products
   const double* TU;    // U boundary products (mirrored indices)
   // state
-  double* Yt;          // per chain n_sp: ytilde, then y (in place)
-  double* Xt;          // per chain n_sp: xtilde
+  double* Yt;          // [set][ny][kVec]: y~ per block row, block-vector fragment layout
+  double* Xt;          // [set][ny][kVec]: x~ per block row, block-vector fragment layout
   double* Yend;        // [set][NG][kVec]: ytilde at each group's last row
   double* Xend;        // [set][NG][kVec]: xtilde at each group's first row
   double* EP;          // [set][NG target][NG source][kVec]: TL products (L)
@@ -283,6 +283,8 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
   const int NG = P.NG;
   const bool inflow = kU ? (G > 0) : (G < NG - 1);
   const bool prev = !kU && t > 0;  // this L kernel writes the outputs of step t-1
+  // chain state of block row J (this chain set), block-vector fragment layout
+  auto frow = [&](double* base, int J) { return base + (size_t(set) * P.ny + J) * kVec; };
   const bool chain = !final_only;
   const double* On = kU ? P.OnU : P.OnL;
   const double* Off = kU ? P.OffU : P.OffL;
@@ -301,15 +303,21 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
   // off-chain stage q = row q, slot q % 2: triangle (+ M1, + Psi for prev)
   const bool use_m1 = inflow && (kU || prev);
   const bool use_psi = !kU && prev && inflow;
+  // (U: the third slot takes the operand y~_J itself, 16 KB from the previous
+  // kernel, so it is copied only after griddepcontrol.wait: issue_off_v)
   auto issue_off = [&](int q) {
     if (q >= len) return;
     const int J = rowQ(q);
     double* dst = ringO + (q & 1) * 3 * kSlice;
     const size_t sl = (size_t(J) * kCl + r) * kSlice;
-    mbar_expect_tx(&tbarO[q & 1], tri_bytes + (use_m1 ? kSlice * 8 : 0) + (use_psi ? kSlice * 8 : 0));
+    mbar_expect_tx(&tbarO[q & 1], tri_bytes + (use_m1 ? kSlice * 8 : 0) + ((use_psi || kU) ? kSlice * 8 : 0));
     bulk_g2s(dst + okb * 64, Off + sl + okb * 64, tri_bytes, &tbarO[q & 1]);
     if (use_m1) bulk_g2s(dst + kSlice, M1 + sl, kSlice * 8, &tbarO[q & 1]);
     if (use_psi) bulk_g2s(dst + 2 * kSlice, P.Psi + sl, kSlice * 8, &tbarO[q & 1]);
+  };
+  auto issue_off_v = [&](int q) {
+    if (!kU || q >= len) return;
+    bulk_g2s(ringO + (q & 1) * 3 * kSlice + 2 * kSlice, frow(P.Yt, rowQ(q)), kVec * 8, &tbarO[q & 1]);
   };
   if (tid == 0) {
     for (int i = 0; i < 3; ++i) {
@@ -362,6 +370,10 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
   // (dependents launch only after every CTA of this grid has started and
   // triggered, so the cross-cluster waits below cannot be starved by them)
   pdl_launch();
+  if (tid == 0 && chain) {
+    issue_off_v(0);
+    issue_off_v(1);
+  }
   if (tim) tim[1] = clock64();
 
   const int t4 = warp & 3, rt = t4 >> 1, ct = t4 & 1;
@@ -437,7 +449,7 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
           for (int w = 0; w < 2; ++w) {
             const FastStep& st = sp[nch + w];
             if (st.in) {
-              const double x = P.Xt[size_t(cpair + w) * P.nsp + p] + (w ? d1 : d0);
+              const double x = frow(P.Xt, J)[vidx(krow, nch) + w] + (w ? d1 : d0);
               if (st.out) st.out[p] = x;
               if (st.out2) st.out2[p] = x + g2[w];
             }
@@ -501,11 +513,8 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
         double* ev = (kU ? P.Xend : P.Yend) + (size_t(set) * NG + G) * kVec + xi;
         *reinterpret_cast<double2*>(ev) = make_double2(y0, y1);
       }
-      if (krow < P.nx) {
-        const int p = J * P.nx + krow;
-        if (sj[nch].in) ybase[size_t(cpair) * P.nsp + p] = y0;
-        if (sj[nch + 1].in) ybase[size_t(cpair + 1) * P.nsp + p] = y1;
-      }
+      // the chain state in fragment layout (inactive chains and padded rows are 0)
+      *reinterpret_cast<double2*>(frow(ybase, J) + xi) = make_double2(y0, y1);
       if (tim) {
         const long long m5 = clock64();
         tim[20] += m1 - m0;  // TMA ring wait
@@ -528,30 +537,28 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     // adjoint turn step's in is the previous out too (in = out(t-1))
     const bool vadd = !kU && vact && vst.add != nullptr;
     const bool vinp = !kU && vact && prev && sp[vn].in && vst.in == sp[vn].out;
-    const double* xsrc = kU ? P.Yt : P.Xt;
+    // L: b = in*scale + x~_{t-1} (the add operand; U takes y~_J by TMA instead).
+    // x~ is read in fragment order (contiguous), `in` in the reference layout.
     double xin[16], xad[16];
     auto load_v = [&](int J) {
+      if (kU) return;
       // every address valid (masked lanes read `zeros`), so all loads issue at once
-      const double* pin;
-      const double* padd = P.zeros;
-      if (kU) {
-        pin = vact ? xsrc + size_t(set * kCs + vn) * P.nsp + size_t(J) * P.nx : P.zeros;
-      } else {
-        pin = vact ? (vinp ? xsrc + size_t(set * kCs + vn) * P.nsp : vst.in) + size_t(J) * P.nx : P.zeros;
-        if (vadd) padd = xsrc + size_t(set * kCs + vn) * P.nsp + size_t(J) * P.nx;
-      }
+      const double* fx = frow(P.Xt, J);
+      const double* pin = (vact && !vinp) ? vst.in + size_t(J) * P.nx : P.zeros;
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int k = vk0 + 8 * u < P.nx ? vk0 + 8 * u : 0;
-        xin[u] = pin[k];
-        if (!kU) xad[u] = padd[k];
+        const int e = ot + 128 * u;  // == vidx(k, vn)
+        xin[u] = vinp ? fx[e] : pin[vinp ? 0 : k];
+        xad[u] = vadd ? fx[e] : 0.0;
       }
     };
     auto store_v = [&]() {
+      if (kU) return;
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int k = vk0 + 8 * u;
-        const double v = kU ? xin[u] : fma(xin[u], vst.scale, xad[u]);
+        const double v = fma(xin[u], vst.scale, xad[u]);
         V[ot + 128 * u] = (vact && k < P.nx) ? v : 0.0;  // == V[vidx(k, vn)]
       }
     };
@@ -589,9 +596,9 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     auto load_row = [&](int J) {  // per-lane row data: the LA terms, x~_{t-1} of the outputs
       const int kr = krow < P.nx ? krow : 0;
       if (prev) {
-        const size_t p = size_t(J) * P.nx + kr;
-        nx0 = P.Xt[size_t(cpair) * P.nsp + p];
-        nx1 = P.Xt[size_t(cpair + 1) * P.nsp + p];
+        const double2 xv = *reinterpret_cast<const double2*>(frow(P.Xt, J) + vidx(krow, nch));
+        nx0 = xv.x;
+        nx1 = xv.y;
       }
       if (lacoef) {
         const double* la = P.LA + size_t(J) * 3 * kN + kr;  // Li a2, Li a1, Li 1
@@ -615,7 +622,7 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
       long long n1 = otim ? clock64() : 0;
       const double* so = ringO + (q & 1) * 3 * kSlice;
       double c0 = 0.0, c1 = 0.0;
-      warp_mma(so, V, okb, oke, rt, ct, c0, c1);  // Li_J b / Ut_J y~
+      warp_mma(so, kU ? so + 2 * kSlice : V, okb, oke, rt, ct, c0, c1);  // Li_J b / Ut_J y~
       if (use_m1) {
         double m0v = 0.0, m1v = 0.0;
         warp_mma(so + kSlice, EV, 0, 32, rt, ct, m0v, m1v);  // (Li Psi)_J f / (Ut Phi)_J e
@@ -649,9 +656,12 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
         }
       }
       named_bar_sync(1, 128);  // every off warp is done with V and off stage q
-      if (ot == 0) issue_off(q + 2);
+      if (ot == 0) {
+        issue_off(q + 2);
+        issue_off_v(q + 2);
+      }
       long long n4 = otim ? clock64() : 0;
-      if (q + 1 < len) {
+      if (!kU && q + 1 < len) {
         store_v();
         if (q + 2 < len) load_v(rowQ(q + 2));
         named_bar_sync(1, 128);  // V complete
@@ -933,7 +943,7 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
       if (e.exec) cudaGraphExecDestroy(e.exec);
     c->graphs.clear();
     const size_t nvec = size_t(nsets) * NG * kVec;
-    c->v4_state.alloc(size_t(2 * nsets * kCs) * c->nsp + 2 * nvec + 2 * nvec * NG);
+    c->v4_state.alloc(size_t(2 * nsets) * c->ny * kVec + 2 * nvec + 2 * nvec * NG);
     KKT_CUDA(cudaMemsetAsync(c->v4_state.p, 0, sizeof(double) * c->v4_state.n, c->stream));
     c->v4_flags.alloc(size_t(2) * nsets * NG);
     KKT_CUDA(cudaMemsetAsync(c->v4_flags.p, 0, sizeof(unsigned) * c->v4_flags.n, c->stream));
@@ -956,8 +966,8 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.TU = ops + 7 * per + size_t(ntri) * kMat;
   double* st = c->v4_state.p;
   P.Yt = st;
-  P.Xt = st + size_t(nsets_alloc * kCs) * c->nsp;
-  double* vb = st + size_t(2 * nsets_alloc * kCs) * c->nsp;
+  P.Xt = st + size_t(nsets_alloc) * c->ny * kVec;
+  double* vb = st + size_t(2 * nsets_alloc) * c->ny * kVec;
   P.Yend = vb;
   P.Xend = vb + nveca;
   P.EP = vb + 2 * nveca;
