@@ -117,7 +117,7 @@ struct Ctx {
   std::vector<Graph> graphs;
   DBuf<double> arena;              // one allocation for the sweep operators (L2-persisting window)
   // fast v4 (sweep_v4.cu): fragment-ordered operators, chain state, B-phase items
-  DBuf<double> v4_ops, v4_state, v4_zero, v4_la;
+  DBuf<double> v4_ops, v4_state, v4_zero, v4_la, v4_hist;
   DBuf<unsigned> v4_flags;
   int v4_nsets = 0;
   bool v4_coop = false, v4_registered = false;

@@ -218,7 +218,11 @@ struct V4Params {
   const double* TU;    // U boundary products (mirrored indices)
   // state
   double* Yt;          // [set][ny][kVec]: y~ per block row, block-vector fragment layout
-  double* Xt;          // [set][ny][kVec]: x~ per block row, block-vector fragment layout
+  double* Xh;          // [step][set][ny][kVec]: x~ of every step (fragment layout)
+  double* Fh;          // [step][set][NG][kVec]: the U boundary values f_G of every step
+  double* Rin;         // [step][set][ny][kVec]: the external `in` operands, gathered
+  const int* insrc;    // [chain][step]: t' when in(t) == out(t') (t' < t), else -1
+  const int* live;     // [chain][step]: bit 0 out, bit 1 out2 is the plane's final write
   double* Yend;        // [set][NG][kVec]: ytilde at each group's last row
   double* Xend;        // [set][NG][kVec]: xtilde at each group's first row
   double* EP;          // [set][NG target][NG source][kVec]: TL products (L)
@@ -245,20 +249,22 @@ struct V4Params {
 // A kernel: the zero-inflow chain of one group for one chain set on one 8-CTA
 // cluster (CTA r: block rows 16r..16r+15).  Time step t:
 //   L (kU = false):  y~_J = c_J + G_J y~_{J-1},
-//        c_J = Li_J (in*scale + x~_{t-1,J}) + (Li Psi)_J f_{G+1} - coarse_J
-//     The add operand x_{t-1} = x~_{t-1} + Psi f_{G+1} (the inflow correction
-//     of the previous U sweep) enters through the precomputed Li_J Psi_J, and
-//     the outputs of step t-1, x_{t-1,J} = x~_{t-1,J} + Psi_J f_{G+1}, are
-//     written here by the off-chain warps.  (FastStep.add is the previous
-//     step's out or null, sweep.cu.)
+//        c_J = Li_J b~_J + (Li Psi)_J f~ - coarse_J
+//     Every step output is x_t = x~_t + Psi f(t) (the inflow correction of the
+//     U sweep); x~_t and f(t) are kept per step (Xh, Fh), so an operand that is
+//     an earlier output — add = x_{t-1} (FastStep.add is the previous step's
+//     out, sweep.cu), or in = x_{t'} at the adjoint steps — enters as
+//     b~ = in*scale + x~_{t-1} (x~_{t'} for in) and f~ = f(t-1) (+ scale
+//     f(t')) per chain, through the precomputed Li_J Psi_J.  External `in`
+//     planes are gathered into fragment layout once per application (Rin);
+//     the outputs are written once at the end (v4_out_kernel).
 //   U (kU = true):   x~_J = d_J + H_J x~_{J+1},
 //        d_J = Ut_J y~_J + (Ut Phi)_J e_{G-1}      (y_J = y~_J + Phi_J e_{G-1})
-// `final_only` (L): the outputs of the last step only.
 // Warps 0-3 run the dependent chain (one output tile each): wait for the
 // peers' slices of the previous row, + G_J y~_{J-1} (H_J x~_{J+1}), + the
 // off-chain tile, send the slice to the peers.  Warps 4-7 compute the
-// off-chain tiles of the rows ahead and the outputs, load the operands and
-// refill the operator rings.
+// off-chain tiles of the rows ahead, load the operands and refill the
+// operator rings.
 // ---------------------------------------------------------------------------
 template <bool kU>
 __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int final_only) {
@@ -269,12 +275,11 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
   double* V = X + 2 * kVec;              // off-chain operand
   double* EV = V + kVec;                 // inflow vector f_{G+1} (L) / e_{G-1} (U)
   double* Cb = EV + kVec;                // 2 x 256: off-chain tiles
-  double* part = Cb + 2 * 256;           // k-half partials (final_only)
-  double* cslab = sm;                    // final_only: kCMax Psi slices (aliases the rings)
+  double* part = Cb + 2 * 256;           // k-half partials (B tail)
   __shared__ __align__(8) uint64_t tbarC[3], tbarO[2], sfreeC[3], sfreeO[2], xbar[2], cready[2], cfree[2];
   __shared__ __align__(8) uint64_t cbar[kCMax];
   __shared__ FastStep sj[kCs];   // jobs of step t
-  __shared__ FastStep sp[kCs];   // jobs of step t-1 (outputs written by the L kernel)
+  __shared__ int sinp[kCs];      // per chain: t' when in(t) == out(t'), else -1
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = int(cta_rank());
   const int cid = blockIdx.x / kCl;
@@ -282,9 +287,9 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
   const int J0 = G * P.g, J1 = min(P.ny, J0 + P.g) - 1, len = J1 - J0 + 1;
   const int NG = P.NG;
   const bool inflow = kU ? (G > 0) : (G < NG - 1);
-  const bool prev = !kU && t > 0;  // this L kernel writes the outputs of step t-1
   // chain state of block row J (this chain set), block-vector fragment layout
   auto frow = [&](double* base, int J) { return base + (size_t(set) * P.ny + J) * kVec; };
+  const size_t hstep = size_t(P.nsets) * P.ny * kVec;  // one step of Xh / Rin
   const bool chain = !final_only;
   const double* On = kU ? P.OnU : P.OnL;
   const double* Off = kU ? P.OffU : P.OffL;
@@ -300,9 +305,8 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     mbar_expect_tx(&tbarC[u % 3], kSlice * 8);
     bulk_g2s(ringC + (u % 3) * kSlice, On + (size_t(J) * kCl + r) * kSlice, kSlice * 8, &tbarC[u % 3]);
   };
-  // off-chain stage q = row q, slot q % 2: triangle (+ M1, + Psi for prev)
-  const bool use_m1 = inflow && (kU || prev);
-  const bool use_psi = !kU && prev && inflow;
+  // off-chain stage q = row q, slot q % 2: triangle (+ M1)
+  const bool use_m1 = inflow && (kU || t > 0);
   // (U: the third slot takes the operand y~_J itself, 16 KB from the previous
   // kernel, so it is copied only after griddepcontrol.wait: issue_off_v)
   auto issue_off = [&](int q) {
@@ -310,10 +314,9 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     const int J = rowQ(q);
     double* dst = ringO + (q & 1) * 3 * kSlice;
     const size_t sl = (size_t(J) * kCl + r) * kSlice;
-    mbar_expect_tx(&tbarO[q & 1], tri_bytes + (use_m1 ? kSlice * 8 : 0) + ((use_psi || kU) ? kSlice * 8 : 0));
+    mbar_expect_tx(&tbarO[q & 1], tri_bytes + (use_m1 ? kSlice * 8 : 0) + (kU ? kSlice * 8 : 0));
     bulk_g2s(dst + okb * 64, Off + sl + okb * 64, tri_bytes, &tbarO[q & 1]);
     if (use_m1) bulk_g2s(dst + kSlice, M1 + sl, kSlice * 8, &tbarO[q & 1]);
-    if (use_psi) bulk_g2s(dst + 2 * kSlice, P.Psi + sl, kSlice * 8, &tbarO[q & 1]);
   };
   auto issue_off_v = [&](int q) {
     if (!kU || q >= len) return;
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     const int c = set * kCs + tid;
     FastStep z{nullptr, nullptr, nullptr, nullptr, 1.0, 0, 0};
     sj[tid] = (chain && c < P.nchains) ? P.jobs[int64_t(c) * P.nsteps + t] : z;
-    sp[tid] = (prev && c < P.nchains) ? P.jobs[int64_t(c) * P.nsteps + (t - 1)] : z;
+    sinp[tid] = (!kU && c < P.nchains) ? P.insrc[int64_t(c) * P.nsteps + t] : -1;
   }
   if (P.empty == 1) {  // debug: launch-overhead floor
     pdl_wait();
@@ -348,22 +351,31 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     cluster_sync_all();
     return;
   }
-  if (tid == 0) {
-    if (chain) {
-      issue_on(0);
-      issue_on(1);
-      issue_on(2);
-      issue_off(0);
-      issue_off(1);
-    } else if (inflow) {
-      for (int i = 0; i < min(len, kCMax); ++i) {
-        mbar_expect_tx(&cbar[i], kSlice * 8);
-        bulk_g2s(cslab + i * kSlice, P.Psi + (size_t(J0 + i) * kCl + r) * kSlice, kSlice * 8, &cbar[i]);
-      }
-    }
+  if (tid == 0 && chain) {
+    issue_on(0);
+    issue_on(1);
+    issue_on(2);
+    issue_off(0);
+    issue_off(1);
   }
   __syncthreads();
 
+  // L: f(t') of the steps whose output is this step's `in` (t' < t-1) was
+  // recorded by kernels that completed before the predecessor started, so it
+  // can be fetched before griddepcontrol.wait
+  constexpr int kU8 = kVec / kThr4;
+  double fpre[kU8];
+  if (!kU && inflow && t > 0) {
+#pragma unroll
+    for (int u = 0; u < kU8; ++u) {
+      const int e = tid + u * kThr4;
+      const int n = 8 * ((e >> 5) & 1) + (e & 7);
+      const int ts = sinp[n];
+      fpre[u] = (sj[n].in && ts >= 0 && ts != t - 1)
+                    ? P.Fh[((size_t(ts) * P.nsets + set) * NG + G + 1) * kVec + e]
+                    : 0.0;
+    }
+  }
   long long* tim = (P.tim && tid == 0) ? P.tim + (size_t(kU) * gridDim.x + blockIdx.x) * 32 : nullptr;
   if (tim) tim[0] = clock64();
   pdl_wait();  // everything below reads the predecessors' outputs
@@ -384,13 +396,12 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
   // inflow vector e_{G-1} (U) / f_{G+1} (L): the group-end value plus the
   // products T y~_end(src) written by the previous kernel of the other
   // direction, one partial per source group, summed in a fixed order
-  if (inflow && (prev || kU || final_only)) {
+  if (inflow && (kU || t > 0)) {
     const int Gs = kU ? G - 1 : G + 1;
     const double* endv = (kU ? P.Yend : P.Xend) + (size_t(set) * NG + Gs) * kVec;
     const double* pp = (kU ? P.EP : P.FP) + (size_t(set) * NG + Gs) * NG * kVec;
     // sources: L (e_Gs): 0 .. Gs-1; U (f_Gs): Gs+1 .. NG-1
     const int s0 = kU ? 0 : Gs + 1, s1 = kU ? Gs : NG;
-    constexpr int kU8 = kVec / kThr4;
     double v[kU8];
 #pragma unroll
     for (int u = 0; u < kU8; ++u) v[u] = endv[tid + u * kThr4];
@@ -408,8 +419,26 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
 #pragma unroll
         for (int u = 0; u < kU8; ++u) v[u] += w[p][u];
     }
+    if (kU) {
 #pragma unroll
-    for (int u = 0; u < kU8; ++u) EV[tid + u * kThr4] = v[u];
+      for (int u = 0; u < kU8; ++u) EV[tid + u * kThr4] = v[u];
+    } else {
+      // f(t-1) of group Gs: record it (this CTA's quarter... its 256-element
+      // slice of rows), then combine per chain column n(e):
+      //   f~ = [add] f(t-1) + [in = out(t')] scale * f(t')
+      double* fh = P.Fh + ((size_t(t - 1) * P.nsets + set) * NG + Gs) * kVec;
+#pragma unroll
+      for (int u = 0; u < kU8; ++u) {
+        const int e = tid + u * kThr4;
+        if ((e >> 8) == r) fh[e] = v[u];
+        const int n = 8 * ((e >> 5) & 1) + (e & 7);
+        const FastStep& st = sj[n];
+        double w = st.in && st.add ? v[u] : 0.0;
+        const int ts = sinp[n];
+        if (st.in && ts >= 0) w = fma(st.scale, ts == t - 1 ? v[u] : fpre[u], w);
+        EV[e] = w;
+      }
+    }
   }
   // the other direction's publish flags were last used by the previous
   // kernel (complete): reset them for its next launch
@@ -421,49 +450,9 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
   cluster_sync_all();  // also: EV complete, every CTA's barriers armed
   if (tim) tim[2] = clock64();
 
-  // ---------------- final_only: outputs of the last step --------------------
-  if (final_only) {
-    double g2[2] = {0.0, 0.0};
-    if (P.gam) {
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-        if (sp[nch + u].out2 && sp[nch + u].node2 > 0) g2[u] = P.gam[sp[nch + u].node2];
-    }
-    for (int i0 = 0; i0 < len; i0 += kCMax) {
-      if (i0 > 0 && inflow && tid == 0) {
-        for (int i = 0; i < min(len - i0, kCMax); ++i) {
-          mbar_expect_tx(&cbar[i], kSlice * 8);
-          bulk_g2s(cslab + i * kSlice, P.Psi + (size_t(J0 + i0 + i) * kCl + r) * kSlice, kSlice * 8, &cbar[i]);
-        }
-      }
-      for (int u = 0; u < kCMax && i0 + u < len; ++u) {
-        const int J = J0 + i0 + u;
-        double d0 = 0.0, d1 = 0.0;
-        if (inflow) {
-          mbar_wait(&cbar[u], uint32_t(i0 / kCMax) & 1u);
-          cta_mma(cslab + u * kSlice, EV, 0, 32, part, d0, d1);
-        }
-        if (warp < 4 && krow < P.nx) {
-          const int p = J * P.nx + krow;
-#pragma unroll
-          for (int w = 0; w < 2; ++w) {
-            const FastStep& st = sp[nch + w];
-            if (st.in) {
-              const double x = frow(P.Xt, J)[vidx(krow, nch) + w] + (w ? d1 : d0);
-              if (st.out) st.out[p] = x;
-              if (st.out2) st.out2[p] = x + g2[w];
-            }
-          }
-        }
-      }
-    }
-    cluster_sync_all();
-    return;
-  }
-
   // ---------------- the zero-inflow chain (warp-specialised) -----------------
   const uint32_t xb_base = smem_u32(&xbar[0]);  // xbar[1] at +8
-  double* ybase = kU ? P.Xt : P.Yt;
+  double* ybase = kU ? P.Xh + size_t(t) * hstep : P.Yt;
   if (warp < 4) {
     for (int q = 0; q < len; ++q) {
       const int J = rowQ(q);
@@ -533,24 +522,24 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     const int vn = 8 * ((warp - 4) & 1) + (lane & 7), vk0 = 4 * ((warp - 4) >> 1) + ((lane >> 3) & 3);
     const FastStep vst = sj[vn];
     const bool vact = vst.in != nullptr;
-    // add = x_{t-1} = x~_{t-1} + Psi f (sweep.cu: add is the previous out); the
-    // adjoint turn step's in is the previous out too (in = out(t-1))
+    // L: b~ = in*scale + x~_{t-1} with in = x~_{t'} when it is an earlier
+    // output (the rest of those outputs, Psi f, is in the combined f~ of EV)
+    // or the gathered external plane; all in fragment order (contiguous).
+    // U takes y~_J by TMA instead.
     const bool vadd = !kU && vact && vst.add != nullptr;
-    const bool vinp = !kU && vact && prev && sp[vn].in && vst.in == sp[vn].out;
-    // L: b = in*scale + x~_{t-1} (the add operand; U takes y~_J by TMA instead).
-    // x~ is read in fragment order (contiguous), `in` in the reference layout.
+    const int vts = kU ? -1 : sinp[vn];
+    const double* srcin = vts >= 0 ? P.Xh + size_t(vts) * hstep : P.Rin + size_t(t) * hstep;
+    const double* srcad = vadd ? P.Xh + size_t(t - 1) * hstep : P.zeros;
     double xin[16], xad[16];
     auto load_v = [&](int J) {
       if (kU) return;
-      // every address valid (masked lanes read `zeros`), so all loads issue at once
-      const double* fx = frow(P.Xt, J);
-      const double* pin = (vact && !vinp) ? vst.in + size_t(J) * P.nx : P.zeros;
+      const double* fi = srcin + (size_t(set) * P.ny + J) * kVec;
+      const double* fa = vadd ? srcad + (size_t(set) * P.ny + J) * kVec : P.zeros;
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
-        const int k = vk0 + 8 * u < P.nx ? vk0 + 8 * u : 0;
-        const int e = ot + 128 * u;  // == vidx(k, vn)
-        xin[u] = vinp ? fx[e] : pin[vinp ? 0 : k];
-        xad[u] = vadd ? fx[e] : 0.0;
+        const int e = ot + 128 * u;  // == vidx(vk0 + 8u, vn)
+        xin[u] = fi[e];
+        xad[u] = fa[vadd ? e : 0];
       }
     };
     auto store_v = [&]() {
@@ -570,13 +559,8 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     for (int w = 0; w < 2; ++w) {
       const FastStep& sw = sj[nch + w];
       // coefficient of the inflow term: (Ut Phi) e for every active chain (U);
-      // (Li Psi) f for the add operand plus in*scale when in is the previous out (L)
-      if (kU) {
-        addm[w] = sw.in ? 1.0 : 0.0;
-      } else {
-        const bool inp = prev && sw.in && sp[nch + w].in && sw.in == sp[nch + w].out;
-        addm[w] = sw.in ? ((sw.add ? 1.0 : 0.0) + (inp ? sw.scale : 0.0)) : 0.0;
-      }
+      // L: the per-chain f~ is already combined in EV
+      addm[w] = sw.in ? 1.0 : 0.0;
       // the two-level residual term, b -= (Shat y_c)_node / ms, after the
       // product: Li_J (Shat y_c) = al*Li a2 - be*Li a1 + ga*Li 1
       if (lacoef && sw.in && sw.node > 0) {
@@ -588,18 +572,9 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
         ga[w] = d ? gn * P.inv_ms : 0.0;
       }
     }
-    double og2[2] = {0.0, 0.0};
-#pragma unroll
-    for (int w = 0; w < 2; ++w)
-      if (prev && sp[nch + w].out2 && sp[nch + w].node2 > 0 && P.gam) og2[w] = P.gam[sp[nch + w].node2];
-    double la2 = 0.0, la1 = 0.0, la0 = 0.0, nx0 = 0.0, nx1 = 0.0;
-    auto load_row = [&](int J) {  // per-lane row data: the LA terms, x~_{t-1} of the outputs
+    double la2 = 0.0, la1 = 0.0, la0 = 0.0;
+    auto load_row = [&](int J) {  // per-lane row data: the LA terms
       const int kr = krow < P.nx ? krow : 0;
-      if (prev) {
-        const double2 xv = *reinterpret_cast<const double2*>(frow(P.Xt, J) + vidx(krow, nch));
-        nx0 = xv.x;
-        nx1 = xv.y;
-      }
       if (lacoef) {
         const double* la = P.LA + size_t(J) * 3 * kN + kr;  // Li a2, Li a1, Li 1
         la2 = la[0];
@@ -615,7 +590,7 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     long long* otim = (P.tim && ot == 0) ? P.tim + (size_t(kU) * gridDim.x + blockIdx.x) * 32 : nullptr;
     for (int q = 0; q < len; ++q) {
       const int J = rowQ(q);
-      const double cl2 = la2, cl1 = la1, cl0 = la0, ox0 = nx0, ox1 = nx1;
+      const double cl2 = la2, cl1 = la1, cl0 = la0;
       if (q + 1 < len) load_row(rowQ(q + 1));
       long long n0 = otim ? clock64() : 0;
       mbar_wait(&tbarO[q & 1], uint32_t(q >> 1) & 1u);
@@ -639,22 +614,6 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
       Cb[(q & 1) * 256 + (t4 * 32 + lane) * 2] = c0;
       Cb[(q & 1) * 256 + (t4 * 32 + lane) * 2 + 1] = c1;
       mbar_arrive(&cready[q & 1]);
-      if (prev) {  // outputs of step t-1: x_{t-1,J} = x~_{t-1,J} + Psi_J f
-        double o0 = ox0, o1 = ox1;
-        if (use_psi) warp_mma(so + 2 * kSlice, EV, 0, 32, rt, ct, o0, o1);
-        if (krow < P.nx) {
-          const int p = J * P.nx + krow;
-#pragma unroll
-          for (int w = 0; w < 2; ++w) {
-            const FastStep& st = sp[nch + w];
-            if (st.in) {
-              const double x = w ? o1 : o0;
-              if (st.out) st.out[p] = x;
-              if (st.out2) st.out2[p] = x + og2[w];
-            }
-          }
-        }
-      }
       named_bar_sync(1, 128);  // every off warp is done with V and off stage q
       if (ot == 0) {
         issue_off(q + 2);
@@ -732,6 +691,139 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     }
   }
   cluster_sync_all();  // no CTA exits while a peer may still address its shared memory
+}
+
+// ---------------------------------------------------------------------------
+// Per application, before the chains: insrc[c][t] = t' when the `in` plane of
+// step t is the `out` plane of an earlier step t' of the same chain (the RASQ
+// adjoint steps read the forward outputs), else -1; and the external `in`
+// planes gathered into the block-vector fragment layout (Rin).
+// ---------------------------------------------------------------------------
+// live[c][t]: bit 0 out(t), bit 1 out2(t) is the final content of its plane
+// (no later step of the chain writes the same plane), so the output pass can
+// write every step in parallel.
+__global__ void v4_insrc_kernel(const FastStep* __restrict__ jobs, int nchains, int nsteps, int* insrc,
+                                int* live) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nchains * nsteps) return;
+  const int c = i / nsteps, t = i - c * nsteps;
+  const FastStep* J = jobs + int64_t(c) * nsteps;
+  int src = -1;
+  if (J[t].in)
+    for (int tp = 0; tp < t; ++tp)
+      if (J[tp].in && J[tp].out == J[t].in) src = tp;
+  insrc[i] = src;
+  int lv = 0;
+  if (J[t].in) {
+    bool o1 = J[t].out != nullptr, o2 = J[t].out2 != nullptr;
+    if (o2 && J[t].out2 == J[t].out) o1 = false;
+    for (int t2 = t + 1; t2 < nsteps; ++t2) {
+      if (!J[t2].in) continue;
+      if (o1 && (J[t2].out == J[t].out || J[t2].out2 == J[t].out)) o1 = false;
+      if (o2 && (J[t2].out == J[t].out2 || J[t2].out2 == J[t].out2)) o2 = false;
+    }
+    lv = (o1 ? 1 : 0) | (o2 ? 2 : 0);
+  }
+  live[i] = lv;
+}
+
+__global__ void v4_gather_kernel(V4Params P) {
+  const int J = blockIdx.x % P.ny;
+  const int set = (blockIdx.x / P.ny) % P.nsets;
+  const int t = blockIdx.x / (P.ny * P.nsets);
+  double* dst = P.Rin + ((size_t(t) * P.nsets + set) * P.ny + J) * kVec;
+  for (int e = threadIdx.x; e < kVec; e += blockDim.x) {
+    const int k = 4 * (e >> 6) + ((e >> 3) & 3);
+    const int n = 8 * ((e >> 5) & 1) + (e & 7);
+    const int c = set * kCs + n;
+    double v = 0.0;
+    if (c < P.nchains && k < P.nx) {
+      const FastStep st = P.jobs[int64_t(c) * P.nsteps + t];
+      if (st.in && P.insrc[int64_t(c) * P.nsteps + t] < 0) v = st.in[size_t(J) * P.nx + k];
+    }
+    dst[e] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// After the chains: every step's output x_t = x~_t + Psi_J f_{G+1}(t) (Xh, Fh;
+// f of the last step from the last U kernel's partials) to the job's out and
+// out2 (+ gamma[node2]) where that write is live (v4_insrc_kernel), so the
+// steps run in parallel: CTA (t, set, J, slice r), one tile per warp.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) v4_out_kernel(V4Params P) {
+  pdl_wait();
+  const int r = blockIdx.x % kCl;
+  const int J = (blockIdx.x / kCl) % P.ny;
+  const int set = (blockIdx.x / (kCl * P.ny)) % P.nsets;
+  const int t = blockIdx.x / (kCl * P.ny * P.nsets);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rt = warp >> 1, ct = warp & 1;
+  const int krow = r * kRows + rt * 8 + (lane >> 2);
+  const int nch = ct * 8 + 2 * (lane & 3);
+  // skip the CTA when no chain of the set has a live output at this step
+  __shared__ int any_live;
+  if (threadIdx.x == 0) any_live = 0;
+  __syncthreads();
+  if (threadIdx.x < kCs) {
+    const int c = set * kCs + threadIdx.x;
+    if (c < P.nchains && P.live[int64_t(c) * P.nsteps + t]) any_live = 1;
+  }
+  __syncthreads();
+  if (!any_live) {
+    pdl_launch();
+    return;
+  }
+  const int G = J / P.g, NG = P.NG;
+  const bool inflow = G < NG - 1;
+  const int Gs = G + 1;
+  double d0 = 0.0, d1 = 0.0;
+  if (inflow) {
+    const double* A = P.Psi + (size_t(J) * kCl + r) * kSlice + rt * 32 + lane;
+    const int bo = ct * 32 + (lane & 3) * 8 + (lane >> 2);
+    const double* fb = P.Fh + ((size_t(t) * P.nsets + set) * NG + Gs) * kVec + bo;
+    const bool last = t + 1 == P.nsteps;  // f(last): group-end value + its sources' partials
+    const double* ev = P.Xend + (size_t(set) * NG + Gs) * kVec + bo;
+    const double* pp = P.FP + (size_t(set) * NG + Gs) * NG * kVec + bo;
+    double e0 = 0.0, e1 = 0.0;
+#pragma unroll 4
+    for (int ks = 0; ks < 32; ks += 2) {
+      double b0, b1;
+      if (!last) {
+        b0 = fb[ks * 64];
+        b1 = fb[(ks + 1) * 64];
+      } else {
+        b0 = ev[ks * 64];
+        b1 = ev[(ks + 1) * 64];
+        for (int src = Gs + 1; src < NG; ++src) {
+          b0 += pp[size_t(src) * kVec + ks * 64];
+          b1 += pp[size_t(src) * kVec + (ks + 1) * 64];
+        }
+      }
+      dmma4(d0, d1, A[ks * 64], b0);
+      dmma4(e0, e1, A[(ks + 1) * 64], b1);
+    }
+    d0 += e0;
+    d1 += e1;
+  }
+  if (krow < P.nx) {
+    const size_t hstep = size_t(P.nsets) * P.ny * kVec;
+    const double2 xv = *reinterpret_cast<const double2*>(
+        P.Xh + size_t(t) * hstep + (size_t(set) * P.ny + J) * kVec + vidx(krow, nch));
+    const int p = J * P.nx + krow;
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      const int c = set * kCs + nch + w;
+      if (c >= P.nchains) continue;
+      const int lv = P.live[int64_t(c) * P.nsteps + t];
+      if (!lv) continue;
+      const FastStep st = P.jobs[int64_t(c) * P.nsteps + t];
+      const double x = (w ? xv.y : xv.x) + (w ? d1 : d0);
+      if (lv & 1) st.out[p] = x;
+      if (lv & 2) st.out2[p] = x + ((st.node2 > 0 && P.gam) ? P.gam[st.node2] : 0.0);
+    }
+  }
+  pdl_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -824,6 +916,21 @@ void launch_ex(Ctx* c, const void* fn, int grid, size_t smem, bool cluster, void
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
+  KKT_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+  c->launches++;
+}
+
+void launch_ex_threads(Ctx* c, const void* fn, int grid, int threads, void** args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   KKT_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
   c->launches++;
 }
@@ -966,8 +1073,26 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.TU = ops + 7 * per + size_t(ntri) * kMat;
   double* st = c->v4_state.p;
   P.Yt = st;
-  P.Xt = st + size_t(nsets_alloc) * c->ny * kVec;
   double* vb = st + size_t(2 * nsets_alloc) * c->ny * kVec;
+  // per-step history (x~, gathered inputs, f) and the input-source table
+  {
+    const size_t hs = size_t(nsteps) * nsets * c->ny * kVec;
+    const size_t fs = size_t(nsteps) * nsets * NG * kVec;
+    const size_t need = 2 * hs + fs + size_t(nsets) * kCs * nsteps + 1;
+    if (c->v4_hist.n < need) {
+      KKT_CUDA(cudaStreamSynchronize(c->stream));
+      for (auto& e : c->graphs)
+        if (e.exec) cudaGraphExecDestroy(e.exec);
+      c->graphs.clear();
+      c->v4_hist.alloc(need);
+      KKT_CUDA(cudaMemsetAsync(c->v4_hist.p, 0, sizeof(double) * need, c->stream));
+    }
+    P.Xh = c->v4_hist.p;
+    P.Rin = c->v4_hist.p + hs;
+    P.Fh = c->v4_hist.p + 2 * hs;
+    P.insrc = reinterpret_cast<int*>(c->v4_hist.p + 2 * hs + fs);
+    P.live = P.insrc + size_t(nsets) * kCs * nsteps;
+  }
   P.Yend = vb;
   P.Xend = vb + nveca;
   P.EP = vb + 2 * nveca;
@@ -1006,18 +1131,24 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   const int gridA = nsets * NG * kCl;
   const size_t sA = smemA();
   auto sequence = [&]() {
-    for (int t = 0; t <= nsteps; ++t) {
-      int fin = t == nsteps ? 1 : 0;
+    const int npairs = nchains * nsteps;
+    KKT_LAUNCH(c, v4_insrc_kernel, (npairs + 127) / 128, 128, 0, jobs_dev, nchains, nsteps,
+               const_cast<int*>(P.insrc), const_cast<int*>(P.live));
+    KKT_LAUNCH(c, v4_gather_kernel, nsteps * nsets * c->ny, 256, 0, P);
+    for (int t = 0; t < nsteps; ++t) {
+      int zero = 0;
       {
-        void* args[] = {&P, &t, &fin};
+        void* args[] = {&P, &t, &zero};
         launch_ex(c, reinterpret_cast<const void*>(&v4A_kernel<false>), gridA, sA, true, args);
       }
-      if (fin) break;
       {
-        int zero = 0;
         void* args[] = {&P, &t, &zero};
         launch_ex(c, reinterpret_cast<const void*>(&v4A_kernel<true>), gridA, sA, true, args);
       }
+    }
+    {
+      void* args[] = {&P};
+      launch_ex_threads(c, reinterpret_cast<const void*>(&v4_out_kernel), nsteps * nsets * c->ny * kCl, 128, args);
     }
   };
   static const bool no_graph = getenv("KKT_NO_GRAPH") != nullptr;
