@@ -352,7 +352,7 @@ def run_ours(args, ws, rank, local):
     e2e_value = unknowns / (ms_e2e / 1000.0)
 
     # ---- rooflines.  Phase slot 3 brackets the RASQ sweep launches (one
-    # CUDA-graph replay of the group-parallel LU chains per P^-1, sweep_group.cu;
+    # CUDA-graph replay of the cluster LU chains per P^-1, sweep_v4.cu;
     # the transform GEMMs + mode recurrences in SPECTRAL mode), slot 2 the
     # Krylov Gram-Schmidt passes (krylov.cu).  `roofline` is the family with the
     # larger share of the step.
@@ -391,7 +391,7 @@ def run_ours(args, ws, rank, local):
         sw_gbs = sb / (sw_ms / 1000.0) / 1e9 if sw_ms > 0 else None
         sweep = {
             "kernel": ("RASQ sweep: group-parallel block-LU substitution chains, all local subdomains in lock step "
-                       "(sweep_group.cu, one CUDA-graph replay per P^-1)" if args.mode == "fast" else
+                       "(sweep_v4.cu: 8-CTA clusters, fp64 DMMA, one CUDA-graph replay per P^-1)" if args.mode == "fast" else
                        "RASQ sweep: reference-order banded substitution (sweep_strict.cu)"),
             "bound": "hbm", "achieved": sw_gbs, "peak": peak, "unit": "GB/s",
             "frac": (sw_gbs / peak) if sw_gbs else None, "traffic": None, "peak_source": peak_src,
@@ -473,6 +473,11 @@ def run_ours(args, ws, rank, local):
     }
     if alt is not None:
         line["alt_spectral"] = alt
+    if ws == 1 and not args.no_c2 and args.mode == "fast" and args.config == 1:
+        try:
+            line["microbench_c2"] = c2_microbench(local)
+        except Exception as e:  # reported beside the headline, never required
+            line["microbench_c2"] = {"error": str(e)}
     if not args.no_cpu_baseline and ws == 1:
         try:
             from oracle import bindings
@@ -487,6 +492,61 @@ def run_ours(args, ws, rank, local):
     print(json.dumps(line))
 
 
+def c2_microbench(local, reps=10):
+    """BASELINE config 2, the preconditioner-apply microbench: 10 applications
+    of P^-1 at 511^2 x 1024 steps, 64 subdomains, on seeded N(0,1) KKT vectors
+    (device-generated here: timing only; parity is tests/test_gpu_large.py and
+    tests/test_gpu_v5.py).  The sweep runs sweep_v5.cu (fp64 DMMA), so its
+    roofline is the fp64 tensor peak."""
+    import torch
+    from paper_2305_04421_b200.solver import HeatKKT
+    dev = torch.device("cuda", local)
+    p = P.config(2)
+    t0 = time.perf_counter()
+    k = HeatKKT(p, mode="fast", device=local)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    g = torch.Generator(device=dev).manual_seed(2)
+    v = torch.randn(3 * p.block, dtype=torch.float64, device=dev, generator=g)
+    out = torch.empty_like(v)
+    k.apply_P_inv(v, out)
+    torch.cuda.synchronize()
+    k.set_phase_timing(True)
+    ts = []
+    for _ in range(reps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        k.apply_P_inv(v, out)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    phase_ms, phase_cnt = k.phase_times()
+    k.set_phase_timing(False)
+    ts.sort()
+    med = ts[len(ts) // 2]
+    sw_ms = phase_ms[3] / max(1, phase_cnt[3])
+    # v5 arithmetic per RASQ apply: every block row of every spatial solve does
+    # the dense on-chain product (G_J / H_J: nx^2 MACs per chain) and the
+    # off-chain triangle (Li_J / Ui_J: nx^2/2), both sweep directions
+    nx, ny, m = p.nx_int, p.ny_int, p.Nt // p.Nd
+    flops = 2.0 * 2 * 1.5 * nx * nx * ny * p.Nd * (2 * m + 1)
+    tpk, tpk_src = fp64_peak()
+    tf = flops / (sw_ms / 1000.0) / 1e12 if sw_ms > 0 else None
+    res = {"workload": workload_desc(2, p), "applications": reps, "setup_s": setup_s,
+           "ms_per_apply_median": med, "ms_per_apply_min": ts[0],
+           "value": 3 * p.block / (med / 1000.0), "unit": "unknowns/s per P^-1 apply",
+           "sweep_ms_per_apply": sw_ms,
+           "roofline": {"kernel": "v5_kernel<512> (sweep_v5.cu: 16-CTA clusters, fp64 DMMA block substitution)",
+                        "bound": "tensor", "achieved": tf, "peak": tpk, "unit": "TFLOP/s",
+                        "frac": (tf / tpk) if (tf and tpk) else None, "peak_source": tpk_src,
+                        "flops_per_apply": flops},
+           "inputs": "device-generated N(0,1) (torch, seed 2); parity at this size: tests/test_gpu_large.py"}
+    del k, v, out
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -497,6 +557,7 @@ def main():
     ap.add_argument("--mode", default="fast", choices=["fast", "strict", "spectral"])
     ap.add_argument("--no-alt", action="store_true", help="skip the SPECTRAL side measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c2", action="store_true", help="skip the config-2 P^-1 microbench")
     args = ap.parse_args()
     ws, rank, local = dist_setup(args)
     try:

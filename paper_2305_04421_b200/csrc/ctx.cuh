@@ -118,6 +118,9 @@ struct Ctx {
   DBuf<double> arena;              // one allocation for the sweep operators (L2-persisting window)
   // fast v4 (sweep_v4.cu): fragment-ordered operators, chain state, B-phase items
   DBuf<double> v4_ops, v4_state, v4_zero, v4_la, v4_hist;
+  // fast v5 (sweep_v5.cu, 128 < nx <= 511): fragment-ordered G/Li/H/Ui, y workspace
+  DBuf<double> v5_ops, v5_y, v5_la;
+  int v5_kn = 0, v5_jstar = 0;
   DBuf<unsigned> v4_flags;
   int v4_nsets = 0;
   bool v4_coop = false, v4_registered = false;
@@ -212,6 +215,17 @@ Halo exchange_halo(Ctx* c, const double* v, int slot_prev, int slot_next, bool w
 void op_apply_K(Ctx* c, const double* v, double* out, const double* b_minus);
 void op_pinv_uz(Ctx* c, const double* r, double* out);
 void op_shat(Ctx* c, const double* v, double* out, double* tmp);
+
+// ---- batched fp64 tensor-core GEMM (spectral.cu): C[b] = A[b] B[b], row-major
+struct GemmArgs {
+  const double* A;
+  const double* B;
+  double* C;
+  int64_t lda, ldb, ldc;
+  int64_t sA, sB, sC;  // batch strides (0 = shared operand)
+  int M, N, K;
+};
+void gemm_f64(Ctx* c, const GemmArgs& g, int batch);
 
 // ---- solves and sweeps (sweep.cu)
 void band_solve(Ctx* c, double* b, int nrhs, bool transpose);

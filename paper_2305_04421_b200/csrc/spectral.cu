@@ -43,15 +43,6 @@ constexpr int kBM = 64, kBN = 64, kBK = 16;
 constexpr int kGemmThreads = 128;
 constexpr int kApad = 4, kBpad = 4;
 
-struct GemmArgs {
-  const double* A;
-  const double* B;
-  double* C;
-  int64_t lda, ldb, ldc;
-  int64_t sA, sB, sC;  // batch strides (0 = shared operand)
-  int M, N, K;
-};
-
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -134,10 +125,16 @@ __global__ void __launch_bounds__(kGemmThreads) gemm_f64_kernel(GemmArgs g) {
   }
 }
 
-void gemm(Ctx* c, const GemmArgs& g, int batch) {
+}  // namespace
+
+void gemm_f64(Ctx* c, const GemmArgs& g, int batch) {
   const dim3 grid((g.N + kBN - 1) / kBN, (g.M + kBM - 1) / kBM, batch);
   KKT_LAUNCH(c, gemm_f64_kernel, grid, kGemmThreads, 0, g);
 }
+
+namespace {
+
+void gemm(Ctx* c, const GemmArgs& g, int batch) { gemm_f64(c, g, batch); }
 
 // planes (P of them, ny x nx each, contiguous) -> Sy X Sx, via `tmp`
 void transform(Ctx* c, const double* in, double* tmp, double* out, int P) {

@@ -43,5 +43,8 @@ int v4_group_size(const Ctx* c);
 void build_v4(Ctx* c, const double* G, const double* H, const double* Li, const double* dinv);
 void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms);
 void v4_unregister(Ctx* c);
+bool v5_supported(const Ctx* c);
+void build_v5(Ctx* c);
+void v5_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms);
 
 }  // namespace kkt

@@ -66,7 +66,8 @@ constexpr int kSlice = kRows * kN;   // doubles per matrix slice (16 KB)
 constexpr int kMat = kN * kN;        // doubles per matrix
 constexpr int kVec = kN * kCs;       // doubles per block vector of a chain set
 constexpr int kThr4 = 256;
-constexpr int kCMax = 9;             // C-part operator slices in flight (the slab aliases ring + X + V)
+constexpr int kCMax = 9;
+constexpr int kMaxSrc = 18;          // group-boundary sources per inflow vector (NG - 1 <= 148 / kCl)             // C-part operator slices in flight (the slab aliases ring + X + V)
 
 __host__ __device__ inline int tri_idx(int g, int i) { return g * (g - 1) / 2 + i; }  // i < g
 
@@ -363,18 +364,15 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
   // L: f(t') of the steps whose output is this step's `in` (t' < t-1) was
   // recorded by kernels that completed before the predecessor started, so it
   // can be fetched before griddepcontrol.wait
-  constexpr int kU8 = kVec / kThr4;
-  double fpre[kU8];
+  // this CTA sums rows 16r..16r+15 of the inflow vector (its contiguous 256
+  // elements of the block-vector layout, one per thread) and broadcasts them
+  const int ev_e = kRows * kCs * r + tid;
+  double fpre = 0.0;
   if (!kU && inflow && t > 0) {
-#pragma unroll
-    for (int u = 0; u < kU8; ++u) {
-      const int e = tid + u * kThr4;
-      const int n = 8 * ((e >> 5) & 1) + (e & 7);
-      const int ts = sinp[n];
-      fpre[u] = (sj[n].in && ts >= 0 && ts != t - 1)
-                    ? P.Fh[((size_t(ts) * P.nsets + set) * NG + G + 1) * kVec + e]
-                    : 0.0;
-    }
+    const int n = 8 * ((ev_e >> 5) & 1) + (ev_e & 7);
+    const int ts = sinp[n];
+    if (sj[n].in && ts >= 0 && ts != t - 1)
+      fpre = P.Fh[((size_t(ts) * P.nsets + set) * NG + G + 1) * kVec + ev_e];
   }
   long long* tim = (P.tim && tid == 0) ? P.tim + (size_t(kU) * gridDim.x + blockIdx.x) * 32 : nullptr;
   if (tim) tim[0] = clock64();
@@ -402,43 +400,31 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     const double* pp = (kU ? P.EP : P.FP) + (size_t(set) * NG + Gs) * NG * kVec;
     // sources: L (e_Gs): 0 .. Gs-1; U (f_Gs): Gs+1 .. NG-1
     const int s0 = kU ? 0 : Gs + 1, s1 = kU ? Gs : NG;
-    double v[kU8];
+    // every partial's load in flight at once, then summed in source order
+    double w[kMaxSrc];
 #pragma unroll
-    for (int u = 0; u < kU8; ++u) v[u] = endv[tid + u * kThr4];
-    for (int p0 = s0; p0 < s1; p0 += 4) {  // 4 partials' loads in flight at once
-      double w[4][kU8];
+    for (int p = 0; p < kMaxSrc; ++p) w[p] = s0 + p < s1 ? pp[size_t(s0 + p) * kVec + ev_e] : 0.0;
+    double v = endv[ev_e];
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const bool ok = p0 + p < s1;
-        const double* src = ok ? pp + size_t(p0 + p) * kVec : P.zeros;
-#pragma unroll
-        for (int u = 0; u < kU8; ++u) w[p][u] = src[ok ? tid + u * kThr4 : 0];
-      }
-#pragma unroll
-      for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int u = 0; u < kU8; ++u) v[u] += w[p][u];
+    for (int p = 0; p < kMaxSrc; ++p)
+      if (s0 + p < s1) v += w[p];
+    if (!kU) {
+      // f(t-1) of group Gs: record this CTA's slice, then combine per chain
+      // column n(e):  f~ = [add] f(t-1) + [in = out(t')] scale * f(t')
+      P.Fh[((size_t(t - 1) * P.nsets + set) * NG + Gs) * kVec + ev_e] = v;
+      const int n = 8 * ((ev_e >> 5) & 1) + (ev_e & 7);
+      const FastStep& st = sj[n];
+      double f = st.in && st.add ? v : 0.0;
+      const int ts = sinp[n];
+      if (st.in && ts >= 0) f = fma(st.scale, ts == t - 1 ? v : fpre, f);
+      v = f;
     }
-    if (kU) {
-#pragma unroll
-      for (int u = 0; u < kU8; ++u) EV[tid + u * kThr4] = v[u];
-    } else {
-      // f(t-1) of group Gs: record it (this CTA's quarter... its 256-element
-      // slice of rows), then combine per chain column n(e):
-      //   f~ = [add] f(t-1) + [in = out(t')] scale * f(t')
-      double* fh = P.Fh + ((size_t(t - 1) * P.nsets + set) * NG + Gs) * kVec;
-#pragma unroll
-      for (int u = 0; u < kU8; ++u) {
-        const int e = tid + u * kThr4;
-        if ((e >> 8) == r) fh[e] = v[u];
-        const int n = 8 * ((e >> 5) & 1) + (e & 7);
-        const FastStep& st = sj[n];
-        double w = st.in && st.add ? v[u] : 0.0;
-        const int ts = sinp[n];
-        if (st.in && ts >= 0) w = fma(st.scale, ts == t - 1 ? v[u] : fpre[u], w);
-        EV[e] = w;
-      }
-    }
+    EV[ev_e] = v;
+    const uint32_t loc = smem_u32(EV + ev_e);
+#pragma unroll 1
+    for (int pr = 1; pr < kCl; ++pr)
+      asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(mapa_u32(loc, uint32_t((r + pr) % kCl))), "d"(v)
+                   : "memory");
   }
   // the other direction's publish flags were last used by the previous
   // kernel (complete): reset them for its next launch
@@ -1108,6 +1094,7 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.nsp = c->nsp;
   P.g = c->grp_g;
   P.NG = NG;
+  if (NG - 1 > kMaxSrc) throw Error(KKT_EINVAL, "sweep v4: too many groups for the inflow sum");
   P.nchains = nchains;
   P.nsets = nsets;
   P.jobs = jobs_dev;

@@ -1,0 +1,66 @@
+"""Time setup, apply_K and apply_P_inv at the large BASELINE grids (FAST mode).
+
+    python scripts/time_large.py --config 2 [--nt 1024] [--nd 64] [--reps 10]
+
+Inputs are device N(0,1) vectors (timing only; parity lives in tests/).
+Prints one JSON line per config.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    from paper_2305_04421_b200 import problems as P
+    from paper_2305_04421_b200.solver import HeatKKT
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--nt", type=int, default=None)
+    ap.add_argument("--nd", type=int, default=None)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--mode", default="fast")
+    a = ap.parse_args()
+    p = P.config(a.config, Nd=a.nd)
+    if a.nt:
+        p = p.replace(Nt=a.nt)
+    t0 = time.time()
+    k = HeatKKT(p, mode=a.mode)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    g = torch.Generator(device="cuda").manual_seed(0)
+    v = torch.randn(3 * p.block, dtype=torch.float64, device="cuda", generator=g)
+    out = torch.empty_like(v)
+    st = torch.cuda.current_stream()
+
+    def tm(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ts.sort()
+        return ts[len(ts) // 2]
+
+    k_ms = tm(lambda: k.apply_K(v, out), max(3, a.reps))
+    p_ms = tm(lambda: k.apply_P_inv(v, out), a.reps)
+    unk = 3 * p.block
+    print(json.dumps({"config": a.config, "Nt": p.Nt, "Nd": p.Nd, "nx": p.nx_int, "setup_s": setup_s,
+                      "apply_K_ms": k_ms, "apply_P_inv_ms": p_ms,
+                      "P_inv_unknowns_per_s": unk / (p_ms * 1e-3),
+                      "finite": bool(torch.isfinite(out).all().item())}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

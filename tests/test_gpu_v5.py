@@ -1,0 +1,84 @@
+"""GPU: the large-grid FAST sweep (sweep_v5.cu, 128 < nx <= 511) against
+STRICT mode, which is bitwise the reference's banded LU (test_gpu_parity.py),
+on grids small enough in time for STRICT to finish in seconds.
+
+Covers both cluster shapes (kN = 256: 8-CTA clusters; kN = 512: 16-CTA
+clusters), chain counts that do not fill a set of 8, the window solves
+(1 chain), multi-RHS band solves, one-level RASQ and the fused two-level
+residual, rectangular grids (nx != ny).  Tolerance: 1e-10 relative L2 per
+block (north_star's solution tolerance), as for the other FAST operators.
+"""
+import numpy as np
+import pytest
+
+from paper_2305_04421_b200 import problems as P
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # (Nx, Ny, Nt, Nd, precond)
+    (160, 160, 8, 4, "two-level"),    # nx = 159 -> kN 256, 4 chains
+    (200, 150, 9, 3, "two-level"),    # rectangular, 3 chains
+    (300, 300, 8, 2, "one-level"),    # nx = 299 -> kN 512 (16-CTA clusters)
+    (140, 140, 80, 10, "two-level"),  # 10 chains: two chain sets, 17 steps each
+]
+
+
+def _problem(Nx, Ny, Nt, Nd, pre):
+    return P.Problem(Lx=1.0, Ly=1.0, Nx=Nx, Ny=Ny, Nt=Nt, Nd=Nd, nu=0.1, omega=1e-2, precond=pre,
+                     coarse_variant="scalar", tol=1e-8, restart=20)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}_nt{c[2]}_nd{c[3]}_{c[4]}" for c in CASES])
+def test_v5_pinv_against_strict(case):
+    import torch
+    from paper_2305_04421_b200.solver import HeatKKT
+    p = _problem(*case)
+    v = torch.from_numpy(P.random_kkt(p, 1)).cuda()
+    f = HeatKKT(p, mode="fast")
+    s = HeatKKT(p, mode="strict")
+    got = f.apply_P_inv(v).cpu().numpy()
+    want = s.apply_P_inv(v).cpu().numpy()
+    B = p.block
+    for blk in range(3):
+        err = _rel(got[blk * B:(blk + 1) * B], want[blk * B:(blk + 1) * B])
+        assert err <= 1e-10, (blk, err)
+    # RASQ alone (one-level part) too
+    w = v[2 * B:3 * B].contiguous()
+    e = _rel(f.apply_rasq(w).cpu().numpy(), s.apply_rasq(w).cpu().numpy())
+    assert e <= 1e-10, e
+
+
+@pytest.mark.parametrize("Nx,Ny", [(160, 160), (300, 220)])
+def test_v5_window_and_band_solves(Nx, Ny):
+    import torch
+    from paper_2305_04421_b200.solver import HeatKKT
+    p = _problem(Nx, Ny, 8, 2, "one-level")
+    f = HeatKKT(p, mode="fast")
+    s = HeatKKT(p, mode="strict")
+    g = torch.Generator(device="cuda").manual_seed(3)
+    b = torch.randn(5 * p.n_sp, dtype=torch.float64, device="cuda", generator=g)
+    for fn in ("forward_solve_window", "adjoint_solve_window"):
+        x = getattr(f, fn)(b.clone()).cpu().numpy()
+        y = getattr(s, fn)(b.clone()).cpu().numpy()
+        assert _rel(x, y) <= 1e-10, fn
+    for tr in (False, True):
+        x = f.band_solve(b.clone(), transpose=tr).cpu().numpy()
+        y = s.band_solve(b.clone(), transpose=tr).cpu().numpy()
+        assert _rel(x, y) <= 1e-10, tr
+
+
+def test_v5_deterministic():
+    """Fixed reduction order: two applications are bitwise equal."""
+    import torch
+    from paper_2305_04421_b200.solver import HeatKKT
+    p = _problem(300, 300, 16, 8, "two-level")
+    v = torch.from_numpy(P.random_kkt(p, 2)).cuda()
+    f = HeatKKT(p, mode="fast")
+    a = f.apply_P_inv(v).clone()
+    b = f.apply_P_inv(v)
+    assert torch.equal(a, b)
