@@ -451,6 +451,7 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
           mbar_wait(&sfreeC[(u - 1) % 3], uint32_t((u - 1) / 3) & 1u);
           issue_on(u + 2);
         }
+        __syncwarp();  // warp 0 converged again before mma.sync
         mbar_wait(&tbarC[u % 3], uint32_t(u / 3) & 1u);
         if (tim) m1 = clock64();
         const int xb = (q - 1) & 1;
