@@ -21,11 +21,14 @@ CASES = [
     (200, 150, 9, 3, "two-level"),    # rectangular, 3 chains
     (300, 300, 8, 2, "one-level"),    # nx = 299 -> kN 512 (16-CTA clusters)
     (140, 140, 80, 10, "two-level"),  # 10 chains: two chain sets, 17 steps each
+    (257, 3, 8, 2, "two-level"),      # nx = 256 -> kN 512 at its smallest; ny = 2
+    (256, 40, 8, 4, "two-level"),     # nx = 255: kN 256 full width
+    (160, 400, 8, 2, "two-level", 1e-3),  # ny = 399, cy = 20: rows past jstar on resident operators
 ]
 
 
-def _problem(Nx, Ny, Nt, Nd, pre):
-    return P.Problem(Lx=1.0, Ly=1.0, Nx=Nx, Ny=Ny, Nt=Nt, Nd=Nd, nu=0.1, omega=1e-2, precond=pre,
+def _problem(Nx, Ny, Nt, Nd, pre, nu=0.1):
+    return P.Problem(Lx=1.0, Ly=1.0, Nx=Nx, Ny=Ny, Nt=Nt, Nd=Nd, nu=nu, omega=1e-2, precond=pre,
                      coarse_variant="scalar", tol=1e-8, restart=20)
 
 
@@ -33,7 +36,8 @@ def _rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}_nt{c[2]}_nd{c[3]}_{c[4]}" for c in CASES])
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}_nt{c[2]}_nd{c[3]}_{c[4]}_nu{c[5] if len(c) > 5 else 0.1}"
+                                             for c in CASES])
 def test_v5_pinv_against_strict(case):
     import torch
     from paper_2305_04421_b200.solver import HeatKKT
@@ -82,3 +86,25 @@ def test_v5_deterministic():
     a = f.apply_P_inv(v).clone()
     b = f.apply_P_inv(v)
     assert torch.equal(a, b)
+
+
+def test_v5_resident_rows_used():
+    """The tall case converges inside the grid, so part of every sweep runs on
+    the resident operators (jstar < ny); KKT_V5_TIM prints it.  Checked in a
+    subprocess because the switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+    code = ("import torch; from paper_2305_04421_b200 import problems as P; "
+            "from paper_2305_04421_b200.solver import HeatKKT; "
+            "p = P.Problem(Lx=1.0, Ly=1.0, Nx=160, Ny=400, Nt=8, Nd=2, nu=1e-3, omega=1e-2, "
+            "precond='one-level', coarse_variant='scalar', tol=1e-8, restart=20); "
+            "HeatKKT(p, mode='fast'); torch.cuda.synchronize()")
+    env = dict(os.environ, KKT_V5_TIM="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [x for x in r.stderr.splitlines() if x.startswith("v5 jstar")]
+    assert line, r.stderr[-2000:]
+    js, ny = int(line[0].split()[2]), int(line[0].split()[5])
+    assert 0 < js < ny - 1, line[0]
