@@ -133,21 +133,37 @@ __device__ __forceinline__ void dmma5(double& d0, double& d1, double a, double b
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
 // One warp: tile rt (8 rows) x 8 chains += chunk (32 rows x 64 columns) x B (64 x 8).
+// The operands of the next 4 k-steps are loaded while the current 4 DMMAs are
+// in the pipe (a lone warp otherwise waits for shared memory every 4 DMMAs:
+// scripts/mb_dmma_smem.cu).
 __device__ __forceinline__ void chunk_mma(const double* A, const double* B, int rt, double (&acc)[4][2]) {
   const int lane = threadIdx.x & 31;
   const double* Ap = A + rt * 32 + lane;
   const double* Bp = B + (lane & 3) * 8 + (lane >> 2);
+  double av[4], bv[4];
 #pragma unroll
-  for (int ks = 0; ks < 16; ks += 4) {
-    double av[4], bv[4];
+  for (int u = 0; u < 4; ++u) {
+    av[u] = Ap[u * 128];
+    bv[u] = Bp[u * 32];
+  }
+#pragma unroll
+  for (int ks = 4; ks < 16; ks += 4) {
+    double an[4], bn[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      av[u] = Ap[(ks + u) * 128];
-      bv[u] = Bp[(ks + u) * 32];
+      an[u] = Ap[(ks + u) * 128];
+      bn[u] = Bp[(ks + u) * 32];
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) dmma5(acc[u][0], acc[u][1], av[u], bv[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      av[u] = an[u];
+      bv[u] = bn[u];
+    }
   }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) dmma5(acc[u][0], acc[u][1], av[u], bv[u]);
 }
 
 // nonzero 64-column chunks of CTA r's triangle slice: Li lower (k <= 32r+31),
@@ -173,7 +189,7 @@ __global__ void __launch_bounds__(kThr5, 1) v5_kernel(V5Params P) {
   double* X = ringO + NO * kChunk;   // 2 x VEC exchange buffers
   double* V = X + 2 * VEC;           // off-chain operand
   double* Cb = V + VEC;              // 2 x 256 off-chain tiles
-  __shared__ __align__(8) uint64_t fullC[NC], freeC[NC], fullO[NO], freeO[NO], xbar[2][CL], cready[2], cfree[2];
+  __shared__ __align__(8) uint64_t fullC[NC], freeC[NC], fullO[NO], freeO[NO], xbar[2], cready[2], cfree[2];
   __shared__ __align__(8) uint64_t resFullA, resFreeA, resFullB, resFreeB;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -193,10 +209,10 @@ __global__ void __launch_bounds__(kThr5, 1) v5_kernel(V5Params P) {
       mbar_init(&fullO[i], 1);
       mbar_init(&freeO[i], 128);
     }
-    // exchange barriers, one per (buffer, source CTA): a peer's slice
-    // completes by transaction bytes (one 2 KB bulk copy); the own slot is unused
+    // exchange barriers, one per buffer: every CTA's slice (this one's too)
+    // arrives by st.async and completes transaction bytes
     for (int i = 0; i < 2; ++i) {
-      for (int sidx = 0; sidx < CL; ++sidx) mbar_init(&xbar[i][sidx], 1);
+      mbar_init(&xbar[i], 1);
       mbar_init(&cready[i], 128);
       mbar_init(&cfree[i], 128);
     }
@@ -205,9 +221,7 @@ __global__ void __launch_bounds__(kThr5, 1) v5_kernel(V5Params P) {
     mbar_init(&resFullB, 1);
     mbar_init(&resFreeB, 128);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    for (int i = 0; i < 2; ++i)
-      for (int sidx = 0; sidx < CL; ++sidx)
-        if (sidx != r) expect_tx5(&xbar[i][sidx], kSliceBytes);
+    for (int i = 0; i < 2; ++i) expect_tx5(&xbar[i], CL * kSliceBytes);
   }
   cl_arrive();
   cl_wait();
@@ -245,14 +259,18 @@ __global__ void __launch_bounds__(kThr5, 1) v5_kernel(V5Params P) {
           // the previous row, chunk by chunk as its slices land: this CTA's
           // own chunk first, then the others in rotated order (fixed per CTA)
           const uint32_t pb = (gq - 1) & 1u, par = ((gq - 1) >> 1) & 1u;
-          auto wait_src = [&](int sidx) {
-            if (sidx == r) return;  // local slice: visible since the named barrier
-            wait_cluster5(&xbar[pb][sidx], par);
-            if (tid == 0 && sidx != r) expect_tx5(&xbar[pb][sidx], kSliceBytes);  // its next use
+          auto wait_all = [&]() {
+            wait_cluster5(&xbar[pb], par);
+            if (tid == 0) expect_tx5(&xbar[pb], CL * kSliceBytes);  // its next use
           };
           if (q > 0) {
             const double* xv = X + pb * VEC;
             const bool res = J >= P.jstar;
+            // every slice first: per-chunk cluster-scope acquires inside the
+            // product loop measured slower than one pass here
+            if (tim) m0 = clock64();
+            wait_all();
+            if (tim) { m1 = clock64(); tim[0] += m1 - m0; }
             if (res && !cres) {
               mbar_wait(&resFullA, cres_n & 1u);
               cres = true;
@@ -276,9 +294,6 @@ __global__ void __launch_bounds__(kThr5, 1) v5_kernel(V5Params P) {
               for (int u = 0; u < CC; ++u) {
                 const int c = o * CC + u;
                 if (tim) m0 = clock64();
-                wait_src(2 * c);
-                wait_src(2 * c + 1);
-                if (tim) { m1 = clock64(); tim[0] += m1 - m0; m0 = m1; }
                 chunk_mma(A + u * kChunk, xv + c * 64 * kS, rt, acc);
                 if (tim) { m1 = clock64(); tim[2] += m1 - m0; }
               }
@@ -292,7 +307,7 @@ __global__ void __launch_bounds__(kThr5, 1) v5_kernel(V5Params P) {
               cres = false;
             }
           } else {
-            for (int sidx = 0; sidx < CL; ++sidx) wait_src(sidx);
+            wait_all();
             if (tim) { m1 = clock64(); tim[0] += m1 - m0; m0 = m1; }
           }
         }
@@ -305,19 +320,19 @@ __global__ void __launch_bounds__(kThr5, 1) v5_kernel(V5Params P) {
         y0 += Cb[cb * 256 + (rt * 32 + lane) * 2];
         y1 += Cb[cb * 256 + (rt * 32 + lane) * 2 + 1];
         arrive5(&cfree[cb]);
-        // this CTA's 32-row slice: local tiles, then one 2 KB bulk DSMEM copy
-        // per peer, issued in parallel by lanes 1..CL-1 of warp 0
-        *reinterpret_cast<double2*>(X + cb * VEC + a * kS + n0) = make_double2(y0, y1);
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        bar_named(2, 128);  // also: the local slice is visible to every chain warp
-        if (warp == 0 && lane >= 1 && lane < CL) {
-          const uint32_t peer = uint32_t((r + lane) % CL);
-          const uint32_t src = xb0 + cb * uint32_t(VEC * 8) + uint32_t(kRowsV5 * r * kS * 8);
-          asm volatile(
-              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                  mapa5(src, peer)),
-              "r"(src), "r"(kSliceBytes), "r"(mapa5(smem_u32(&xbar[cb][r]), peer))
-              : "memory");
+        // the slice to every CTA of the cluster (itself included) by st.async
+        {
+          const uint32_t loc = xb0 + cb * uint32_t(VEC * 8) + uint32_t((a * kS + n0) * 8);
+          const uint32_t bar = smem_u32(&xbar[cb]);
+#pragma unroll 1
+          for (int pr = 0; pr < CL; ++pr) {
+            const uint32_t peer = uint32_t((r + pr) % CL);
+            asm volatile(
+                "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(
+                    mapa5(loc, peer)),
+                "d"(y0), "d"(y1), "r"(mapa5(bar, peer))
+                : "memory");
+          }
         }
         if (!up) {
           double* yw = P.Y + (size_t(set) * ny + J) * VEC + a * kS + n0;
@@ -339,8 +354,7 @@ __global__ void __launch_bounds__(kThr5, 1) v5_kernel(V5Params P) {
       cl_arrive();
     }
     // the last exchange has landed before this CTA can exit
-    for (int sidx = 0; sidx < CL; ++sidx)
-      if (sidx != r) wait_cluster5(&xbar[(gq - 1) & 1u][sidx], ((gq - 1) >> 1) & 1u);
+    wait_cluster5(&xbar[(gq - 1) & 1u], ((gq - 1) >> 1) & 1u);
     cl_wait();
     if (tim) tim[14] = clock64();
   } else if (warp < 8) {
