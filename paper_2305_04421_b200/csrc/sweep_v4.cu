@@ -430,8 +430,8 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
   // kernel (complete): reset them for its next launch
   if (tid < NG && r == 0 && G == 0) (kU ? P.flagL : P.flagU)[set * NG + tid] = 0u;
   if (tid == 0 && chain) {  // peer exchange buffers armed before anyone can send
-    mbar_expect_tx(&xbar[0], (kCl - 1) * kRows * kCs * 8);
-    mbar_expect_tx(&xbar[1], (kCl - 1) * kRows * kCs * 8);
+    mbar_expect_tx(&xbar[0], kCl * kRows * kCs * 8);
+    mbar_expect_tx(&xbar[1], kCl * kRows * kCs * 8);
   }
   cluster_sync_all();  // also: EV complete, every CTA's barriers armed
   if (tim) tim[2] = clock64();
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
         if (tim) m2 = clock64();
         // re-arm for the next use (peers refill it only after receiving this
         // CTA's next slices, sent below after every chain warp read it)
-        if (tid == 0) mbar_expect_tx(&xbar[xb], (kCl - 1) * kRows * kCs * 8);
+        if (tid == 0) mbar_expect_tx(&xbar[xb], kCl * kRows * kCs * 8);
         warp_mma(ringC + (u % 3) * kSlice, X + xb * kVec, 0, 32, rt, ct, y0, y1);
         mbar_arrive(&sfreeC[u % 3]);
       }
@@ -470,12 +470,12 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
       y1 += Cb[(q & 1) * 256 + (t4 * 32 + lane) * 2 + 1];
       mbar_arrive(&cfree[q & 1]);
       const int xi = vidx(krow, nch);
-      {  // the last row too: every CTA gets the whole group-end vector (B below)
-        double* xs = X + (q & 1) * kVec + xi;
-        *reinterpret_cast<double2*>(xs) = make_double2(y0, y1);
-        const uint32_t loc = smem_u32(xs);
+      {  // the last row too: every CTA gets the whole group-end vector (B below).
+        // This CTA's own tiles go through st.async as well, so the exchange
+        // barrier also orders the sibling warps' tiles before the next row reads them.
+        const uint32_t loc = smem_u32(X + (q & 1) * kVec + xi);
 #pragma unroll
-        for (int pr = 1; pr < kCl; ++pr) {
+        for (int pr = 0; pr < kCl; ++pr) {
           const uint32_t peer = (uint32_t(r) + pr) % kCl;
           asm volatile(
               "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(
