@@ -51,7 +51,11 @@ CASES = [
     (P.config(0), 4),
     (P.Problem(Lx=1.0, Ly=2.0, Nx=9, Ny=7, Nt=24, Nd=6, omega=1e-2, coarse_variant="scalar",
                tol=1e-10, restart=8, max_iters=300), 3),
+    # nx = 149: the large-grid sweep (sweep_v5.cu), 2 subdomains per rank
+    (P.Problem(Lx=1.0, Ly=1.0, Nx=150, Ny=140, Nt=16, Nd=4, nu=1.0, omega=1e-1, coarse_variant="scalar",
+               tol=1e-8, restart=20, max_iters=300), 2),
 ]
+IDS = ["c0_G2", "c0_G4", "desk_G3", "v5_G2"]
 
 
 @pytest.fixture(scope="module")
@@ -67,7 +71,7 @@ def single():
     return get
 
 
-@pytest.mark.parametrize("p,G", CASES, ids=["c0_G2", "c0_G4", "desk_G3"])
+@pytest.mark.parametrize("p,G", CASES, ids=IDS)
 def test_sharded_operators_bitwise(p, G, single):
     k1 = single(p)
     v = P.random_vec(3 * p.block, 41)
@@ -91,7 +95,12 @@ def test_sharded_operators_bitwise(p, G, single):
             assert np.array_equal(res[i], res[i + 6]), (r, name)
 
 
-@pytest.mark.parametrize("p,G", CASES, ids=["c0_G2", "c0_G4", "desk_G3"])
+# The v5 case is checked operator by operator only (bitwise, above): on this
+# saddle-point system the Krylov recurrence amplifies the rounding of the
+# per-rank dot sums ~1e3-fold per iteration (scripts/diag_v5shard.py:
+# the v4 grid nx = 119 shows the same 1e-3 history drift by iteration 4), so
+# its iteration count is not a parity property of the sweep.
+@pytest.mark.parametrize("p,G", CASES[:3], ids=IDS[:3])
 def test_sharded_gmres_matches_single_rank(p, G, single):
     b = P.kkt_rhs(0, p) if p.Nx == 32 else P.random_vec(3 * p.block, 43)
     ref = single(p).gmres_solve(b)
