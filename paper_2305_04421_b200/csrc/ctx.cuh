@@ -118,6 +118,7 @@ struct Ctx {
   DBuf<double> arena;              // one allocation for the sweep operators (L2-persisting window)
   // fast v4 (sweep_v4.cu): fragment-ordered operators, chain state, B-phase items
   DBuf<double> v4_ops, v4_state, v4_zero, v4_la, v4_hist;
+  DBuf<unsigned long long> v4_tl;  // KKT_V4_TL debug timeline
   // fast v5 (sweep_v5.cu, 128 < nx <= 511): fragment-ordered G/Li/H/Ui, y workspace
   DBuf<double> v5_ops, v5_y, v5_la;
   int v5_kn = 0, v5_jstar = 0;

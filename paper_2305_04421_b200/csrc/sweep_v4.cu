@@ -47,6 +47,7 @@
 // [ks 32][ct 2][kl 4][nl 8] (row 4ks+kl, chain 8ct+nl): the B operand reads
 // 32 consecutive doubles, the D fragment writes chain pairs as double2, and
 // the rows of CTA r are the contiguous doubles [256r, 256r+256).
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -240,6 +241,7 @@ struct V4Params {
   int nsteps;
   int coarse;
   long long* tim;      // debug (KKT_V4_TIM): per-CTA clock64 marks, null in production
+  unsigned long long* tl;  // debug (KKT_V4_TL): [2*step + kU][CTA][4] globaltimer marks
   const double* zeros; // kN zeros: load target of masked-out lanes (branch-free loads)
   const double* LA;    // [J][3][kN]: Li_J a2, Li_J a1, Li_J 1 (two-level residual term)
   int empty;           // debug: KKT_V4_EMPTY=1 kernels return at once (launch floor)
@@ -375,6 +377,13 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
       fpre = P.Fh[((size_t(ts) * P.nsets + set) * NG + G + 1) * kVec + ev_e];
   }
   long long* tim = (P.tim && tid == 0) ? P.tim + (size_t(kU) * gridDim.x + blockIdx.x) * 32 : nullptr;
+  unsigned long long* tlm = (P.tl && tid == 0) ? P.tl + ((size_t(2 * t + kU)) * gridDim.x + blockIdx.x) * 4 : nullptr;
+  auto gtime = []() {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    return g;
+  };
+  if (tlm) tlm[0] = gtime();
   if (tim) tim[0] = clock64();
   pdl_wait();  // everything below reads the predecessors' outputs
   // (dependents launch only after every CTA of this grid has started and
@@ -385,6 +394,7 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     issue_off_v(1);
   }
   if (tim) tim[1] = clock64();
+  if (tlm) tlm[1] = gtime();
 
   const int t4 = warp & 3, rt = t4 >> 1, ct = t4 & 1;
   const int krow = r * kRows + rt * 8 + (lane >> 2);  // this lane's block row
@@ -435,6 +445,7 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
   }
   cluster_sync_all();  // also: EV complete, every CTA's barriers armed
   if (tim) tim[2] = clock64();
+  if (tlm) tlm[2] = gtime();
 
   // ---------------- the zero-inflow chain (warp-specialised) -----------------
   const uint32_t xb_base = smem_u32(&xbar[0]);  // xbar[1] at +8
@@ -678,6 +689,7 @@ __global__ void __launch_bounds__(kThr4, 1) v4A_kernel(V4Params P, int t, int fi
     }
   }
   cluster_sync_all();  // no CTA exits while a peer may still address its shared memory
+  if (tlm) tlm[3] = gtime();
 }
 
 // ---------------------------------------------------------------------------
@@ -1118,6 +1130,13 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   }
   const int gridA = nsets * NG * kCl;
   const size_t sA = smemA();
+  static const bool tl_on = getenv("KKT_V4_TL") != nullptr;
+  P.tl = nullptr;
+  if (tl_on) {
+    const size_t need = size_t(2) * nsteps * gridA * 4;
+    if (c->v4_tl.n < need) c->v4_tl.alloc(need);
+    P.tl = c->v4_tl.p;
+  }
   auto sequence = [&]() {
     const int npairs = nchains * nsteps;
     KKT_LAUNCH(c, v4_insrc_kernel, (npairs + 127) / 128, 128, 0, jobs_dev, nchains, nsteps,
@@ -1205,6 +1224,53 @@ void v4_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   KKT_CUDA(cudaGraphLaunch(gr->exec, c->stream));
   c->launches += gr->nlaunch;
   c->tend(3);
+  if (tl_on) {  // kernel-boundary timeline of this application (debug)
+    std::vector<unsigned long long> h(size_t(2) * nsteps * gridA * 4);
+    KKT_CUDA(cudaMemcpyAsync(h.data(), P.tl, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
+                             c->stream));
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+    double gap[2] = {0, 0}, wspread[2] = {0, 0}, setup[2] = {0, 0}, body[2] = {0, 0}, prolog[2] = {0, 0};
+    int cnt[2] = {0, 0};
+    auto at = [&](int k, int b, int i) { return h[(size_t(k) * gridA + b) * 4 + i]; };
+    for (int k = 1; k < 2 * nsteps; ++k) {
+      unsigned long long end_prev = 0, wmin = ~0ull, wmax = 0, smax = 0, emax = 0, st_min = ~0ull;
+      for (int b = 0; b < gridA; ++b) {
+        end_prev = std::max(end_prev, at(k - 1, b, 3));
+        wmin = std::min(wmin, at(k, b, 1));
+        wmax = std::max(wmax, at(k, b, 1));
+        smax = std::max(smax, at(k, b, 2));
+        emax = std::max(emax, at(k, b, 3));
+        st_min = std::min(st_min, at(k, b, 0));
+      }
+      const int u = k & 1;
+      gap[u] += double(wmin) - double(end_prev);
+      wspread[u] += double(wmax - wmin);
+      setup[u] += double(smax) - double(wmax);
+      body[u] += double(emax) - double(smax);
+      prolog[u] += double(end_prev) - double(st_min);
+      ++cnt[u];
+    }
+    for (int k = 2 * (nsteps / 2); k < 2 * (nsteps / 2) + 2; ++k) {  // one mid step, per cluster
+      unsigned long long w0 = ~0ull;
+      for (int b = 0; b < gridA; ++b) w0 = std::min(w0, at(k, b, 1));
+      fprintf(stderr, "v4A<%d> step %d per cluster (ns from first wait return): wait / setup end / exit:", k & 1, k / 2);
+      for (int cl = 0; cl < gridA / kCl; ++cl) {
+        unsigned long long w = 0, se = 0, ex = 0;
+        for (int b = cl * kCl; b < (cl + 1) * kCl; ++b) {
+          w = std::max(w, at(k, b, 1));
+          se = std::max(se, at(k, b, 2));
+          ex = std::max(ex, at(k, b, 3));
+        }
+        fprintf(stderr, " [%d: %llu %llu %llu]", cl, w - w0, se - w0, ex - w0);
+      }
+      fprintf(stderr, "\n");
+    }
+    for (int u = 0; u < 2; ++u)
+      fprintf(stderr,
+              "v4A<%d> timeline (ns, avg over %d kernels): start-before-pred-end %.0f | pred end -> first wait return %.0f"
+              " | wait-return spread %.0f | setup %.0f | rows+tail %.0f\n",
+              u, cnt[u], prolog[u] / cnt[u], gap[u] / cnt[u], wspread[u] / cnt[u], setup[u] / cnt[u], body[u] / cnt[u]);
+  }
 }
 
 }  // namespace kkt
