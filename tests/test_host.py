@@ -157,3 +157,19 @@ def test_mode_names():
     txt = open(HEADER).read()
     assert "KKT_MODE_SPECTRAL = 2" in txt
 
+
+
+def test_smoke_problem_converges_in_the_oracle():
+    """__graft_entry__.smoke() checks the device solve against the oracle on a
+    small problem; that problem must converge in the reference too (with
+    GMRES(12) it stagnates there, so smoke uses GMRES(30): 36 iterations)."""
+    import ast
+    from oracle import bindings
+    if not bindings.available("orc"):
+        pytest.skip("oracle restatement not built")
+    src = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "__graft_entry__.py")).read()
+    call = [n for n in ast.walk(ast.parse(src)) if isinstance(n, ast.Call) and getattr(n.func, "attr", "") == "Problem"][0]
+    kw = {k.arg: ast.literal_eval(k.value) for k in call.keywords}
+    p = P.Problem(**kw)
+    out = bindings.Orc(p).gmres_solve(P.kkt_rhs(0, p))
+    assert out["converged"] and out["iterations"] < p.max_iters, out["iterations"]
