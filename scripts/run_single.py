@@ -18,9 +18,10 @@ def main():
     ap.add_argument("--mode", default="fast")
     ap.add_argument("--coarse", default="scalar")
     ap.add_argument("--precond", default="two-level")
+    ap.add_argument("--nd", type=int, default=None, help="override the config's subdomain count")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    p = P.config(a.config, coarse=a.coarse, precond=a.precond)
+    p = P.config(a.config, coarse=a.coarse, precond=a.precond, Nd=a.nd)
     rec = run_single(p, mode=a.mode)
     text = to_json_string(rec)
     print(text)
