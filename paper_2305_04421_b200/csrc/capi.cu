@@ -181,7 +181,10 @@ void setup(Ctx* c, const kkt_problem_desc& d, const kkt_runtime_opts* o) {
   static const bool force_rec = getenv("KKT_FORCE_BLOCK_RECURSION") != nullptr;  // testing
   if (c->mode == KKT_MODE_FAST && (c->nx > 128 || force_rec)) {
     build_block_recursion(c);
-    if (v5_supported(c)) build_v5(c);
+    if (v6_supported(c))
+      build_v6(c);
+    else if (v5_supported(c))
+      build_v5(c);
   } else {
     build_factor(c);
     if (c->mode == KKT_MODE_FAST) build_block_inverses(c);

@@ -122,6 +122,10 @@ struct Ctx {
   // fast v5 (sweep_v5.cu, 128 < nx <= 511): fragment-ordered G/Li/H/Ui, y workspace
   DBuf<double> v5_ops, v5_y, v5_la;
   int v5_kn = 0, v5_jstar = 0;
+  // fast v6 (sweep_v6.cu, 511 < nx <= 1024): fragment-ordered Li/Ui/G/H, block-vector workspaces
+  DBuf<double> v6_ops, v6_w;
+  DBuf<unsigned> v6_cnt;
+  int v6_jstar = 0, v6_nops = 0;
   DBuf<unsigned> v4_flags;
   int v4_nsets = 0;
   bool v4_coop = false, v4_registered = false;

@@ -46,5 +46,8 @@ void v4_unregister(Ctx* c);
 bool v5_supported(const Ctx* c);
 void build_v5(Ctx* c);
 void v5_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms);
+bool v6_supported(const Ctx* c);
+void build_v6(Ctx* c);
+void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms);
 
 }  // namespace kkt

@@ -166,6 +166,10 @@ void fast_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool
     v4_chains(c, jobs_dev, nchains, nsteps, coarse_terms);
     return;
   }
+  if (c->v6_ops.p) {
+    v6_chains(c, jobs_dev, nchains, nsteps, coarse_terms);
+    return;
+  }
   if (c->v5_ops.p) {
     v5_chains(c, jobs_dev, nchains, nsteps, coarse_terms);
     return;

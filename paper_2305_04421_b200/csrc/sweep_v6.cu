@@ -1,0 +1,500 @@
+// sweep_v6.cu — FAST RASQ sweeps for the largest grids (511 < nx <= 1023:
+// BASELINE config 4), device-wide block substitution.
+//
+// Same block recursion as sweep v5 (the reference's LU solve
+// BandedLU::solve_in_place, linalg.cpp:127-145, on the block factors of
+// factor_block.cu, with the two dependent triangular products of a block step
+// pre-multiplied):
+//     L:  y_J = Li_J b_J + G_J y_{J-1},   G_J = cy Li_J Ui_{J-1}
+//     U:  x_J = Ui_J y_J + H_J x_{J+1},   H_J = cy Ui_J Li_J
+// At nx = 1023 a block row is 1024 x 1024 doubles (8 MB): one cluster cannot
+// hold a row slice next to its vectors (v5's layout), so v6 spreads every
+// block step over the whole device instead:
+//   * off-chain terms first, for all J at once: c_J = Li_J b_J (d_J = Ui_J y_J)
+//     is a batched triangular product with no dependency (v6_off_kernel), the
+//     triangle streamed once per spatial solve for all local chains;
+//   * then the dependent chain y_J = c_J + G_J y_{J-1} (v6_chain_kernel): a
+//     co-resident grid of 64 row slices x chain groups; CTA (s, g) owns rows
+//     16s..16s+15 for the 8 chains of group g, holds its slice of G_J in
+//     registers (loaded before the row barrier, so the operator stream overlaps
+//     the wait), multiplies it with y_{J-1} read from L2 as fp64 DMMA
+//     (m8n8k4) tiles split over 8 warps along k, and publishes y_J with a
+//     release counter per chain group (one grid-wide barrier per block row).
+// Block vectors are chain-interleaved, W[g][J][k][8] (kN = 1024 rows, zero
+// padded), so the DMMA B operand of a k-step is 256 contiguous bytes.
+// Operators are packed in fragment order, [J][s][ks][mt][lane] =
+// M[16s + 8mt + lane/4][4ks + lane%4], so each warp's A operand is 32
+// consecutive doubles.  Chains, steps and the fused two-level residual follow
+// fast_chain_kernel (sweep_fast.cu) exactly; only the operation order differs
+// (FAST mode, rounding level).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "sweep.cuh"
+
+namespace kkt {
+namespace {
+
+constexpr int kN6 = 1024;             // padded block size
+constexpr int kSl = kN6 / 16;         // row slices per block row
+constexpr int kKS = kN6 / 4;          // k-steps of a full row
+constexpr int kThr6 = 256;            // 8 warps
+constexpr int kKW = kKS / 8;          // k-steps per warp (chain kernel)
+constexpr int kG = 8;                 // chains per group (the n of m8n8k4)
+
+__device__ __forceinline__ void dmma6(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+struct V6Params {
+  const double* Lp;  // packed Li_J
+  const double* Up;  // packed Ui_J
+  const double* Gp;  // packed G_J (J >= 1)
+  const double* Hp;  // packed H_J (J <= ny-2)
+  double* W0;        // [g][J][kN][8]: b, then y, then x
+  double* W1;        // [g][J][kN][8]: c, then d
+  const FastStep* jobs;
+  int nsteps, t;
+  int nx, ny, nchains, ngroups;
+  const double* a1;
+  const double* a2;
+  const double* gam;
+  double inv_ms;
+  int coarse;
+  unsigned* cnt;     // per chain group: row-completion counter (chain kernels)
+  int g0;            // first chain group of this chain-kernel wave
+  int jstar;         // block rows J >= jstar use row jstar's operators (ny: none)
+};
+
+// Operator row of block row J, and its load: rows past jstar share one
+// operator set, which stays in L2 (default caching); the others stream
+// (evict-first).
+__device__ __forceinline__ int oprow(int J, int jstar) { return J < jstar ? J : jstar; }
+__device__ __forceinline__ double ldop(const double* p, bool res) { return res ? __ldg(p) : __ldcs(p); }
+
+__device__ __forceinline__ size_t widx(int g, int J, int ny) { return (size_t(g) * ny + J) * kN6 * kG; }
+
+// b = in*scale + add - (Shat y_c)_node / ms, chain-interleaved (fast_chain_kernel's b)
+__global__ void __launch_bounds__(256) v6_form_b_kernel(V6Params P) {
+  const size_t total = size_t(P.ngroups) * P.ny * kN6 * kG;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const int c = int(e % kG);
+    const size_t r = e / kG;
+    const int k = int(r % kN6);
+    const size_t gj = r / kN6;
+    const int J = int(gj % P.ny), g = int(gj / P.ny);
+    const int ch = g * kG + c;
+    double v = 0.0;
+    if (k < P.nx && ch < P.nchains) {
+      const FastStep st = P.jobs[size_t(ch) * P.nsteps + P.t];
+      if (st.in) {
+        const int p = J * P.nx + k;
+        v = st.in[p] * st.scale;
+        if (st.add) v += st.add[p];
+        if (P.coarse && st.node > 0) {
+          const double gn = P.gam[st.node], gm = P.gam[st.node - 1], gp = P.gam[st.node + 1];
+          double sh = gn * P.a2[p] - gp * P.a1[p];
+          if (st.node != 1) sh += gn - gm * P.a1[p];
+          v -= sh * P.inv_ms;
+        }
+      }
+    }
+    P.W0[e] = v;
+  }
+}
+
+// Partials of 8 warps -> 16 x 8 slice (fixed order): thread t < 128 owns
+// D[m][n], m = 8mt + lane/4, n = 2(lane%4) + e with t = (mt*32 + lane)*2 + e.
+__device__ __forceinline__ double reduce8(const double* red, int t) {
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) s += red[w * 128 + t];
+  return s;
+}
+__device__ __forceinline__ void slice_coords(int t, int& m, int& n) {
+  const int e = t & 1, q = t >> 1, mt = q >> 5, lane = q & 31;
+  m = 8 * mt + (lane >> 2);
+  n = 2 * (lane & 3) + e;
+}
+
+// Batched triangular products for every block row: Out[g][J] = T_J In[g][J]
+// over the nonzero k-steps of the triangle (lower: Li, upper: Ui).  One CTA
+// per block row J; chain groups in pairs, their block vectors In[g][J] staged
+// in shared memory (2 x 64 KB); each warp owns whole row slices (zig-zag
+// pairs s, 15-s of every 16, so the triangle work is balanced) and streams
+// them from HBM in fragment order, the next 16 k-steps in flight while the
+// current 16 are multiplied.  A warp accumulates a slice over all its k-steps
+// itself, so no cross-warp reduction is needed.
+constexpr int kOffChunk = 16;
+constexpr size_t kOffSmem = sizeof(double) * 2 * kN6 * kG;
+
+template <bool kUpper>
+__global__ void __launch_bounds__(kThr6, 1) v6_off_kernel(V6Params P) {
+  extern __shared__ double Bs[];  // [2][kN][8]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bo = (lane & 3) * kG + (lane >> 2);  // B fragment offset within a k-step
+  for (int J = blockIdx.x; J < P.ny; J += gridDim.x) {
+    for (int gp = 0; gp < P.ngroups; gp += 2) {
+      __syncthreads();  // the previous pair's readers are done with Bs
+      for (int i = threadIdx.x; i < kN6 * kG; i += kThr6) {  // double2 units over both groups
+        const int gi = i / (kN6 * kG / 2), r = i - gi * (kN6 * kG / 2);
+        double2 v = make_double2(0.0, 0.0);
+        if (gp + gi < P.ngroups) v = __ldcg(reinterpret_cast<const double2*>(P.W0 + widx(gp + gi, J, P.ny)) + r);
+        reinterpret_cast<double2*>(Bs)[i] = v;
+      }
+      __syncthreads();
+      for (int i = 0; i < kSl / 8; ++i) {
+        const int s = (i >> 1) * 16 + ((i & 1) ? 15 - warp : warp);
+        const int ks0 = kUpper ? 4 * s : 0;
+        const int ks1 = kUpper ? kKS : 4 * s + 4;
+        const bool res = J >= P.jstar;
+        const double* A = (kUpper ? P.Up : P.Lp) + (size_t(oprow(J, P.jstar)) * kSl + s) * kKS * 64 + lane;
+        double d[2][2][2] = {};
+        double ac[kOffChunk][2], an[kOffChunk][2];
+#pragma unroll
+        for (int u = 0; u < kOffChunk; ++u) {
+          const bool ok = ks0 + u < ks1;
+          ac[u][0] = ok ? ldop(A + size_t(ks0 + u) * 64, res) : 0.0;
+          ac[u][1] = ok ? ldop(A + size_t(ks0 + u) * 64 + 32, res) : 0.0;
+        }
+        for (int ks = ks0; ks < ks1; ks += kOffChunk) {
+#pragma unroll
+          for (int u = 0; u < kOffChunk; ++u) {
+            const bool ok = ks + kOffChunk + u < ks1;
+            an[u][0] = ok ? ldop(A + size_t(ks + kOffChunk + u) * 64, res) : 0.0;
+            an[u][1] = ok ? ldop(A + size_t(ks + kOffChunk + u) * 64 + 32, res) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < kOffChunk; ++u) {
+            if (ks + u < ks1) {
+              const double b0 = Bs[(4 * (ks + u)) * kG + bo];
+              const double b1 = Bs[kN6 * kG + (4 * (ks + u)) * kG + bo];
+              dmma6(d[0][0][0], d[0][0][1], ac[u][0], b0);
+              dmma6(d[0][1][0], d[0][1][1], ac[u][1], b0);
+              dmma6(d[1][0][0], d[1][0][1], ac[u][0], b1);
+              dmma6(d[1][1][0], d[1][1][1], ac[u][1], b1);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kOffChunk; ++u) {
+            ac[u][0] = an[u][0];
+            ac[u][1] = an[u][1];
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          if (gp + g >= P.ngroups) break;
+          double* O = P.W1 + widx(gp + g, J, P.ny) + size_t(16 * s + (lane >> 2)) * kG + 2 * (lane & 3);
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+            *reinterpret_cast<double2*>(O + mt * 8 * kG) = make_double2(d[g][mt][0], d[g][mt][1]);
+        }
+      }
+    }
+  }
+}
+
+// The dependent chain of one sweep direction for chain groups g0 .. g0 + gridDim.x/kSl - 1.
+//   L: y_J = c_J + G_J y_{J-1}  (J = 0 .. ny-1; c in W1, y to W0)
+//   U: x_J = d_J + H_J x_{J+1}  (J = ny-1 .. 0; d in W1, x to W0 and the job's outputs)
+template <bool kUpper>
+__global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
+  __shared__ double red[8 * 128];
+  const int s = blockIdx.x % kSl, g = P.g0 + blockIdx.x / kSl;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ny = P.ny;
+  const double* Mbase = (kUpper ? P.Hp : P.Gp) + size_t(s) * kKS * 64 + lane;
+  const size_t mstride = size_t(kSl) * kKS * 64;  // doubles per packed block row
+  unsigned* cnt = P.cnt + g;
+  // output thread's coordinates and job (U direction writes the step outputs)
+  int m = 0, n = 0;
+  const bool outt = threadIdx.x < 128;
+  if (outt) slice_coords(threadIdx.x, m, n);
+  const int row = 16 * s + m, ch = g * kG + n;
+  double* out = nullptr;
+  double* out2 = nullptr;
+  double g2 = 0.0;
+  if (kUpper && outt && row < P.nx && ch < P.nchains) {
+    const FastStep st = P.jobs[size_t(ch) * P.nsteps + P.t];
+    if (st.in) {
+      out = st.out;
+      out2 = st.out2;
+      if (st.out2 && st.node2 > 0 && P.gam) g2 = P.gam[st.node2];
+    }
+  }
+  auto Jof = [&](int idx) { return kUpper ? ny - 1 - idx : idx; };
+  auto emit = [&](int J, double v) {
+    P.W0[widx(g, J, ny) + size_t(row) * kG + n] = v;
+    if (out) out[size_t(J) * P.nx + row] = v;
+    if (out2) out2[size_t(J) * P.nx + row] = v + g2;
+  };
+  auto signal = [&]() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(cnt, 1u);
+    }
+  };
+  double a[kKW][2];
+  auto load_a = [&](int J) {
+    const bool res = J >= P.jstar;
+    const double* M = Mbase + size_t(oprow(J, P.jstar)) * mstride;
+#pragma unroll
+    for (int i = 0; i < kKW; ++i) {
+      const int ks = warp * kKW + i;
+      a[i][0] = ldop(M + size_t(ks) * 64, res);
+      a[i][1] = ldop(M + size_t(ks) * 64 + 32, res);
+    }
+  };
+  // first row: no inflow
+  {
+    const int J = Jof(0);
+    if (outt) emit(J, __ldcg(P.W1 + widx(g, J, ny) + size_t(row) * kG + n));
+    if (ny > 1) load_a(Jof(1));
+    signal();
+  }
+  for (int idx = 1; idx < ny; ++idx) {
+    const int J = Jof(idx), Jp = kUpper ? J + 1 : J - 1;
+    double cval = 0.0;
+    if (outt) cval = __ldcg(P.W1 + widx(g, J, ny) + size_t(row) * kG + n);
+    // wait until every slice of the group has published row idx-1
+    if (threadIdx.x == 0) {
+      const unsigned target = unsigned(idx) * kSl;
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
+      } while (v < target);
+    }
+    __syncthreads();
+    const double* B = P.W0 + widx(g, Jp, ny) + (lane & 3) * kG + (lane >> 2);
+    double b[kKW];
+#pragma unroll
+    for (int i = 0; i < kKW; ++i) b[i] = __ldcg(B + size_t(warp * kKW + i) * 4 * kG);
+    double d[2][2][2] = {};
+#pragma unroll
+    for (int i = 0; i < kKW; ++i) {
+      dmma6(d[i & 1][0][0], d[i & 1][0][1], a[i][0], b[i]);
+      dmma6(d[i & 1][1][0], d[i & 1][1][1], a[i][1], b[i]);
+    }
+    if (idx + 1 < ny) load_a(Jof(idx + 1));
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) red[warp * 128 + (mt * 32 + lane) * 2 + e] = d[0][mt][e] + d[1][mt][e];
+    __syncthreads();
+    if (outt) emit(J, cval + reduce8(red, threadIdx.x));
+    signal();
+  }
+}
+
+// dev[2J + m] = max |M_J - M_{ny-1}|, mag[2J + m] = max |M_J|, M = Li (m = 0), Ui (m = 1)
+__global__ void __launch_bounds__(256) v6_conv_kernel(const double* __restrict__ Li, const double* __restrict__ Ui,
+                                                      int nx, int ny, double* __restrict__ dev,
+                                                      double* __restrict__ mag) {
+  __shared__ double sh[4][256];
+  const int J = blockIdx.x;
+  const size_t nn = size_t(nx) * nx;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (size_t e = threadIdx.x; e < nn; e += blockDim.x) {
+    const double l = Li[size_t(J) * nn + e], u = Ui[size_t(J) * nn + e];
+    v[0] = fmax(v[0], fabs(l - Li[size_t(ny - 1) * nn + e]));
+    v[1] = fmax(v[1], fabs(u - Ui[size_t(ny - 1) * nn + e]));
+    v[2] = fmax(v[2], fabs(l));
+    v[3] = fmax(v[3], fabs(u));
+  }
+  for (int q = 0; q < 4; ++q) sh[q][threadIdx.x] = v[q];
+  __syncthreads();
+  for (int w = 128; w; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int q = 0; q < 4; ++q) sh[q][threadIdx.x] = fmax(sh[q][threadIdx.x], sh[q][threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x < 2) {
+    dev[2 * J + threadIdx.x] = sh[threadIdx.x][0];
+    mag[2 * J + threadIdx.x] = sh[2 + threadIdx.x][0];
+  }
+}
+
+// Fragment-order pack: dst[J][s][ks][mt][lane] = scale * src[J][16s+8mt+lane/4][4ks+lane%4]
+__global__ void v6_pack_kernel(const double* __restrict__ src, int nx, int nJ, double scale,
+                               double* __restrict__ dst) {
+  const size_t per = size_t(kN6) * kN6, total = size_t(nJ) * per, nn = size_t(nx) * nx;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const size_t J = e / per;
+    const int r = int(e - J * per);
+    const int lane = r & 31, mt = (r >> 5) & 1, ks = (r >> 6) % kKS, s = (r >> 6) / kKS;
+    const int a = 16 * s + 8 * mt + (lane >> 2), b = 4 * ks + (lane & 3);
+    dst[e] = (a < nx && b < nx) ? scale * src[J * nn + size_t(a) * nx + b] : 0.0;
+  }
+}
+
+void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kSl * ngroups_wave);
+  cfg.blockDim = dim3(kThr6);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // every CTA of the grid co-resident (row barriers)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  V6Params p = P;
+  void* args[] = {&p};
+  const void* fn = upper ? reinterpret_cast<const void*>(&v6_chain_kernel<true>)
+                         : reinterpret_cast<const void*>(&v6_chain_kernel<false>);
+  KKT_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+  c->launches++;
+}
+
+int groups_per_wave() {
+  static int gpw = 0;
+  if (!gpw) {
+    int per_sm = 0;
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v6_chain_kernel<false>, kThr6, 0));
+    int per_sm_u = 0;
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_u, v6_chain_kernel<true>, kThr6, 0));
+    per_sm = std::min(per_sm, per_sm_u);
+    int dev = 0, nsm = kSmCount;
+    KKT_CUDA(cudaGetDevice(&dev));
+    KKT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    gpw = std::max(1, per_sm * nsm / kSl);
+  }
+  return gpw;
+}
+
+}  // namespace
+
+bool v6_supported(const Ctx* c) {
+  static const bool force = std::getenv("KKT_SWEEP_V6") != nullptr;  // testing: v6 on v5 grids too
+  return c->mode == KKT_MODE_FAST && c->ny >= 2 && c->nx <= kN6 && (c->nx > 511 || (force && c->nx > 128));
+}
+
+// The block recursion D_J = T - cy^2 D_{J-1}^{-1} converges geometrically
+// (factor_block.cu): from some row on, Li_J and Ui_J equal the last row's to
+// rounding, so rows J >= jstar use row jstar's operators (as sweep v5 does),
+// which stay in L2, and only jstar + 1 operator rows are packed.  jstar is the
+// first row from which Li and Ui (and so G, H) stay within tol * max|M| of the
+// last row's (KKT_V6_JTOL, default 1e-15; 0 disables); none: ny.
+static int v6_find_jstar(Ctx* c) {
+  const int nx = c->nx, ny = c->ny;
+  static const char* jt = std::getenv("KKT_V6_JTOL");
+  const double tol = jt ? std::atof(jt) : 1e-15;
+  if (!(tol > 0.0) || ny < 3) return ny;
+  DBuf<double> dev(2 * size_t(ny)), mag(2 * size_t(ny));
+  KKT_LAUNCH(c, v6_conv_kernel, ny, 256, 0, c->Li.p, c->Ui.p, nx, ny, dev.p, mag.p);
+  std::vector<double> hd(2 * ny), hm(2 * ny);
+  KKT_CUDA(cudaMemcpyAsync(hd.data(), dev.p, sizeof(double) * 2 * ny, cudaMemcpyDeviceToHost, c->stream));
+  KKT_CUDA(cudaMemcpyAsync(hm.data(), mag.p, sizeof(double) * 2 * ny, cudaMemcpyDeviceToHost, c->stream));
+  KKT_CUDA(cudaStreamSynchronize(c->stream));
+  int first = ny - 1;  // rows first .. ny-1 all within tol
+  while (first > 0 && hd[2 * (first - 1)] <= tol * hm[2 * (ny - 1)] &&
+         hd[2 * (first - 1) + 1] <= tol * hm[2 * (ny - 1) + 1])
+    --first;
+  const int js = first + 1;  // G_J needs Li_J and Ui_{J-1}
+  return js <= ny - 2 ? js : ny;
+}
+
+void build_v6(Ctx* c) {
+  const int nx = c->nx, ny = c->ny;
+  c->v6_jstar = v6_find_jstar(c);
+  const int nops = std::min(ny, c->v6_jstar + 1);  // packed operator rows
+  if (std::getenv("KKT_V6_TIM")) std::fprintf(stderr, "v6 jstar %d of ny %d\n", c->v6_jstar, ny);
+  const size_t mat = size_t(kN6) * kN6, nn = size_t(nx) * nx;
+  c->v6_nops = nops;
+  c->v6_ops.alloc(4 * size_t(nops) * mat);
+  double* Lp = c->v6_ops.p;
+  double* Up = Lp + nops * mat;
+  double* Gp = Up + nops * mat;
+  double* Hp = Gp + nops * mat;
+  const int pg = kSmCount * 8;
+  KKT_LAUNCH(c, v6_pack_kernel, pg, 256, 0, c->Li.p, nx, nops, 1.0, Lp);
+  KKT_LAUNCH(c, v6_pack_kernel, pg, 256, 0, c->Ui.p, nx, nops, 1.0, Up);
+  KKT_CUDA(cudaMemsetAsync(Gp, 0, sizeof(double) * mat, c->stream));  // G_0: unused
+  if (nops == ny)
+    KKT_CUDA(cudaMemsetAsync(Hp + size_t(ny - 1) * mat, 0, sizeof(double) * mat, c->stream));  // H_{ny-1}
+  const int nh = std::min(nops, ny - 1);  // H_J rows computed
+  const int Jb = std::min(ny - 1, 32);
+  DBuf<double> T(size_t(Jb) * nn);
+  for (int J0 = 1; J0 < nops; J0 += Jb) {  // G_J = cy Li_J Ui_{J-1}
+    const int nb = std::min(Jb, nops - J0);
+    GemmArgs g{c->Li.p + J0 * nn, c->Ui.p + (J0 - 1) * nn, T.p, nx, nx, nx,
+               int64_t(nn), int64_t(nn), int64_t(nn), nx, nx, nx};
+    gemm_f64(c, g, nb);
+    KKT_LAUNCH(c, v6_pack_kernel, pg, 256, 0, T.p, nx, nb, c->cy, Gp + J0 * mat);
+  }
+  for (int J0 = 0; J0 < nh; J0 += Jb) {  // H_J = cy Ui_J Li_J
+    const int nb = std::min(Jb, nh - J0);
+    GemmArgs g{c->Ui.p + J0 * nn, c->Li.p + J0 * nn, T.p, nx, nx, nx,
+               int64_t(nn), int64_t(nn), int64_t(nn), nx, nx, nx};
+    gemm_f64(c, g, nb);
+    KKT_LAUNCH(c, v6_pack_kernel, pg, 256, 0, T.p, nx, nb, c->cy, Hp + J0 * mat);
+  }
+  KKT_CUDA(cudaStreamSynchronize(c->stream));  // T is freed on return
+}
+
+void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms) {
+  const int ny = c->ny;
+  const size_t mat = size_t(kN6) * kN6;
+  const int ngroups = (nchains + kG - 1) / kG;
+  const size_t need = size_t(ngroups) * ny * kN6 * kG;
+  if (c->v6_w.n < 2 * need || c->v6_cnt.n < size_t(ngroups)) {
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+    c->v6_w.alloc(2 * need);
+    c->v6_cnt.alloc(ngroups);
+  }
+  V6Params P;
+  const int nops = c->v6_nops;
+  P.Lp = c->v6_ops.p;
+  P.Up = P.Lp + nops * mat;
+  P.Gp = P.Up + nops * mat;
+  P.Hp = P.Gp + nops * mat;
+  P.jstar = c->v6_jstar;
+  P.W0 = c->v6_w.p;
+  P.W1 = c->v6_w.p + need;
+  P.jobs = jobs_dev;
+  P.nsteps = nsteps;
+  P.nx = c->nx;
+  P.ny = ny;
+  P.nchains = nchains;
+  P.ngroups = ngroups;
+  P.a1 = c->a1.p;
+  P.a2 = c->a2.p;
+  P.gam = c->gam.p;
+  P.inv_ms = 1.0 / c->ms;
+  P.coarse = coarse_terms ? 1 : 0;
+  P.cnt = c->v6_cnt.p;
+  const int gpw = groups_per_wave();
+  static bool attr = false;
+  if (!attr) {
+    KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kOffSmem)));
+    KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kOffSmem)));
+    attr = true;
+  }
+  const int og = std::min(ny, kSmCount);
+  c->tbegin(3);
+  for (int t = 0; t < nsteps; ++t) {
+    P.t = t;
+    P.g0 = 0;
+    KKT_LAUNCH(c, v6_form_b_kernel, kSmCount * 8, 256, 0, P);
+    for (int dir = 0; dir < 2; ++dir) {
+      const bool up = dir == 1;
+      if (up)
+        KKT_LAUNCH(c, v6_off_kernel<true>, og, kThr6, kOffSmem, P);
+      else
+        KKT_LAUNCH(c, v6_off_kernel<false>, og, kThr6, kOffSmem, P);
+      KKT_CUDA(cudaMemsetAsync(P.cnt, 0, sizeof(unsigned) * ngroups, c->stream));
+      for (int g0 = 0; g0 < ngroups; g0 += gpw) {
+        P.g0 = g0;
+        launch_chain(c, up, P, std::min(gpw, ngroups - g0));
+      }
+    }
+  }
+  c->tend(3);
+}
+
+}  // namespace kkt
