@@ -478,6 +478,11 @@ def run_ours(args, ws, rank, local):
             line["microbench_c2"] = c2_microbench(local)
         except Exception as e:  # reported beside the headline, never required
             line["microbench_c2"] = {"error": str(e)}
+    if ws == 1 and args.c4 and args.mode == "fast" and args.config == 1:
+        try:
+            line["microbench_c4_slab"] = c4_microbench(local)
+        except Exception as e:  # reported beside the headline, never required
+            line["microbench_c4_slab"] = {"error": str(e)}
     if not args.no_cpu_baseline and ws == 1:
         try:
             from oracle import bindings
@@ -547,6 +552,62 @@ def c2_microbench(local, reps=10):
     return res
 
 
+def c4_microbench(local, reps=3):
+    """BASELINE config 4 (1023^2 interior, 8 GPUs) on the one GPU this pool
+    has: one rank's time slab at G = 8 -- 16 subdomains of m = 8 steps,
+    Nt = 128 with config 4's dt = 1/1024 (T = 1/8) -- and P^-1 applications on
+    seeded N(0,1) KKT vectors (device-generated: timing only; parity of the
+    kernels at nx = 1023: tests/test_gpu_v6.py).  The sweep runs sweep_v6.cu
+    (device-wide block substitution, fp64 DMMA).  Opt-in (--c4): the block
+    recursion's setup takes ~3.5 min at nx = 1023."""
+    import torch
+    from paper_2305_04421_b200.solver import HeatKKT
+    dev = torch.device("cuda", local)
+    p = P.config(4).replace(Nt=128, Nd=16, T=0.125)
+    t0 = time.perf_counter()
+    k = HeatKKT(p, mode="fast", device=local)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    g = torch.Generator(device=dev).manual_seed(4)
+    v = torch.randn(3 * p.block, dtype=torch.float64, device=dev, generator=g)
+    out = torch.empty_like(v)
+    k.apply_P_inv(v, out)
+    torch.cuda.synchronize()
+    k.set_phase_timing(True)
+    ts = []
+    for _ in range(reps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        k.apply_P_inv(v, out)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    phase_ms, phase_cnt = k.phase_times()
+    k.set_phase_timing(False)
+    ts.sort()
+    med = ts[len(ts) // 2]
+    sw_ms = phase_ms[3] / max(1, phase_cnt[3])
+    nx, ny, m = p.nx_int, p.ny_int, p.Nt // p.Nd
+    flops = 2.0 * 2 * 1.5 * nx * nx * ny * p.Nd * (2 * m + 1)
+    tpk, tpk_src = fp64_peak()
+    tf = flops / (sw_ms / 1000.0) / 1e12 if sw_ms > 0 else None
+    res = {"workload": "config4 per-GPU slab at G=8: 1023x1023 interior, Nt=128 (dt=1/1024 as config 4), "
+                       "Nd=16 (m=8), nu=1, omega=1e-4, two-level scalar multiplicative (minus)",
+           "applications": reps, "setup_s": setup_s,
+           "ms_per_apply_median": med, "ms_per_apply_min": ts[0],
+           "value": 3 * p.block / (med / 1000.0), "unit": "unknowns/s per P^-1 apply",
+           "sweep_ms_per_apply": sw_ms,
+           "roofline": {"kernel": "v6_chain_kernel + v6_off_kernel (sweep_v6.cu: device-wide fp64 DMMA block substitution)",
+                        "bound": "tensor", "achieved": tf, "peak": tpk, "unit": "TFLOP/s",
+                        "frac": (tf / tpk) if (tf and tpk) else None, "peak_source": tpk_src,
+                        "flops_per_apply": flops},
+           "inputs": "device-generated N(0,1) (torch, seed 4); parity at nx = 1023: tests/test_gpu_v6.py"}
+    del k, v, out
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -558,6 +619,7 @@ def main():
     ap.add_argument("--no-alt", action="store_true", help="skip the SPECTRAL side measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the config-2 P^-1 microbench")
+    ap.add_argument("--c4", action="store_true", help="add the config-4 per-GPU-slab P^-1 microbench (~4 min setup)")
     args = ap.parse_args()
     ws, rank, local = dist_setup(args)
     try:

@@ -15,11 +15,11 @@
 //     triangle streamed once per spatial solve for all local chains;
 //   * then the dependent chain y_J = c_J + G_J y_{J-1} (v6_chain_kernel): a
 //     co-resident grid of 64 row slices x chain groups; CTA (s, g) owns rows
-//     16s..16s+15 for the 8 chains of group g, holds its slice of G_J in
-//     registers (loaded before the row barrier, so the operator stream overlaps
-//     the wait), multiplies it with y_{J-1} read from L2 as fp64 DMMA
-//     (m8n8k4) tiles split over 8 warps along k, and publishes y_J with a
-//     release counter per chain group (one grid-wide barrier per block row).
+//     16s..16s+15 for the 8 chains of group g, stages its slice of G_J (the
+//     next row's during this row's barrier) and y_{J-1} by bulk copies,
+//     multiplies them as fp64 DMMA (m8n8k4) tiles split over 8 warps along k,
+//     and publishes y_J with a release counter per chain group (one
+//     grid-wide barrier per block row).
 // Block vectors are chain-interleaved, W[g][J][k][8] (kN = 1024 rows, zero
 // padded), so the DMMA B operand of a k-step is 256 contiguous bytes.
 // Operators are packed in fragment order, [J][s][ks][mt][lane] =
@@ -33,9 +33,13 @@
 #include <vector>
 
 #include "sweep.cuh"
+#include "sweep_tma.cuh"
 
 namespace kkt {
 namespace {
+using tma::mbar_init;
+using tma::mbar_wait;
+using tma::tma_load;
 
 constexpr int kN6 = 1024;             // padded block size
 constexpr int kSl = kN6 / 16;         // row slices per block row
@@ -68,6 +72,7 @@ struct V6Params {
   unsigned* cnt;     // per chain group: row-completion counter (chain kernels)
   int g0;            // first chain group of this chain-kernel wave
   int jstar;         // block rows J >= jstar use row jstar's operators (ny: none)
+  long long* tim;    // KKT_V6_TIM: per-row clock64 phase sums of CTA 0 (6 per direction)
 };
 
 // Operator row of block row J, and its load: rows past jstar share one
@@ -198,19 +203,33 @@ __global__ void __launch_bounds__(kThr6, 1) v6_off_kernel(V6Params P) {
   }
 }
 
-// The dependent chain of one sweep direction for chain groups g0 .. g0 + gridDim.x/kSl - 1.
+// The dependent chain of one sweep direction for chain groups g0 .. g0 + gridDim.x/kSl - 1:
 //   L: y_J = c_J + G_J y_{J-1}  (J = 0 .. ny-1; c in W1, y to W0)
 //   U: x_J = d_J + H_J x_{J+1}  (J = ny-1 .. 0; d in W1, x to W0 and the job's outputs)
+// CTA (s, g) owns rows 16s..16s+15 of the 8 chains of group g.  Its operator
+// slice (128 KB) and y_{J-1} (64 KB) arrive by bulk copies into shared memory:
+// plain loads were bounded by the SM's outstanding-miss limit (~15 B/clk/SM
+// measured with the operands replaced by constants: the operator stream, not
+// the DMMA, set the row time), the copy engine is not.  The next row's slice
+// is copied while this row's reduction, outputs and row barrier run.  Each
+// output warp publishes its own stores (release after __syncwarp), 4 counts
+// per CTA and row, so no CTA barrier sits between the stores and the count.
+constexpr size_t kChainSmem = sizeof(double) * (16 * kN6 + kN6 * kG + 2 * 8 * 128) + 2 * sizeof(uint64_t);
+
 template <bool kUpper>
 __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
-  __shared__ double red[8 * 128];
+  extern __shared__ __align__(128) double sm6[];
+  double* As = sm6;                 // [ks 256][mt 2][lane 32]
+  double* Bs = As + 16 * kN6;       // [k 1024][8]
+  double* red2 = Bs + kN6 * kG;     // [row parity 2][warp 8][128]: no barrier between a row's reads and the next row's writes
+  uint64_t* barA = reinterpret_cast<uint64_t*>(red2 + 2 * 8 * 128);
+  uint64_t* barB = barA + 1;
   const int s = blockIdx.x % kSl, g = P.g0 + blockIdx.x / kSl;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ny = P.ny;
-  const double* Mbase = (kUpper ? P.Hp : P.Gp) + size_t(s) * kKS * 64 + lane;
-  const size_t mstride = size_t(kSl) * kKS * 64;  // doubles per packed block row
+  const double* Mbase = (kUpper ? P.Hp : P.Gp) + size_t(s) * kKS * 64;
+  const size_t mstride = size_t(kSl) * kKS * 64;
   unsigned* cnt = P.cnt + g;
-  // output thread's coordinates and job (U direction writes the step outputs)
   int m = 0, n = 0;
   const bool outt = threadIdx.x < 128;
   if (outt) slice_coords(threadIdx.x, m, n);
@@ -232,63 +251,90 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
     if (out) out[size_t(J) * P.nx + row] = v;
     if (out2) out2[size_t(J) * P.nx + row] = v + g2;
   };
+  // each output warp publishes its own stores (release after __syncwarp), so
+  // no CTA-wide barrier sits between the stores and the count; 4 per CTA and row
   auto signal = [&]() {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(cnt, 1u);
+    if (outt) {
+      __syncwarp();
+      if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(cnt) : "memory");
     }
   };
-  double a[kKW][2];
-  auto load_a = [&](int J) {
-    const bool res = J >= P.jstar;
-    const double* M = Mbase + size_t(oprow(J, P.jstar)) * mstride;
-#pragma unroll
-    for (int i = 0; i < kKW; ++i) {
-      const int ks = warp * kKW + i;
-      a[i][0] = ldop(M + size_t(ks) * 64, res);
-      a[i][1] = ldop(M + size_t(ks) * 64 + 32, res);
-    }
+  auto copy_a = [&](int J) {  // thread 0
+    tma_load(As, Mbase + size_t(oprow(J, P.jstar)) * mstride, sizeof(double) * 16 * kN6, barA);
   };
-  // first row: no inflow
+  if (threadIdx.x == 0) {
+    mbar_init(barA, 1);
+    mbar_init(barB, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
   {
     const int J = Jof(0);
     if (outt) emit(J, __ldcg(P.W1 + widx(g, J, ny) + size_t(row) * kG + n));
-    if (ny > 1) load_a(Jof(1));
     signal();
+    if (ny > 1 && threadIdx.x == 0) copy_a(Jof(1));
   }
+  const int bo = (lane & 3) * kG + (lane >> 2);
+  const bool tm = P.tim && blockIdx.x == 0 && threadIdx.x == 0;
+  long long ts[7] = {0, 0, 0, 0, 0, 0, 0}, acc[6] = {0, 0, 0, 0, 0, 0};
   for (int idx = 1; idx < ny; ++idx) {
     const int J = Jof(idx), Jp = kUpper ? J + 1 : J - 1;
+    if (tm) ts[0] = clock64();
+    const uint32_t par = uint32_t(idx - 1) & 1u;
     double cval = 0.0;
     if (outt) cval = __ldcg(P.W1 + widx(g, J, ny) + size_t(row) * kG + n);
-    // wait until every slice of the group has published row idx-1
     if (threadIdx.x == 0) {
-      const unsigned target = unsigned(idx) * kSl;
+      const unsigned target = unsigned(idx) * kSl * 4;
       unsigned v;
       do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
       } while (v < target);
+      if (tm) ts[1] = clock64();
+      // y_{J-1} was written by other CTAs through the generic proxy; the copy reads it through the async proxy
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      tma_load(Bs, P.W0 + widx(g, Jp, ny), sizeof(double) * kN6 * kG, barB);
     }
-    __syncthreads();
-    const double* B = P.W0 + widx(g, Jp, ny) + (lane & 3) * kG + (lane >> 2);
-    double b[kKW];
-#pragma unroll
-    for (int i = 0; i < kKW; ++i) b[i] = __ldcg(B + size_t(warp * kKW + i) * 4 * kG);
+    mbar_wait(barA, par);
+    if (tm) ts[2] = clock64();
+    mbar_wait(barB, par);
+    if (tm) ts[3] = clock64();
+    double* red = red2 + (idx & 1) * 8 * 128;
     double d[2][2][2] = {};
+    const double* Aw = As + size_t(warp * kKW) * 64 + lane;
+    const double* Bw = Bs + size_t(warp * kKW) * 4 * kG + bo;
 #pragma unroll
-    for (int i = 0; i < kKW; ++i) {
-      dmma6(d[i & 1][0][0], d[i & 1][0][1], a[i][0], b[i]);
-      dmma6(d[i & 1][1][0], d[i & 1][1][1], a[i][1], b[i]);
+    for (int i0 = 0; i0 < kKW; i0 += 8) {
+      double a0[8], a1[8], b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a0[u] = Aw[(i0 + u) * 64];
+        a1[u] = Aw[(i0 + u) * 64 + 32];
+        b[u] = Bw[(i0 + u) * 4 * kG];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        dmma6(d[u & 1][0][0], d[u & 1][0][1], a0[u], b[u]);
+        dmma6(d[u & 1][1][0], d[u & 1][1][1], a1[u], b[u]);
+      }
     }
-    if (idx + 1 < ny) load_a(Jof(idx + 1));
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) red[warp * 128 + (mt * 32 + lane) * 2 + e] = d[0][mt][e] + d[1][mt][e];
-    __syncthreads();
+    if (tm) ts[4] = clock64();
+    __syncthreads();  // As / Bs consumed by every warp; red complete
     if (outt) emit(J, cval + reduce8(red, threadIdx.x));
+    if (tm) ts[5] = clock64();
     signal();
+    if (idx + 1 < ny && threadIdx.x == 0) copy_a(Jof(idx + 1));
+    if (tm) {
+      ts[6] = clock64();
+      for (int q = 0; q < 6; ++q) acc[q] += ts[q + 1] - ts[q];
+    }
   }
+  if (tm)
+    for (int q = 0; q < 6; ++q) atomicAdd(reinterpret_cast<unsigned long long*>(P.tim + (kUpper ? 6 : 0) + q),
+                                          (unsigned long long)acc[q]);
 }
 
 // dev[2J + m] = max |M_J - M_{ny-1}|, mag[2J + m] = max |M_J|, M = Li (m = 0), Ui (m = 1)
@@ -336,7 +382,7 @@ void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(kSl * ngroups_wave);
   cfg.blockDim = dim3(kThr6);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = kChainSmem;
   cfg.stream = c->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // every CTA of the grid co-resident (row barriers)
@@ -354,15 +400,15 @@ void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
 int groups_per_wave() {
   static int gpw = 0;
   if (!gpw) {
-    int per_sm = 0;
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v6_chain_kernel<false>, kThr6, 0));
-    int per_sm_u = 0;
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_u, v6_chain_kernel<true>, kThr6, 0));
-    per_sm = std::min(per_sm, per_sm_u);
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kChainSmem)));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kChainSmem)));
+    int p0 = 0, p1 = 0;
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p0, v6_chain_kernel<false>, kThr6, kChainSmem));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, v6_chain_kernel<true>, kThr6, kChainSmem));
     int dev = 0, nsm = kSmCount;
     KKT_CUDA(cudaGetDevice(&dev));
     KKT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    gpw = std::max(1, per_sm * nsm / kSl);
+    gpw = std::max(1, std::min(p0, p1) * nsm / kSl);
   }
   return gpw;
 }
@@ -371,7 +417,8 @@ int groups_per_wave() {
 
 bool v6_supported(const Ctx* c) {
   static const bool force = std::getenv("KKT_SWEEP_V6") != nullptr;  // testing: v6 on v5 grids too
-  return c->mode == KKT_MODE_FAST && c->ny >= 2 && c->nx <= kN6 && (c->nx > 511 || (force && c->nx > 128));
+  static const bool off = std::getenv("KKT_SWEEP_V6_OFF") != nullptr;  // testing: sweep_fast.cu chains
+  return !off && c->mode == KKT_MODE_FAST && c->ny >= 2 && c->nx <= kN6 && (c->nx > 511 || (force && c->nx > 128));
 }
 
 // The block recursion D_J = T - cy^2 D_{J-1}^{-1} converges geometrically
@@ -468,6 +515,14 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.inv_ms = 1.0 / c->ms;
   P.coarse = coarse_terms ? 1 : 0;
   P.cnt = c->v6_cnt.p;
+  static const bool dbg = std::getenv("KKT_V6_TIM") != nullptr;
+  DBuf<long long> tim;
+  P.tim = nullptr;
+  if (dbg) {
+    tim.alloc(12);
+    KKT_CUDA(cudaMemsetAsync(tim.p, 0, sizeof(long long) * 12, c->stream));
+    P.tim = tim.p;
+  }
   const int gpw = groups_per_wave();
   static bool attr = false;
   if (!attr) {
@@ -495,6 +550,16 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
     }
   }
   c->tend(3);
+  if (dbg) {
+    long long h[12];
+    KKT_CUDA(cudaMemcpyAsync(h, tim.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+    const double rows = double(ny - 1) * nsteps;
+    for (int u = 0; u < 2; ++u)
+      std::fprintf(stderr, "v6 %s cycles/row (CTA 0): poll %.0f waitA %.0f waitB %.0f mma %.0f emit %.0f signal %.0f\n",
+                   u ? "U" : "L", h[6 * u] / rows, h[6 * u + 1] / rows, h[6 * u + 2] / rows, h[6 * u + 3] / rows,
+                   h[6 * u + 4] / rows, h[6 * u + 5] / rows);
+  }
 }
 
 }  // namespace kkt

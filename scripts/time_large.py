@@ -24,12 +24,15 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--nt", type=int, default=None)
     ap.add_argument("--nd", type=int, default=None)
+    ap.add_argument("--T", type=float, default=None, help="final time (config 4's per-GPU slab: --nt 128 --T 0.125)")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--mode", default="fast")
     a = ap.parse_args()
     p = P.config(a.config, Nd=a.nd)
     if a.nt:
         p = p.replace(Nt=a.nt)
+    if a.T:
+        p = p.replace(T=a.T)
     t0 = time.time()
     k = HeatKKT(p, mode=a.mode)
     torch.cuda.synchronize()
