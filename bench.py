@@ -501,8 +501,9 @@ def c2_microbench(local, reps=10):
     """BASELINE config 2, the preconditioner-apply microbench: 10 applications
     of P^-1 at 511^2 x 1024 steps, 64 subdomains, on seeded N(0,1) KKT vectors
     (device-generated here: timing only; parity is tests/test_gpu_large.py and
-    tests/test_gpu_v5.py).  The sweep runs sweep_v5.cu (fp64 DMMA), so its
-    roofline is the fp64 tensor peak."""
+    tests/test_gpu_v5.py, tests/test_gpu_v6.py).  The sweep runs sweep_v6.cu
+    (device-wide fp64 DMMA block substitution), so its roofline is the fp64
+    tensor peak."""
     import torch
     from paper_2305_04421_b200.solver import HeatKKT
     dev = torch.device("cuda", local)
@@ -531,7 +532,7 @@ def c2_microbench(local, reps=10):
     ts.sort()
     med = ts[len(ts) // 2]
     sw_ms = phase_ms[3] / max(1, phase_cnt[3])
-    # v5 arithmetic per RASQ apply: every block row of every spatial solve does
+    # v5/v6 arithmetic per RASQ apply: every block row of every spatial solve does
     # the dense on-chain product (G_J / H_J: nx^2 MACs per chain) and the
     # off-chain triangle (Li_J / Ui_J: nx^2/2), both sweep directions
     nx, ny, m = p.nx_int, p.ny_int, p.Nt // p.Nd
@@ -542,7 +543,7 @@ def c2_microbench(local, reps=10):
            "ms_per_apply_median": med, "ms_per_apply_min": ts[0],
            "value": 3 * p.block / (med / 1000.0), "unit": "unknowns/s per P^-1 apply",
            "sweep_ms_per_apply": sw_ms,
-           "roofline": {"kernel": "v5_kernel<512> (sweep_v5.cu: 16-CTA clusters, fp64 DMMA block substitution)",
+           "roofline": {"kernel": "v6_chain_kernel<512> + v6_off_kernel<512> (sweep_v6.cu: device-wide fp64 DMMA block substitution)",
                         "bound": "tensor", "achieved": tf, "peak": tpk, "unit": "TFLOP/s",
                         "frac": (tf / tpk) if (tf and tpk) else None, "peak_source": tpk_src,
                         "flops_per_apply": flops},

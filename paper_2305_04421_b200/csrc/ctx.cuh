@@ -125,7 +125,7 @@ struct Ctx {
   // fast v6 (sweep_v6.cu, 511 < nx <= 1024): fragment-ordered Li/Ui/G/H, block-vector workspaces
   DBuf<double> v6_ops, v6_w;
   DBuf<unsigned> v6_cnt;
-  int v6_jstar = 0, v6_nops = 0;
+  int v6_jstar = 0, v6_nops = 0, v6_kn = 0;
   DBuf<unsigned> v4_flags;
   int v4_nsets = 0;
   bool v4_coop = false, v4_registered = false;

@@ -1,5 +1,6 @@
-// sweep_v6.cu — FAST RASQ sweeps for the largest grids (511 < nx <= 1023:
-// BASELINE config 4), device-wide block substitution.
+// sweep_v6.cu — FAST RASQ sweeps for the large grids (255 < nx <= 1023:
+// BASELINE configs 2 and 4), device-wide block substitution; block size KN =
+// 512 (nx <= 511) or 1024.
 //
 // Same block recursion as sweep v5 (the reference's LU solve
 // BandedLU::solve_in_place, linalg.cpp:127-145, on the block factors of
@@ -8,8 +9,9 @@
 //     L:  y_J = Li_J b_J + G_J y_{J-1},   G_J = cy Li_J Ui_{J-1}
 //     U:  x_J = Ui_J y_J + H_J x_{J+1},   H_J = cy Ui_J Li_J
 // At nx = 1023 a block row is 1024 x 1024 doubles (8 MB): one cluster cannot
-// hold a row slice next to its vectors (v5's layout), so v6 spreads every
-// block step over the whole device instead:
+// hold a row slice next to its vectors (v5's layout); at nx = 511 v5's 16-CTA
+// clusters fit only 7 of 8 chain sets at once and wait on their triangle
+// imbalance.  v6 spreads every block step over the whole device instead:
 //   * off-chain terms first, for all J at once: c_J = Li_J b_J (d_J = Ui_J y_J)
 //     is a batched triangular product with no dependency (v6_off_kernel), the
 //     triangle streamed once per spatial solve for all local chains;
@@ -41,12 +43,15 @@ using tma::mbar_init;
 using tma::mbar_wait;
 using tma::tma_load;
 
-constexpr int kN6 = 1024;             // padded block size
-constexpr int kSl = kN6 / 16;         // row slices per block row
-constexpr int kKS = kN6 / 4;          // k-steps of a full row
+// KN: padded block size, 1024 (511 < nx <= 1023) or 512 (255 < nx <= 511)
 constexpr int kThr6 = 256;            // 8 warps
-constexpr int kKW = kKS / 8;          // k-steps per warp (chain kernel)
 constexpr int kG = 8;                 // chains per group (the n of m8n8k4)
+#define V6_DIMS                                                                          \
+  constexpr int kSl = KN / 16; /* row slices per block row */                           \
+  constexpr int kKS = KN / 4;  /* k-steps of a full row */                              \
+  constexpr int kKW = kKS / 8; /* k-steps per warp (chain kernel) */                    \
+  (void)kSl;                                                                             \
+  (void)kKW;
 
 __device__ __forceinline__ void dmma6(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -81,16 +86,18 @@ struct V6Params {
 __device__ __forceinline__ int oprow(int J, int jstar) { return J < jstar ? J : jstar; }
 __device__ __forceinline__ double ldop(const double* p, bool res) { return res ? __ldg(p) : __ldcs(p); }
 
-__device__ __forceinline__ size_t widx(int g, int J, int ny) { return (size_t(g) * ny + J) * kN6 * kG; }
+template <int KN>
+__device__ __forceinline__ size_t widx(int g, int J, int ny) { return (size_t(g) * ny + J) * KN * kG; }
 
 // b = in*scale + add - (Shat y_c)_node / ms, chain-interleaved (fast_chain_kernel's b)
+template <int KN>
 __global__ void __launch_bounds__(256) v6_form_b_kernel(V6Params P) {
-  const size_t total = size_t(P.ngroups) * P.ny * kN6 * kG;
+  const size_t total = size_t(P.ngroups) * P.ny * KN * kG;
   for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
     const int c = int(e % kG);
     const size_t r = e / kG;
-    const int k = int(r % kN6);
-    const size_t gj = r / kN6;
+    const int k = int(r % KN);
+    const size_t gj = r / KN;
     const int J = int(gj % P.ny), g = int(gj / P.ny);
     const int ch = g * kG + c;
     double v = 0.0;
@@ -135,20 +142,22 @@ __device__ __forceinline__ void slice_coords(int t, int& m, int& n) {
 // current 16 are multiplied.  A warp accumulates a slice over all its k-steps
 // itself, so no cross-warp reduction is needed.
 constexpr int kOffChunk = 16;
-constexpr size_t kOffSmem = sizeof(double) * 2 * kN6 * kG;
+template <int KN>
+constexpr size_t off_smem() { return sizeof(double) * 2 * KN * kG; }
 
-template <bool kUpper>
+template <int KN, bool kUpper>
 __global__ void __launch_bounds__(kThr6, 1) v6_off_kernel(V6Params P) {
+  V6_DIMS
   extern __shared__ double Bs[];  // [2][kN][8]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bo = (lane & 3) * kG + (lane >> 2);  // B fragment offset within a k-step
   for (int J = blockIdx.x; J < P.ny; J += gridDim.x) {
     for (int gp = 0; gp < P.ngroups; gp += 2) {
       __syncthreads();  // the previous pair's readers are done with Bs
-      for (int i = threadIdx.x; i < kN6 * kG; i += kThr6) {  // double2 units over both groups
-        const int gi = i / (kN6 * kG / 2), r = i - gi * (kN6 * kG / 2);
+      for (int i = threadIdx.x; i < KN * kG; i += kThr6) {  // double2 units over both groups
+        const int gi = i / (KN * kG / 2), r = i - gi * (KN * kG / 2);
         double2 v = make_double2(0.0, 0.0);
-        if (gp + gi < P.ngroups) v = __ldcg(reinterpret_cast<const double2*>(P.W0 + widx(gp + gi, J, P.ny)) + r);
+        if (gp + gi < P.ngroups) v = __ldcg(reinterpret_cast<const double2*>(P.W0 + widx<KN>(gp + gi, J, P.ny)) + r);
         reinterpret_cast<double2*>(Bs)[i] = v;
       }
       __syncthreads();
@@ -177,7 +186,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_off_kernel(V6Params P) {
           for (int u = 0; u < kOffChunk; ++u) {
             if (ks + u < ks1) {
               const double b0 = Bs[(4 * (ks + u)) * kG + bo];
-              const double b1 = Bs[kN6 * kG + (4 * (ks + u)) * kG + bo];
+              const double b1 = Bs[KN * kG + (4 * (ks + u)) * kG + bo];
               dmma6(d[0][0][0], d[0][0][1], ac[u][0], b0);
               dmma6(d[0][1][0], d[0][1][1], ac[u][1], b0);
               dmma6(d[1][0][0], d[1][0][1], ac[u][0], b1);
@@ -193,7 +202,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_off_kernel(V6Params P) {
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           if (gp + g >= P.ngroups) break;
-          double* O = P.W1 + widx(gp + g, J, P.ny) + size_t(16 * s + (lane >> 2)) * kG + 2 * (lane & 3);
+          double* O = P.W1 + widx<KN>(gp + g, J, P.ny) + size_t(16 * s + (lane >> 2)) * kG + 2 * (lane & 3);
 #pragma unroll
           for (int mt = 0; mt < 2; ++mt)
             *reinterpret_cast<double2*>(O + mt * 8 * kG) = make_double2(d[g][mt][0], d[g][mt][1]);
@@ -214,14 +223,16 @@ __global__ void __launch_bounds__(kThr6, 1) v6_off_kernel(V6Params P) {
 // is copied while this row's reduction, outputs and row barrier run.  Each
 // output warp publishes its own stores (release after __syncwarp), 4 counts
 // per CTA and row, so no CTA barrier sits between the stores and the count.
-constexpr size_t kChainSmem = sizeof(double) * (16 * kN6 + kN6 * kG + 2 * 8 * 128) + 2 * sizeof(uint64_t);
+template <int KN>
+constexpr size_t chain_smem() { return sizeof(double) * (16 * KN + KN * kG + 2 * 8 * 128) + 2 * sizeof(uint64_t); }
 
-template <bool kUpper>
+template <int KN, bool kUpper>
 __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
+  V6_DIMS
   extern __shared__ __align__(128) double sm6[];
-  double* As = sm6;                 // [ks 256][mt 2][lane 32]
-  double* Bs = As + 16 * kN6;       // [k 1024][8]
-  double* red2 = Bs + kN6 * kG;     // [row parity 2][warp 8][128]: no barrier between a row's reads and the next row's writes
+  double* As = sm6;                 // [ks KN/4][mt 2][lane 32]
+  double* Bs = As + 16 * KN;       // [k KN][8]
+  double* red2 = Bs + KN * kG;     // [row parity 2][warp 8][128]: no barrier between a row's reads and the next row's writes
   uint64_t* barA = reinterpret_cast<uint64_t*>(red2 + 2 * 8 * 128);
   uint64_t* barB = barA + 1;
   const int s = blockIdx.x % kSl, g = P.g0 + blockIdx.x / kSl;
@@ -247,7 +258,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
   }
   auto Jof = [&](int idx) { return kUpper ? ny - 1 - idx : idx; };
   auto emit = [&](int J, double v) {
-    P.W0[widx(g, J, ny) + size_t(row) * kG + n] = v;
+    P.W0[widx<KN>(g, J, ny) + size_t(row) * kG + n] = v;
     if (out) out[size_t(J) * P.nx + row] = v;
     if (out2) out2[size_t(J) * P.nx + row] = v + g2;
   };
@@ -260,7 +271,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
     }
   };
   auto copy_a = [&](int J) {  // thread 0
-    tma_load(As, Mbase + size_t(oprow(J, P.jstar)) * mstride, sizeof(double) * 16 * kN6, barA);
+    tma_load(As, Mbase + size_t(oprow(J, P.jstar)) * mstride, sizeof(double) * 16 * KN, barA);
   };
   if (threadIdx.x == 0) {
     mbar_init(barA, 1);
@@ -270,7 +281,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
   __syncthreads();
   {
     const int J = Jof(0);
-    if (outt) emit(J, __ldcg(P.W1 + widx(g, J, ny) + size_t(row) * kG + n));
+    if (outt) emit(J, __ldcg(P.W1 + widx<KN>(g, J, ny) + size_t(row) * kG + n));
     signal();
     if (ny > 1 && threadIdx.x == 0) copy_a(Jof(1));
   }
@@ -282,7 +293,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
     if (tm) ts[0] = clock64();
     const uint32_t par = uint32_t(idx - 1) & 1u;
     double cval = 0.0;
-    if (outt) cval = __ldcg(P.W1 + widx(g, J, ny) + size_t(row) * kG + n);
+    if (outt) cval = __ldcg(P.W1 + widx<KN>(g, J, ny) + size_t(row) * kG + n);
     if (threadIdx.x == 0) {
       const unsigned target = unsigned(idx) * kSl * 4;
       unsigned v;
@@ -292,7 +303,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
       if (tm) ts[1] = clock64();
       // y_{J-1} was written by other CTAs through the generic proxy; the copy reads it through the async proxy
       asm volatile("fence.proxy.async.global;\n" ::: "memory");
-      tma_load(Bs, P.W0 + widx(g, Jp, ny), sizeof(double) * kN6 * kG, barB);
+      tma_load(Bs, P.W0 + widx<KN>(g, Jp, ny), sizeof(double) * KN * kG, barB);
     }
     mbar_wait(barA, par);
     if (tm) ts[2] = clock64();
@@ -366,9 +377,11 @@ __global__ void __launch_bounds__(256) v6_conv_kernel(const double* __restrict__
 }
 
 // Fragment-order pack: dst[J][s][ks][mt][lane] = scale * src[J][16s+8mt+lane/4][4ks+lane%4]
+template <int KN>
 __global__ void v6_pack_kernel(const double* __restrict__ src, int nx, int nJ, double scale,
                                double* __restrict__ dst) {
-  const size_t per = size_t(kN6) * kN6, total = size_t(nJ) * per, nn = size_t(nx) * nx;
+  V6_DIMS
+  const size_t per = size_t(KN) * KN, total = size_t(nJ) * per, nn = size_t(nx) * nx;
   for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
     const size_t J = e / per;
     const int r = int(e - J * per);
@@ -378,11 +391,13 @@ __global__ void v6_pack_kernel(const double* __restrict__ src, int nx, int nJ, d
   }
 }
 
+template <int KN>
 void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
+  V6_DIMS
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(kSl * ngroups_wave);
   cfg.blockDim = dim3(kThr6);
-  cfg.dynamicSmemBytes = kChainSmem;
+  cfg.dynamicSmemBytes = chain_smem<KN>();
   cfg.stream = c->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // every CTA of the grid co-resident (row barriers)
@@ -391,20 +406,26 @@ void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
   cfg.numAttrs = 1;
   V6Params p = P;
   void* args[] = {&p};
-  const void* fn = upper ? reinterpret_cast<const void*>(&v6_chain_kernel<true>)
-                         : reinterpret_cast<const void*>(&v6_chain_kernel<false>);
+  const void* fn = upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true>)
+                         : reinterpret_cast<const void*>(&v6_chain_kernel<KN, false>);
   KKT_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
   c->launches++;
 }
 
+// chain groups per co-resident wave; also sets the kernels' shared-memory limits
+template <int KN>
 int groups_per_wave() {
+  V6_DIMS
   static int gpw = 0;
   if (!gpw) {
-    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kChainSmem)));
-    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kChainSmem)));
+    const int cs = int(chain_smem<KN>()), os = int(off_smem<KN>());
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
+    KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     int p0 = 0, p1 = 0;
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p0, v6_chain_kernel<false>, kThr6, kChainSmem));
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, v6_chain_kernel<true>, kThr6, kChainSmem));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p0, v6_chain_kernel<KN, false>, kThr6, cs));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, v6_chain_kernel<KN, true>, kThr6, cs));
     int dev = 0, nsm = kSmCount;
     KKT_CUDA(cudaGetDevice(&dev));
     KKT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -413,12 +434,42 @@ int groups_per_wave() {
   return gpw;
 }
 
+template <int KN>
+void pack(Ctx* c, const double* src, int nJ, double scale, double* dst) {
+  KKT_LAUNCH(c, v6_pack_kernel<KN>, kSmCount * 8, 256, 0, src, c->nx, nJ, scale, dst);
+}
+
+template <int KN>
+void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
+  const int gpw = groups_per_wave<KN>();
+  const int og = std::min(P.ny, kSmCount);
+  for (int t = 0; t < nsteps; ++t) {
+    P.t = t;
+    P.g0 = 0;
+    KKT_LAUNCH(c, v6_form_b_kernel<KN>, kSmCount * 8, 256, 0, P);
+    for (int dir = 0; dir < 2; ++dir) {
+      const bool up = dir == 1;
+      if (up)
+        KKT_LAUNCH(c, (v6_off_kernel<KN, true>), og, kThr6, off_smem<KN>(), P);
+      else
+        KKT_LAUNCH(c, (v6_off_kernel<KN, false>), og, kThr6, off_smem<KN>(), P);
+      KKT_CUDA(cudaMemsetAsync(P.cnt, 0, sizeof(unsigned) * ngroups, c->stream));
+      for (int g0 = 0; g0 < ngroups; g0 += gpw) {
+        P.g0 = g0;
+        launch_chain<KN>(c, up, P, std::min(gpw, ngroups - g0));
+      }
+    }
+  }
+}
+
 }  // namespace
 
 bool v6_supported(const Ctx* c) {
   static const bool force = std::getenv("KKT_SWEEP_V6") != nullptr;  // testing: v6 on v5 grids too
   static const bool off = std::getenv("KKT_SWEEP_V6_OFF") != nullptr;  // testing: sweep_fast.cu chains
-  return !off && c->mode == KKT_MODE_FAST && c->ny >= 2 && c->nx <= kN6 && (c->nx > 511 || (force && c->nx > 128));
+  // 255 < nx <= 1023 (configs 2 and 4): v6 measured 182 ms per P^-1 at config 2 against v5's 584;
+  // at nx = 255 (config 3) v5's cluster chains stay ahead (390 vs 446 ms, v6 padded to 512)
+  return !off && c->mode == KKT_MODE_FAST && c->ny >= 2 && c->nx <= 1024 && (c->nx > 255 || (force && c->nx > 128));
 }
 
 // The block recursion D_J = T - cy^2 D_{J-1}^{-1} converges geometrically
@@ -451,16 +502,23 @@ void build_v6(Ctx* c) {
   c->v6_jstar = v6_find_jstar(c);
   const int nops = std::min(ny, c->v6_jstar + 1);  // packed operator rows
   if (std::getenv("KKT_V6_TIM")) std::fprintf(stderr, "v6 jstar %d of ny %d\n", c->v6_jstar, ny);
-  const size_t mat = size_t(kN6) * kN6, nn = size_t(nx) * nx;
+  const int kn = nx <= 511 ? 512 : 1024;
+  const size_t mat = size_t(kn) * kn, nn = size_t(nx) * nx;
+  c->v6_kn = kn;
   c->v6_nops = nops;
   c->v6_ops.alloc(4 * size_t(nops) * mat);
   double* Lp = c->v6_ops.p;
   double* Up = Lp + nops * mat;
   double* Gp = Up + nops * mat;
   double* Hp = Gp + nops * mat;
-  const int pg = kSmCount * 8;
-  KKT_LAUNCH(c, v6_pack_kernel, pg, 256, 0, c->Li.p, nx, nops, 1.0, Lp);
-  KKT_LAUNCH(c, v6_pack_kernel, pg, 256, 0, c->Ui.p, nx, nops, 1.0, Up);
+  auto pk = [&](const double* src, int nJ, double scale, double* dst) {
+    if (kn == 512)
+      pack<512>(c, src, nJ, scale, dst);
+    else
+      pack<1024>(c, src, nJ, scale, dst);
+  };
+  pk(c->Li.p, nops, 1.0, Lp);
+  pk(c->Ui.p, nops, 1.0, Up);
   KKT_CUDA(cudaMemsetAsync(Gp, 0, sizeof(double) * mat, c->stream));  // G_0: unused
   if (nops == ny)
     KKT_CUDA(cudaMemsetAsync(Hp + size_t(ny - 1) * mat, 0, sizeof(double) * mat, c->stream));  // H_{ny-1}
@@ -472,23 +530,24 @@ void build_v6(Ctx* c) {
     GemmArgs g{c->Li.p + J0 * nn, c->Ui.p + (J0 - 1) * nn, T.p, nx, nx, nx,
                int64_t(nn), int64_t(nn), int64_t(nn), nx, nx, nx};
     gemm_f64(c, g, nb);
-    KKT_LAUNCH(c, v6_pack_kernel, pg, 256, 0, T.p, nx, nb, c->cy, Gp + J0 * mat);
+    pk(T.p, nb, c->cy, Gp + J0 * mat);
   }
   for (int J0 = 0; J0 < nh; J0 += Jb) {  // H_J = cy Ui_J Li_J
     const int nb = std::min(Jb, nh - J0);
     GemmArgs g{c->Ui.p + J0 * nn, c->Li.p + J0 * nn, T.p, nx, nx, nx,
                int64_t(nn), int64_t(nn), int64_t(nn), nx, nx, nx};
     gemm_f64(c, g, nb);
-    KKT_LAUNCH(c, v6_pack_kernel, pg, 256, 0, T.p, nx, nb, c->cy, Hp + J0 * mat);
+    pk(T.p, nb, c->cy, Hp + J0 * mat);
   }
   KKT_CUDA(cudaStreamSynchronize(c->stream));  // T is freed on return
 }
 
 void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms) {
   const int ny = c->ny;
-  const size_t mat = size_t(kN6) * kN6;
+  const int kn = c->v6_kn;
+  const size_t mat = size_t(kn) * kn;
   const int ngroups = (nchains + kG - 1) / kG;
-  const size_t need = size_t(ngroups) * ny * kN6 * kG;
+  const size_t need = size_t(ngroups) * ny * kn * kG;
   if (c->v6_w.n < 2 * need || c->v6_cnt.n < size_t(ngroups)) {
     KKT_CUDA(cudaStreamSynchronize(c->stream));
     c->v6_w.alloc(2 * need);
@@ -523,32 +582,11 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
     KKT_CUDA(cudaMemsetAsync(tim.p, 0, sizeof(long long) * 12, c->stream));
     P.tim = tim.p;
   }
-  const int gpw = groups_per_wave();
-  static bool attr = false;
-  if (!attr) {
-    KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kOffSmem)));
-    KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kOffSmem)));
-    attr = true;
-  }
-  const int og = std::min(ny, kSmCount);
   c->tbegin(3);
-  for (int t = 0; t < nsteps; ++t) {
-    P.t = t;
-    P.g0 = 0;
-    KKT_LAUNCH(c, v6_form_b_kernel, kSmCount * 8, 256, 0, P);
-    for (int dir = 0; dir < 2; ++dir) {
-      const bool up = dir == 1;
-      if (up)
-        KKT_LAUNCH(c, v6_off_kernel<true>, og, kThr6, kOffSmem, P);
-      else
-        KKT_LAUNCH(c, v6_off_kernel<false>, og, kThr6, kOffSmem, P);
-      KKT_CUDA(cudaMemsetAsync(P.cnt, 0, sizeof(unsigned) * ngroups, c->stream));
-      for (int g0 = 0; g0 < ngroups; g0 += gpw) {
-        P.g0 = g0;
-        launch_chain(c, up, P, std::min(gpw, ngroups - g0));
-      }
-    }
-  }
+  if (kn == 512)
+    run_steps<512>(c, P, nsteps, ngroups);
+  else
+    run_steps<1024>(c, P, nsteps, ngroups);
   c->tend(3);
   if (dbg) {
     long long h[12];

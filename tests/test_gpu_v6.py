@@ -1,5 +1,6 @@
-"""GPU: the device-wide FAST sweep for the largest grids (sweep_v6.cu,
-511 < nx <= 1023, BASELINE config 4's 1023-point rows) against STRICT mode,
+"""GPU: the device-wide FAST sweep for the large grids (sweep_v6.cu,
+255 < nx <= 1023: BASELINE config 2's 511-point rows on 512-blocks, config
+4's 1023-point rows on 1024-blocks) against STRICT mode,
 which is bitwise the reference's banded LU (test_gpu_parity.py), on grids
 short enough in y and t for STRICT to finish in seconds.
 
@@ -25,6 +26,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CASES = [
     # (Nx, Ny, Nt, Nd, precond)
     (600, 6, 8, 2, "two-level"),      # nx = 599, 2 chains
+    (512, 6, 8, 4, "two-level"),      # nx = 511: the full 512-block (config 2's)
+    (300, 9, 12, 12, "one-level"),    # nx = 299 on 512-blocks, 12 chains
     (1024, 4, 8, 4, "two-level"),     # nx = 1023: the full padded row (config 4's)
     (700, 12, 9, 3, "one-level"),     # 3 chains, one-level RASQ
     (520, 5, 40, 20, "two-level"),    # 20 chains: 3 groups, two chain-kernel waves
@@ -118,7 +121,7 @@ def test_v6_full_solve_against_strict():
 
 
 def test_v6_forced_on_v5_grid():
-    """KKT_SWEEP_V6=1 runs v6 on a v5 grid (nx = 199, zero padded to 1024):
+    """KKT_SWEEP_V6=1 runs v6 on a v5 grid (nx = 199, zero padded to 512):
     the same operator to rounding.  Subprocess: the switch is read once."""
     code = (
         "import numpy as np, torch; from paper_2305_04421_b200 import problems as P; "
@@ -167,3 +170,20 @@ def test_v6_resident_rows_against_streamed(tmp_path):
     n = x.size // 3
     for blk in range(3):
         assert _rel(x[blk * n:(blk + 1) * n], y[blk * n:(blk + 1) * n]) <= 1e-10, blk
+
+
+def test_v5_kn512_fallback():
+    """v5's 16-CTA kN = 512 clusters, now behind v6 for 255 < nx <= 511, stay
+    correct (KKT_SWEEP_V6_OFF=1): P^-1 against STRICT at nx = 299."""
+    code = (
+        "import numpy as np, torch; from paper_2305_04421_b200 import problems as P; "
+        "from paper_2305_04421_b200.solver import HeatKKT; "
+        "p = P.Problem(Lx=1.0, Ly=1.0, Nx=300, Ny=40, Nt=8, Nd=2, nu=0.1, omega=1e-2, "
+        "precond='two-level', coarse_variant='scalar', tol=1e-8, restart=20); "
+        "v = torch.from_numpy(P.random_kkt(p, 1)).cuda(); "
+        "a = HeatKKT(p, mode='fast').apply_P_inv(v).cpu().numpy(); "
+        "b = HeatKKT(p, mode='strict').apply_P_inv(v).cpu().numpy(); "
+        "print('REL', np.linalg.norm(a - b) / np.linalg.norm(b))")
+    r = _run_sub(code, {"KKT_SWEEP_V6_OFF": "1"}, None)
+    rel = float([x for x in r.stdout.splitlines() if x.startswith("REL")][0].split()[1])
+    assert rel <= 1e-10, rel
