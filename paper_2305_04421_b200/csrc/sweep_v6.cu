@@ -1,6 +1,6 @@
-// sweep_v6.cu — FAST RASQ sweeps for the large grids (255 < nx <= 1023:
-// BASELINE configs 2 and 4), device-wide block substitution; block size KN =
-// 512 (nx <= 511) or 1024.
+// sweep_v6.cu — FAST RASQ sweeps for the large grids (128 < nx <= 1023:
+// BASELINE configs 2, 3 and 4), device-wide block substitution; block size
+// KN = 256 (nx <= 255), 512 (nx <= 511) or 1024.
 //
 // Same block recursion as sweep v5 (the reference's LU solve
 // BandedLU::solve_in_place, linalg.cpp:127-145, on the block factors of
@@ -465,11 +465,10 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
 }  // namespace
 
 bool v6_supported(const Ctx* c) {
-  static const bool force = std::getenv("KKT_SWEEP_V6") != nullptr;  // testing: v6 on v5 grids too
   static const bool off = std::getenv("KKT_SWEEP_V6_OFF") != nullptr;  // testing: sweep_fast.cu chains
-  // 255 < nx <= 1023 (configs 2 and 4): v6 measured 182 ms per P^-1 at config 2 against v5's 584;
-  // at nx = 255 (config 3) v5's cluster chains stay ahead (390 vs 446 ms, v6 padded to 512)
-  return !off && c->mode == KKT_MODE_FAST && c->ny >= 2 && c->nx <= 1024 && (c->nx > 255 || (force && c->nx > 128));
+  // 128 < nx <= 1023 (configs 2, 3 and 4).  P^-1 measured against v5's cluster chains:
+  // config 2 181 vs 584 ms, config 3 310 vs 390 ms.  v5 stays as the KKT_SWEEP_V6_OFF=1 fallback.
+  return !off && c->mode == KKT_MODE_FAST && c->ny >= 2 && c->nx <= 1024 && c->nx > 128;
 }
 
 // The block recursion D_J = T - cy^2 D_{J-1}^{-1} converges geometrically
@@ -502,7 +501,7 @@ void build_v6(Ctx* c) {
   c->v6_jstar = v6_find_jstar(c);
   const int nops = std::min(ny, c->v6_jstar + 1);  // packed operator rows
   if (std::getenv("KKT_V6_TIM")) std::fprintf(stderr, "v6 jstar %d of ny %d\n", c->v6_jstar, ny);
-  const int kn = nx <= 511 ? 512 : 1024;
+  const int kn = nx <= 255 ? 256 : nx <= 511 ? 512 : 1024;
   const size_t mat = size_t(kn) * kn, nn = size_t(nx) * nx;
   c->v6_kn = kn;
   c->v6_nops = nops;
@@ -512,7 +511,9 @@ void build_v6(Ctx* c) {
   double* Gp = Up + nops * mat;
   double* Hp = Gp + nops * mat;
   auto pk = [&](const double* src, int nJ, double scale, double* dst) {
-    if (kn == 512)
+    if (kn == 256)
+      pack<256>(c, src, nJ, scale, dst);
+    else if (kn == 512)
       pack<512>(c, src, nJ, scale, dst);
     else
       pack<1024>(c, src, nJ, scale, dst);
@@ -583,7 +584,9 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
     P.tim = tim.p;
   }
   c->tbegin(3);
-  if (kn == 512)
+  if (kn == 256)
+    run_steps<256>(c, P, nsteps, ngroups);
+  else if (kn == 512)
     run_steps<512>(c, P, nsteps, ngroups);
   else
     run_steps<1024>(c, P, nsteps, ngroups);

@@ -1,6 +1,9 @@
-"""GPU: the large-grid FAST sweep (sweep_v5.cu, 128 < nx <= 511) against
-STRICT mode, which is bitwise the reference's banded LU (test_gpu_parity.py),
-on grids small enough in time for STRICT to finish in seconds.
+"""GPU: the large-grid FAST sweeps against STRICT mode, which is bitwise the
+reference's banded LU (test_gpu_parity.py), on grids small enough in time for
+STRICT to finish in seconds.  The in-process tests run the default sweep for
+128 < nx <= 511, which is sweep v6 (sweep_v6.cu) since it replaced v5 there;
+sweep v5 (sweep_v5.cu) itself is checked in subprocesses with
+KKT_SWEEP_V6_OFF=1 (the switch is read once per process).
 
 Covers both cluster shapes (kN = 256: 8-CTA clusters; kN = 512: 16-CTA
 clusters), chain counts that do not fill a set of 8, the window solves
@@ -100,7 +103,7 @@ def test_v5_resident_rows_used():
             "p = P.Problem(Lx=1.0, Ly=1.0, Nx=160, Ny=400, Nt=8, Nd=2, nu=1e-3, omega=1e-2, "
             "precond='one-level', coarse_variant='scalar', tol=1e-8, restart=20); "
             "HeatKKT(p, mode='fast'); torch.cuda.synchronize()")
-    env = dict(os.environ, KKT_V5_TIM="1")
+    env = dict(os.environ, KKT_V5_TIM="1", KKT_SWEEP_V6_OFF="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stderr[-2000:]
@@ -108,3 +111,28 @@ def test_v5_resident_rows_used():
     assert line, r.stderr[-2000:]
     js, ny = int(line[0].split()[2]), int(line[0].split()[5])
     assert 0 < js < ny - 1, line[0]
+
+
+@pytest.mark.parametrize("case", [CASES[0], CASES[3], CASES[6]], ids=["kN256_4ch", "kN256_10ch", "kN256_resident"])
+def test_v5_fallback_against_strict(case):
+    """Sweep v5 (KKT_SWEEP_V6_OFF=1), kN = 256 cluster chains: P^-1 against STRICT."""
+    import os
+    import subprocess
+    import sys
+    Nx, Ny, Nt, Nd, pre = case[:5]
+    nu = case[5] if len(case) > 5 else 0.1
+    code = (
+        "import numpy as np, torch; from paper_2305_04421_b200 import problems as P; "
+        "from paper_2305_04421_b200.solver import HeatKKT; "
+        f"p = P.Problem(Lx=1.0, Ly=1.0, Nx={Nx}, Ny={Ny}, Nt={Nt}, Nd={Nd}, nu={nu}, omega=1e-2, "
+        f"precond='{pre}', coarse_variant='scalar', tol=1e-8, restart=20); "
+        "v = torch.from_numpy(P.random_kkt(p, 1)).cuda(); "
+        "a = HeatKKT(p, mode='fast').apply_P_inv(v).cpu().numpy(); "
+        "b = HeatKKT(p, mode='strict').apply_P_inv(v).cpu().numpy(); "
+        "B = p.block; print('REL', max(np.linalg.norm(a[k*B:(k+1)*B] - b[k*B:(k+1)*B]) / np.linalg.norm(b[k*B:(k+1)*B]) for k in range(3)))")
+    env = dict(os.environ, KKT_SWEEP_V6_OFF="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    rel = float([x for x in r.stdout.splitlines() if x.startswith("REL")][0].split()[1])
+    assert rel <= 1e-10, rel

@@ -1,6 +1,6 @@
 """GPU: the device-wide FAST sweep for the large grids (sweep_v6.cu,
-255 < nx <= 1023: BASELINE config 2's 511-point rows on 512-blocks, config
-4's 1023-point rows on 1024-blocks) against STRICT mode,
+128 < nx <= 1023: config 3's 255-point rows on 256-blocks, config 2's 511 on
+512-blocks, config 4's 1023 on 1024-blocks) against STRICT mode,
 which is bitwise the reference's banded LU (test_gpu_parity.py), on grids
 short enough in y and t for STRICT to finish in seconds.
 
@@ -120,23 +120,17 @@ def test_v6_full_solve_against_strict():
     assert _rel(x, y) <= 1e-7, _rel(x, y)
 
 
-def test_v6_forced_on_v5_grid():
-    """KKT_SWEEP_V6=1 runs v6 on a v5 grid (nx = 199, zero padded to 512):
-    the same operator to rounding.  Subprocess: the switch is read once."""
-    code = (
-        "import numpy as np, torch; from paper_2305_04421_b200 import problems as P; "
-        "from paper_2305_04421_b200.solver import HeatKKT; "
-        "p = P.Problem(Lx=1.0, Ly=1.0, Nx=200, Ny=30, Nt=8, Nd=4, nu=0.1, omega=1e-2, "
-        "precond='two-level', coarse_variant='scalar', tol=1e-8, restart=20); "
-        "v = torch.from_numpy(P.random_kkt(p, 1)).cuda(); "
-        "a = HeatKKT(p, mode='fast').apply_P_inv(v).cpu().numpy(); "
-        "b = HeatKKT(p, mode='strict').apply_P_inv(v).cpu().numpy(); "
-        "print('REL', np.linalg.norm(a - b) / np.linalg.norm(b))")
-    env = dict(os.environ, KKT_SWEEP_V6="1")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
-    assert r.returncode == 0, r.stderr[-2000:]
-    rel = float([x for x in r.stdout.splitlines() if x.startswith("REL")][0].split()[1])
-    assert rel <= 1e-10, rel
+def test_v6_kn256_grid():
+    """v6 on a 256-block (nx = 199, zero padded to 256; config 3's block size)
+    against STRICT, with 4 chains and the fused two-level residual."""
+    import torch
+    from paper_2305_04421_b200.solver import HeatKKT
+    p = P.Problem(Lx=1.0, Ly=1.0, Nx=200, Ny=30, Nt=8, Nd=4, nu=0.1, omega=1e-2, precond="two-level",
+                  coarse_variant="scalar", tol=1e-8, restart=20)
+    v = torch.from_numpy(P.random_kkt(p, 1)).cuda()
+    a = HeatKKT(p, mode="fast").apply_P_inv(v).cpu().numpy()
+    b = HeatKKT(p, mode="strict").apply_P_inv(v).cpu().numpy()
+    assert _rel(a, b) <= 1e-10, _rel(a, b)
 
 
 def _run_sub(code, env_extra, tmp):
