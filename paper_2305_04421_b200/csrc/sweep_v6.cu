@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_off_kernel(V6Params P) {
 // output warp publishes its own stores (release after __syncwarp), 4 counts
 // per CTA and row, so no CTA barrier sits between the stores and the count.
 template <int KN>
-constexpr size_t chain_smem() { return sizeof(double) * (16 * KN + KN * kG + 2 * 8 * 128) + 2 * sizeof(uint64_t); }
+constexpr size_t chain_smem() { return sizeof(double) * (16 * KN + KN * kG + 8 * 128) + 2 * sizeof(uint64_t); }
 
 template <int KN, bool kUpper>
 __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
@@ -232,8 +232,8 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
   extern __shared__ __align__(128) double sm6[];
   double* As = sm6;                 // [ks KN/4][mt 2][lane 32]
   double* Bs = As + 16 * KN;       // [k KN][8]
-  double* red2 = Bs + KN * kG;     // [row parity 2][warp 8][128]: no barrier between a row's reads and the next row's writes
-  uint64_t* barA = reinterpret_cast<uint64_t*>(red2 + 2 * 8 * 128);
+  double* red = Bs + KN * kG;      // [warp 8][128]
+  uint64_t* barA = reinterpret_cast<uint64_t*>(red + 8 * 128);
   uint64_t* barB = barA + 1;
   const int s = blockIdx.x % kSl, g = P.g0 + blockIdx.x / kSl;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -305,11 +305,14 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
       asm volatile("fence.proxy.async.global;\n" ::: "memory");
       tma_load(Bs, P.W0 + widx<KN>(g, Jp, ny), sizeof(double) * KN * kG, barB);
     }
+    // the previous row's readers of red are done (costs nothing: every warp
+    // waits for thread 0's copy of y_{J-1} below anyway); one red buffer keeps
+    // the KN = 512 kernel at 2 CTAs per SM
+    __syncthreads();
     mbar_wait(barA, par);
     if (tm) ts[2] = clock64();
     mbar_wait(barB, par);
     if (tm) ts[3] = clock64();
-    double* red = red2 + (idx & 1) * 8 * 128;
     double d[2][2][2] = {};
     const double* Aw = As + size_t(warp * kKW) * 64 + lane;
     const double* Bw = Bs + size_t(warp * kKW) * 4 * kG + bo;
