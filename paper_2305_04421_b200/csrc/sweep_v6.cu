@@ -212,6 +212,130 @@ __global__ void __launch_bounds__(kThr6, 1) v6_off_kernel(V6Params P) {
   }
 }
 
+// TMA-streamed batched triangular products (default for KN >= 512; KKT_V6_OFF=1
+// selects v6_off_kernel above; measured P^-1: config 2 181.5 -> 176.3 ms,
+// config-4 slab 174.9 -> 165.9 ms; at KN = 256 the plain kernel stays, 308 vs 312 ms).  The plain loads of v6_off_kernel are bounded by the
+// SM's outstanding misses (~3.2 TB/s over the device); here one producer warp
+// streams each slice's nonzero k-steps in 32 KB bulk copies through a 2-slot
+// ring, and 8 consumer warps split every chunk along k, accumulate the slice
+// in registers and reduce it through shared memory (double-buffered by slice
+// parity, one named barrier per slice) in a fixed order.
+constexpr int kOffRing = 2;      // ring slots
+constexpr int kOffCk = 64;       // k-steps per chunk (32 KB)
+constexpr int kOffThr = 288;     // 8 consumer warps + 1 producer warp
+template <int KN>
+constexpr size_t off2_smem() {
+  return sizeof(double) * (2 * KN * kG + kOffRing * kOffCk * 64 + 2 * 8 * 256) + 8 * sizeof(uint64_t);
+}
+
+template <int KN, bool kUpper>
+__global__ void __launch_bounds__(kOffThr, 1) v6_off2_kernel(V6Params P) {
+  V6_DIMS
+  extern __shared__ __align__(128) double so[];
+  double* Bs = so;                               // [2][KN][8]
+  double* ring = Bs + 2 * KN * kG;               // [slot][kOffCk][64]
+  double* red = ring + kOffRing * kOffCk * 64;   // [slice parity 2][warp 8][256]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * 8 * 256);
+  uint64_t* empty = full + kOffRing;
+  uint64_t* barB = empty + kOffRing;
+  uint64_t* bfree = barB + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kOffRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 8);
+    }
+    mbar_init(barB, 1);
+    mbar_init(bfree, 8);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const double* T = kUpper ? P.Up : P.Lp;
+  if (warp == 8) {  // producer
+    if (lane == 0) {
+      int it = 0, item = 0;
+      for (int J = blockIdx.x; J < P.ny; J += gridDim.x) {
+        const double* TJ = T + size_t(oprow(J, P.jstar)) * kSl * kKS * 64;
+        for (int gp = 0; gp < P.ngroups; gp += 2, ++item) {
+          if (item > 0) mbar_wait(bfree, uint32_t(item - 1) & 1u);
+          const int g1 = gp + 1 < P.ngroups ? gp + 1 : gp;  // a missing partner reads gp (outputs not written)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tma::smem_u32(barB)),
+                       "r"(uint32_t(sizeof(double) * 2 * KN * kG))
+                       : "memory");
+          const uint32_t vb = uint32_t(sizeof(double) * KN * kG);
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                           tma::smem_u32(Bs)), "l"(P.W0 + widx<KN>(gp, J, P.ny)), "r"(vb), "r"(tma::smem_u32(barB))
+                       : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                           tma::smem_u32(Bs + KN * kG)), "l"(P.W0 + widx<KN>(g1, J, P.ny)), "r"(vb), "r"(tma::smem_u32(barB))
+                       : "memory");
+          for (int s = 0; s < kSl; ++s) {
+            const int ks0 = kUpper ? 4 * s : 0, ks1 = kUpper ? kKS : 4 * s + 4;
+            for (int kb = ks0; kb < ks1; kb += kOffCk, ++it) {
+              const int slot = it % kOffRing, len = min(kOffCk, ks1 - kb);
+              if (it >= kOffRing) mbar_wait(&empty[slot], uint32_t(it / kOffRing - 1) & 1u);
+              tma_load(ring + size_t(slot) * kOffCk * 64, TJ + (size_t(s) * kKS + kb) * 64,
+                       uint32_t(sizeof(double) * 64 * len), &full[slot]);
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+  const int bo = (lane & 3) * kG + (lane >> 2);
+  int it = 0, item = 0, sl = 0;
+  for (int J = blockIdx.x; J < P.ny; J += gridDim.x) {
+    for (int gp = 0; gp < P.ngroups; gp += 2, ++item) {
+      mbar_wait(barB, uint32_t(item) & 1u);
+      for (int s = 0; s < kSl; ++s, ++sl) {
+        const int ks0 = kUpper ? 4 * s : 0, ks1 = kUpper ? kKS : 4 * s + 4;
+        double d[2][2][2] = {};
+        for (int kb = ks0; kb < ks1; kb += kOffCk, ++it) {
+          const int slot = it % kOffRing, len = min(kOffCk, ks1 - kb);
+          mbar_wait(&full[slot], uint32_t(it / kOffRing) & 1u);
+          const double* R = ring + size_t(slot) * kOffCk * 64 + lane;
+#pragma unroll
+          for (int q = 0; q < kOffCk / 8; ++q) {
+            const int u = warp + 8 * q;
+            if (u < len) {
+              const double a0 = R[u * 64], a1 = R[u * 64 + 32];
+              const double b0 = Bs[(4 * (kb + u)) * kG + bo];
+              const double b1 = Bs[KN * kG + (4 * (kb + u)) * kG + bo];
+              dmma6(d[0][0][0], d[0][0][1], a0, b0);
+              dmma6(d[0][1][0], d[0][1][1], a1, b0);
+              dmma6(d[1][0][0], d[1][0][1], a0, b1);
+              dmma6(d[1][1][0], d[1][1][1], a1, b1);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tma::smem_u32(&empty[slot])) : "memory");
+        }
+        double* rw = red + size_t(sl & 1) * 8 * 256 + warp * 256;
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) rw[g * 128 + (mt * 32 + lane) * 2 + e] = d[g][mt][e];
+        asm volatile("bar.sync 1, 256;\n" ::: "memory");
+        {
+          const int t = threadIdx.x, g = t >> 7, r = t & 127;
+          int m, n;
+          slice_coords(r, m, n);
+          const double* rr = red + size_t(sl & 1) * 8 * 256 + g * 128 + r;
+          double v = 0.0;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) v += rr[w * 256];
+          if (gp + g < P.ngroups) P.W1[widx<KN>(gp + g, J, P.ny) + size_t(16 * s + m) * kG + n] = v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tma::smem_u32(bfree)) : "memory");
+    }
+  }
+}
+
 // The dependent chain of one sweep direction for chain groups g0 .. g0 + gridDim.x/kSl - 1:
 //   L: y_J = c_J + G_J y_{J-1}  (J = 0 .. ny-1; c in W1, y to W0)
 //   U: x_J = d_J + H_J x_{J+1}  (J = ny-1 .. 0; d in W1, x to W0 and the job's outputs)
@@ -394,6 +518,11 @@ __global__ void v6_pack_kernel(const double* __restrict__ src, int nx, int nJ, d
   }
 }
 
+bool off_plain() {  // KKT_V6_OFF=1: the plain-load off-chain kernel
+  static const bool v = std::getenv("KKT_V6_OFF") != nullptr;
+  return v;
+}
+
 template <int KN>
 void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
   V6_DIMS
@@ -426,6 +555,9 @@ int groups_per_wave() {
     KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
+    const int os2 = int(off2_smem<KN>());
+    KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
+    KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
     int p0 = 0, p1 = 0;
     KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p0, v6_chain_kernel<KN, false>, kThr6, cs));
     KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, v6_chain_kernel<KN, true>, kThr6, cs));
@@ -452,10 +584,17 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
     KKT_LAUNCH(c, v6_form_b_kernel<KN>, kSmCount * 8, 256, 0, P);
     for (int dir = 0; dir < 2; ++dir) {
       const bool up = dir == 1;
-      if (up)
-        KKT_LAUNCH(c, (v6_off_kernel<KN, true>), og, kThr6, off_smem<KN>(), P);
-      else
-        KKT_LAUNCH(c, (v6_off_kernel<KN, false>), og, kThr6, off_smem<KN>(), P);
+      if (off_plain() || KN == 256) {  // 256-blocks: one small copy per slice, plain loads measured ahead
+        if (up)
+          KKT_LAUNCH(c, (v6_off_kernel<KN, true>), og, kThr6, off_smem<KN>(), P);
+        else
+          KKT_LAUNCH(c, (v6_off_kernel<KN, false>), og, kThr6, off_smem<KN>(), P);
+      } else {
+        if (up)
+          KKT_LAUNCH(c, (v6_off2_kernel<KN, true>), og, kOffThr, off2_smem<KN>(), P);
+        else
+          KKT_LAUNCH(c, (v6_off2_kernel<KN, false>), og, kOffThr, off2_smem<KN>(), P);
+      }
       KKT_CUDA(cudaMemsetAsync(P.cnt, 0, sizeof(unsigned) * ngroups, c->stream));
       for (int g0 = 0; g0 < ngroups; g0 += gpw) {
         P.g0 = g0;
