@@ -565,6 +565,8 @@ int groups_per_wave() {
     KKT_CUDA(cudaGetDevice(&dev));
     KKT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     gpw = std::max(1, std::min(p0, p1) * nsm / kSl);
+    if (std::getenv("KKT_V6_TIM"))
+      std::fprintf(stderr, "v6 KN %d: %d chain CTAs per SM, %d chain groups per wave\n", KN, std::min(p0, p1), gpw);
   }
   return gpw;
 }
