@@ -620,7 +620,7 @@ def main():
     ap.add_argument("--no-alt", action="store_true", help="skip the SPECTRAL side measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the config-2 P^-1 microbench")
-    ap.add_argument("--c4", action="store_true", help="add the config-4 per-GPU-slab P^-1 microbench (~4 min setup)")
+    ap.add_argument("--c4", action="store_true", help="add the config-4 per-GPU-slab P^-1 microbench (~40 s setup)")
     args = ap.parse_args()
     ws, rank, local = dist_setup(args)
     try:

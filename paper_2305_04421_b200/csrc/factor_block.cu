@@ -57,16 +57,68 @@ __global__ void __launch_bounds__(kLuThreads) dense_lu_nopiv_kernel(int n, doubl
 
 // Li = (unit lower of A)^{-1}, Ui = (upper of A)^{-1}; one thread per column,
 // columns spread over CTAs.
+// The same unpivoted LU, spread over a co-resident grid with a grid barrier
+// after the multipliers and after the rank-1 update of every column: each
+// element sees exactly the single-CTA kernel's operations in the same order
+// (the division, then fma(-A[i][j], A[j][c], A[i][c]) for j ascending), so the
+// factors are bitwise those of dense_lu_nopiv_kernel.  That kernel took
+// ~148 ms per 1023 x 1023 block on one SM, 72% of the config-4 setup.
+// All reads of A go through L2 (__ldcg): other CTAs wrote it since the last barrier.
+constexpr int kLuCoopThreads = 512;
+
+__global__ void __launch_bounds__(kLuCoopThreads) dense_lu_nopiv_coop_kernel(int n, double tol, double* A,
+                                                                             int* status, unsigned* bar) {
+  const int nt = gridDim.x * blockDim.x, gt = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned target = 0;
+  auto gsync = [&]() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      target += gridDim.x;
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
+      } while (v < target);
+    }
+    __syncthreads();
+  };
+  for (int j = 0; j < n; ++j) {
+    const double d = __ldcg(&A[int64_t(j) * n + j]);
+    if (!(fabs(d) > tol)) {
+      if (gt == 0) *status = j;
+      return;  // every CTA reads the same pivot: a uniform exit
+    }
+    for (int i = j + 1 + gt; i < n; i += nt) A[int64_t(i) * n + j] = __ldcg(&A[int64_t(i) * n + j]) / d;
+    gsync();
+    const int rows = n - j - 1;
+    const int64_t pairs = int64_t(rows) * rows;
+    for (int64_t t = gt; t < pairs; t += nt) {
+      const int i = j + 1 + int(t / rows);
+      const int c = j + 1 + int(t % rows);
+      A[int64_t(i) * n + c] =
+          fma(-__ldcg(&A[int64_t(i) * n + j]), __ldcg(&A[int64_t(j) * n + c]), __ldcg(&A[int64_t(i) * n + c]));
+    }
+    gsync();
+  }
+  if (gt == 0) *status = -1;
+}
+
+// Threads 0..n-1 invert L (column b each), threads n..2n-1 invert U: the two
+// sequential column solves run side by side (same operations per element).
 __global__ void tri_inverse_kernel(int n, const double* __restrict__ A, double* __restrict__ Li,
                                    double* __restrict__ Ui) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= n) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2 * n) return;
+  const bool upper = t >= n;
+  const int b = upper ? t - n : t;
+  if (!upper)
   for (int a = 0; a < n; ++a) {
     double acc = (a == b) ? 1.0 : 0.0;
     if (a > b)
       for (int k = b; k < a; ++k) acc = fma(-A[int64_t(a) * n + k], Li[int64_t(k) * n + b], acc);
     Li[int64_t(a) * n + b] = acc;
   }
+  if (upper)
   for (int a = n - 1; a >= 0; --a) {
     double acc = 0.0;
     if (a <= b) {
@@ -130,15 +182,38 @@ void build_block_recursion(Ctx* c) {
   c->Ui.alloc(size_t(ny) * nn);
   DBuf<double> D(nn), S(nn);
   DBuf<int> st(1);
+  DBuf<unsigned> bar(1);
   const double cy2 = c->cy * c->cy;
   const dim3 gg((nx + 31) / 32, (nx + 31) / 32), gb(32, 8);
   for (int J = 0; J < ny; ++J) {
     KKT_LAUNCH(c, form_d_kernel, kSmCount * 2, 256, 0, nx, c->Ahat.diag, c->Ahat.mcx, cy2,
                J > 0 ? S.p : nullptr, D.p);
-    KKT_LAUNCH(c, dense_lu_nopiv_kernel, 1, kLuThreads, 0, nx, tol, D.p, st.p);
+    static const bool single = getenv("KKT_LU_SINGLE") != nullptr;  // testing: the one-CTA kernel
+    if (single) {
+      KKT_LAUNCH(c, dense_lu_nopiv_kernel, 1, kLuThreads, 0, nx, tol, D.p, st.p);
+    } else {
+      KKT_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(unsigned), c->stream));
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(kSmCount);
+      cfg.blockDim = dim3(kLuCoopThreads);
+      cfg.stream = c->stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers: every CTA co-resident
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n_ = nx;
+      double tol_ = tol;
+      double* A_ = D.p;
+      int* st_ = st.p;
+      unsigned* bar_ = bar.p;
+      void* args[] = {&n_, &tol_, &A_, &st_, &bar_};
+      KKT_CUDA(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(&dense_lu_nopiv_coop_kernel), args));
+      c->launches++;
+    }
     double* Li = c->Li.p + J * nn;
     double* Ui = c->Ui.p + J * nn;
-    KKT_LAUNCH(c, tri_inverse_kernel, (nx + 127) / 128, 128, 0, nx, D.p, Li, Ui);
+    KKT_LAUNCH(c, tri_inverse_kernel, (2 * nx + 63) / 64, 64, 0, nx, D.p, Li, Ui);
     if (J + 1 < ny) KKT_LAUNCH(c, gemm_kernel, gg, gb, 0, nx, Ui, Li, S.p);
     int hs = -1;
     KKT_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));

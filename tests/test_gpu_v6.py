@@ -181,3 +181,20 @@ def test_v5_kn512_fallback():
     r = _run_sub(code, {"KKT_SWEEP_V6_OFF": "1"}, None)
     rel = float([x for x in r.stdout.splitlines() if x.startswith("REL")][0].split()[1])
     assert rel <= 1e-10, rel
+
+
+def test_block_lu_grid_kernel_bitwise(tmp_path):
+    """The block recursion's dense LU on a co-resident grid (factor_block.cu)
+    does each element's operations in the single-CTA kernel's order, so the
+    whole FAST P^-1 is bitwise the same with KKT_LU_SINGLE=1."""
+    code = (
+        "import sys, numpy as np, torch; from paper_2305_04421_b200 import problems as P; "
+        "from paper_2305_04421_b200.solver import HeatKKT; "
+        "p = P.Problem(Lx=1.0, Ly=1.0, Nx=600, Ny=6, Nt=8, Nd=2, nu=0.1, omega=1e-2, "
+        "precond='two-level', coarse_variant='scalar', tol=1e-8, restart=20); "
+        "v = torch.from_numpy(P.random_kkt(p, 1)).cuda(); "
+        "np.save(sys.argv[1], HeatKKT(p, mode='fast').apply_P_inv(v).cpu().numpy())")
+    a, b = str(tmp_path / "grid.npy"), str(tmp_path / "single.npy")
+    _run_sub(code.replace("sys.argv[1]", repr(a)), {}, tmp_path)
+    _run_sub(code.replace("sys.argv[1]", repr(b)), {"KKT_LU_SINGLE": "1"}, tmp_path)
+    assert np.array_equal(np.load(a), np.load(b))
