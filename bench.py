@@ -560,7 +560,7 @@ def c4_microbench(local, reps=3):
     seeded N(0,1) KKT vectors (device-generated: timing only; parity of the
     kernels at nx = 1023: tests/test_gpu_v6.py).  The sweep runs sweep_v6.cu
     (device-wide block substitution, fp64 DMMA).  Opt-in (--c4): the block
-    recursion's setup takes ~3.5 min at nx = 1023."""
+    recursion's setup takes ~40 s at nx = 1023."""
     import torch
     from paper_2305_04421_b200.solver import HeatKKT
     dev = torch.device("cuda", local)
