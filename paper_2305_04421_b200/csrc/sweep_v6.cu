@@ -13,17 +13,17 @@
 // clusters fit only 7 of 8 chain sets at once and wait on their triangle
 // imbalance.  v6 spreads every block step over the whole device instead:
 //   * off-chain terms first, for all J at once: c_J = Li_J b_J (d_J = Ui_J y_J)
-//     is a batched triangular product with no dependency (v6_off_kernel), the
-//     triangle streamed once per spatial solve for all local chains;
+//     is a batched triangular product with no dependency (v6_off2_kernel, or
+//     v6_off_kernel at KN = 256), the triangle streamed once per spatial
+//     solve for all local chains;
 //   * then the dependent chain y_J = c_J + G_J y_{J-1} (v6_chain_kernel): a
-//     co-resident grid of 64 row slices x chain groups; CTA (s, g) owns rows
+//     co-resident grid of KN/16 row slices x chain groups; CTA (s, g) owns rows
 //     16s..16s+15 for the 8 chains of group g, stages its slice of G_J (the
 //     next row's during this row's barrier) and y_{J-1} by bulk copies,
 //     multiplies them as fp64 DMMA (m8n8k4) tiles split over 8 warps along k,
 //     and publishes y_J with a release counter per chain group (one
 //     grid-wide barrier per block row).
-// Block vectors are chain-interleaved, W[g][J][k][8] (kN = 1024 rows, zero
-// padded), so the DMMA B operand of a k-step is 256 contiguous bytes.
+// Block vectors are chain-interleaved, W[g][J][k][8] (KN rows, zero padded), so the DMMA B operand of a k-step is 256 contiguous bytes.
 // Operators are packed in fragment order, [J][s][ks][mt][lane] =
 // M[16s + 8mt + lane/4][4ks + lane%4], so each warp's A operand is 32
 // consecutive doubles.  Chains, steps and the fused two-level residual follow
