@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kOffThr, 1) v6_off2_kernel(V6Params P) {
 // output warp publishes its own stores (release after __syncwarp), 4 counts
 // per CTA and row, so no CTA barrier sits between the stores and the count.
 template <int KN>
-constexpr size_t chain_smem() { return sizeof(double) * (16 * KN + KN * kG + 8 * 128) + 2 * sizeof(uint64_t); }
+constexpr size_t chain_smem() { return sizeof(double) * (16 * KN + KN * kG + 8 * 128) + 3 * sizeof(uint64_t); }
 
 template <int KN, bool kUpper>
 __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
   double* Bs = As + 16 * KN;       // [k KN][8]
   double* red = Bs + KN * kG;      // [warp 8][128]
   uint64_t* barA = reinterpret_cast<uint64_t*>(red + 8 * 128);
-  uint64_t* barB = barA + 1;
+  uint64_t* barB = barA + 1;  // [2]: the halves of y_{J-1} (warps 0-3 use k < KN/2, warps 4-7 the rest)
   const int s = blockIdx.x % kSl, g = P.g0 + blockIdx.x / kSl;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ny = P.ny;
@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
   if (threadIdx.x == 0) {
     mbar_init(barA, 1);
     mbar_init(barB, 1);
+    mbar_init(barB + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -427,7 +428,9 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
       if (tm) ts[1] = clock64();
       // y_{J-1} was written by other CTAs through the generic proxy; the copy reads it through the async proxy
       asm volatile("fence.proxy.async.global;\n" ::: "memory");
-      tma_load(Bs, P.W0 + widx<KN>(g, Jp, ny), sizeof(double) * KN * kG, barB);
+      const double* ysrc = P.W0 + widx<KN>(g, Jp, ny);
+      tma_load(Bs, ysrc, sizeof(double) * KN * kG / 2, barB);
+      tma_load(Bs + KN * kG / 2, ysrc + KN * kG / 2, sizeof(double) * KN * kG / 2, barB + 1);
     }
     // the previous row's readers of red are done (costs nothing: every warp
     // waits for thread 0's copy of y_{J-1} below anyway); one red buffer keeps
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
     __syncthreads();
     mbar_wait(barA, par);
     if (tm) ts[2] = clock64();
-    mbar_wait(barB, par);
+    mbar_wait(barB + (warp >> 2), par);  // this warp's half only: the other half may still be landing
     if (tm) ts[3] = clock64();
     double d[2][2][2] = {};
     const double* Aw = As + size_t(warp * kKW) * 64 + lane;
