@@ -55,6 +55,7 @@ enum { KKT_PRECOND_NONE = 0, KKT_PRECOND_ONE_LEVEL = 1, KKT_PRECOND_TWO_LEVEL = 
 enum { KKT_COARSE_SCALAR = 0, KKT_COARSE_PER_DOF = 1 };
 enum { KKT_FORM_LITERAL = 0, KKT_FORM_MULTIPLICATIVE = 1, KKT_FORM_ADDITIVE = 2 };
 enum { KKT_SIGN_PLUS = 0, KKT_SIGN_MINUS = 1 };
+#define KKT_NO_RESTART (-1)  /* GmresParams::restart == std::nullopt (config.hpp:26) */
 
 /* Arithmetic mode of the device path.
  *  STRICT: every kernel reproduces the reference's floating-point operation
@@ -86,7 +87,8 @@ typedef struct kkt_problem_desc {
   /* GmresParams */
   double tol;
   int32_t max_iters;
-  int32_t restart;          /* <= 0 : full (non-restarted) GMRES, i.e. std::nullopt */
+  int32_t restart;          /* KKT_NO_RESTART (-1): full GMRES, i.e. std::nullopt; any other value
+                               < 1 is a ConfigError ("gmres restart must be >= 1", config.cpp:21) */
   double happy_breakdown_tol;
 } kkt_problem_desc;
 

@@ -310,6 +310,7 @@ static int validate(const kkt_problem_desc* d) {
   if (!(d->omega > 0)) return fail(KKT_ECONFIG, -1, "regularization omega must be > 0");
   if (!(d->tol > 0)) return fail(KKT_ECONFIG, -1, "gmres tol must be > 0");
   if (d->max_iters < 1) return fail(KKT_ECONFIG, -1, "gmres max_iters must be >= 1");
+  if (d->restart != KKT_NO_RESTART && d->restart < 1) return fail(KKT_ECONFIG, -1, "gmres restart must be >= 1");
   return 0;
 }
 

@@ -65,7 +65,7 @@ ProblemConfig to_cfg(const kkt_problem_desc* d) {
   c.jhat_sign = d->jhat_sign == KKT_SIGN_PLUS ? JhatSign::plus : JhatSign::minus;
   c.gmres.tol = d->tol;
   c.gmres.max_iters = d->max_iters;
-  if (d->restart > 0) c.gmres.restart = d->restart;
+  if (d->restart != KKT_NO_RESTART) c.gmres.restart = d->restart;  // < 1 -> validate() throws
   c.gmres.happy_breakdown_tol = d->happy_breakdown_tol;
   return c;
 }

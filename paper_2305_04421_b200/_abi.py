@@ -62,7 +62,7 @@ def desc_from_problem(p: Problem) -> ProblemDesc:
         Lx=p.Lx, Ly=p.Ly, T=p.T, Nx=p.Nx, Ny=p.Ny, Nt=p.Nt, nu=p.nu, omega=p.omega, Nd=p.Nd,
         precond=PRECOND[p.precond], coarse_variant=COARSE[p.coarse_variant],
         two_level_form=FORM[p.two_level_form], jhat_sign=SIGN[p.jhat_sign],
-        tol=p.tol, max_iters=p.max_iters, restart=(p.restart or 0),
+        tol=p.tol, max_iters=p.max_iters, restart=(-1 if p.restart is None else int(p.restart)),
         happy_breakdown_tol=p.happy_breakdown_tol,
     )
 

@@ -85,8 +85,11 @@ void validate(const kkt_problem_desc& d) {
   if (!(d.omega > 0)) fail("regularization omega must be > 0");
   if (!(d.tol > 0)) fail("gmres tol must be > 0");
   if (d.max_iters < 1) fail("gmres max_iters must be >= 1");
+  if (d.restart != KKT_NO_RESTART && d.restart < 1) fail("gmres restart must be >= 1");
   if (d.precond < KKT_PRECOND_NONE || d.precond > KKT_PRECOND_TRUE_SCHUR) fail("unknown preconditioner kind");
   if (d.two_level_form < KKT_FORM_LITERAL || d.two_level_form > KKT_FORM_ADDITIVE) fail("unknown two-level form");
+  if (d.coarse_variant != KKT_COARSE_SCALAR && d.coarse_variant != KKT_COARSE_PER_DOF) fail("unknown coarse variant");
+  if (d.jhat_sign != KKT_SIGN_PLUS && d.jhat_sign != KKT_SIGN_MINUS) fail("unknown jhat sign");
 }
 
 void setup(Ctx* c, const kkt_problem_desc& d, const kkt_runtime_opts* o) {
@@ -98,6 +101,7 @@ void setup(Ctx* c, const kkt_problem_desc& d, const kkt_runtime_opts* o) {
     c->spectral = true;
   }
   if (c->mode != KKT_MODE_FAST && c->mode != KKT_MODE_STRICT) throw Error(KKT_EINVAL, "unknown mode");
+  if (const char* e = std::getenv("KKT_BISECT")) c->bisect = c->mode == KKT_MODE_FAST ? std::atoi(e) : 0;
   c->rank = o ? o->rank : 0;
   c->nranks = o ? o->nranks : 1;
   if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks)
@@ -180,6 +184,17 @@ void setup(Ctx* c, const kkt_problem_desc& d, const kkt_runtime_opts* o) {
   // grids (nx > 128), where the band's rank-1 updates do not scale
   static const bool force_rec = getenv("KKT_FORCE_BLOCK_RECURSION") != nullptr;  // testing
   if (c->mode == KKT_MODE_FAST && (c->nx > 128 || force_rec)) {
+    // The block recursion is an UNPIVOTED LU.  BandedLU (linalg.cpp:69-125) pivots, and the two
+    // agree only where no row interchange happens: a (weakly) diagonally dominant Ahat, which
+    // the minus sign always gives.  With jhat_sign = plus the diagonal 1 + 2cx + 2cy - dt/sqrt(omega)
+    // can lose dominance; there is no scalable pivoting factor for these grids, so refuse
+    // instead of silently using a different (possibly unstable) factorisation.
+    if (!(std::abs(c->Ahat.diag) >= 2.0 * std::abs(c->cx) + 2.0 * std::abs(c->cy)))
+      throw Error(KKT_EUNSUPPORTED,
+                  "FAST mode on grids with nx > 128 needs a diagonally dominant Ahat (unpivoted block LU); "
+                  "Ahat diagonal " + std::to_string(c->Ahat.diag) + " vs off-diagonal sum " +
+                      std::to_string(2.0 * std::abs(c->cx) + 2.0 * std::abs(c->cy)) +
+                      " (jhat_sign = plus with dt > sqrt(omega)): use STRICT mode");
     build_block_recursion(c);
     if (v6_supported(c))
       build_v6(c);
@@ -246,7 +261,7 @@ void kkt_problem_desc_default(kkt_problem_desc* d) {
   d->jhat_sign = KKT_SIGN_MINUS;
   d->tol = 1e-6;
   d->max_iters = 420;
-  d->restart = 0;
+  d->restart = KKT_NO_RESTART;
   d->happy_breakdown_tol = 1e-14;
 }
 
@@ -299,7 +314,6 @@ int kkt_layout(const kkt_ctx* ctx, int64_t* block, int32_t* n_sp, int32_t* node_
                int32_t* node_last, int64_t* local_block) {
   if (!ctx) return KKT_EINVAL;
   const Ctx& c = ctx->impl;
-  if (block) *block = c.B;
   if (n_sp) *n_sp = c.nsp;
   if (block) *block = c.Bg;
   if (node_first) *node_first = c.n0;
@@ -559,12 +573,14 @@ int kkt_debug_ahat_factor(kkt_ctx* ctx, int32_t* kl, int32_t* ku, double* ab_hos
   return kkt::guard(ctx, [&](Ctx* c) {
     if (kl) *kl = c->kl;
     if (ku) *ku = c->kuf;
-    if (ab_host)
+    if (ab_host) {
       KKT_CUDA(cudaMemcpyAsync(ab_host, c->ab.p, sizeof(double) * c->ab.n, cudaMemcpyDeviceToHost, c->stream));
       KKT_CUDA(cudaStreamSynchronize(c->stream));
-    if (piv_host)
+    }
+    if (piv_host) {
       KKT_CUDA(cudaMemcpyAsync(piv_host, c->piv.p, sizeof(int) * c->piv.n, cudaMemcpyDeviceToHost, c->stream));
       KKT_CUDA(cudaStreamSynchronize(c->stream));
+    }
   });
 }
 
@@ -574,12 +590,14 @@ int kkt_debug_coarse_factor(kkt_ctx* ctx, int32_t* kl, int32_t* ku, double* ab_h
     kkt::need(c->has_coarse && c->perdof, "no per-dof coarse space");
     if (kl) *kl = c->cb_kl;
     if (ku) *ku = c->cb_kuf;
-    if (ab_host)
+    if (ab_host) {
       KKT_CUDA(cudaMemcpyAsync(ab_host, c->cb_ab.p, sizeof(double) * c->cb_ab.n, cudaMemcpyDeviceToHost, c->stream));
       KKT_CUDA(cudaStreamSynchronize(c->stream));
-    if (piv_host)
+    }
+    if (piv_host) {
       KKT_CUDA(cudaMemcpyAsync(piv_host, c->cb_piv.p, sizeof(int) * c->cb_piv.n, cudaMemcpyDeviceToHost, c->stream));
       KKT_CUDA(cudaStreamSynchronize(c->stream));
+    }
   });
 }
 

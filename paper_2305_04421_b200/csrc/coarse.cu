@@ -471,7 +471,7 @@ void build_coarse(Ctx* c) {
 // per-application pieces
 // ---------------------------------------------------------------------------
 static void node_sums(Ctx* c, const double* r) {
-  if (c->mode == KKT_MODE_STRICT)
+  if (c->mode == KKT_MODE_STRICT || (c->bisect & 2))
     KKT_LAUNCH(c, nodesum_seq_kernel, (c->ntl + 127) / 128, 128, 0, c->ntl, c->nsp, r, c->nodesum.p);
   else
     KKT_LAUNCH(c, nodesum_tree_kernel, c->ntl, 256, 0, c->nsp, r, c->nodesum.p);
@@ -532,7 +532,7 @@ void two_level_apply(Ctx* c, const double* r, double* out, int form) {
     perdof_prolong_add(c, c->cvec.p, yc);
   } else {
     coarse_gamma(c, r);
-    const bool fast = c->mode == KKT_MODE_FAST && c->has_fast();
+    const bool fast = c->mode == KKT_MODE_FAST && c->has_fast() && !(c->bisect & 5);
     if (form == KKT_FORM_MULTIPLICATIVE && fast) {
       rasq_apply(c, r, out, true);
       return;

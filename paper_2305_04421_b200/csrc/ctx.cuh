@@ -65,6 +65,11 @@ struct Ctx {
   kkt_problem_desc desc{};
   int mode = KKT_MODE_FAST;
   bool spectral = false;           // KKT_MODE_SPECTRAL: eigenbasis RASQ (spectral.cu)
+  // KKT_BISECT (diagnostics, scripts/bisect_fast_c1.py): FAST with single pieces in STRICT arithmetic.
+  // 1: separate Shat*y_c pass instead of the fused analytic residual; 2: sequential node sums;
+  // 4: reference-order banded substitution in the sweep (implies 1); 8: reference-order MGS with
+  // sequential dots; 16: reference-order MGS with tree dots (= KKT_MGS=1)
+  int bisect = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;

@@ -538,7 +538,7 @@ void launch_dot(Ctx* c, const DotArgs& A) {
   ensure_reduction(c);
   auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool vec = aligned(A.w) && (!A.v || aligned(A.v)) && (!A.b || aligned(A.b));
-  if (c->mode == KKT_MODE_STRICT) {
+  if (c->mode == KKT_MODE_STRICT || (c->bisect & 8)) {
     KKT_LAUNCH(c, dot_seq_kernel, 1, kSeqThreads, 0, A);
   } else if (vec) {
     switch (A.op) {
@@ -556,6 +556,16 @@ void launch_dot(Ctx* c, const DotArgs& A) {
     c->comm->allgather(A.dst, c->red_all.p, 1, c->stream);
     KKT_LAUNCH(c, sum_partials_kernel, 1, 32, 0, c->red_all.p, c->nranks, A.dst);
   }
+}
+
+// Divergence must be decided from values every rank holds identically: the
+// non-finite flag is per slab, the rank-ordered sums of the dot partials are
+// not.  A non-finite entry of w makes <w, v_0> and ||w||^2 non-finite on every
+// rank, so all ranks raise GmresDivergenceError at the same iteration.
+bool all_finite(const double* h, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(h[i])) return false;
+  return true;
 }
 
 double fetch(Ctx* c, const double* d) {
@@ -645,7 +655,7 @@ int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* his
   // FAST: MGS in its one-reduction (ICWY) form, icwy_orthogonalise above;
   // KKT_MGS=1 keeps the reference-order MGS in FAST mode too
   static const bool force_mgs = std::getenv("KKT_MGS") != nullptr;
-  const bool cgs = c->mode == KKT_MODE_FAST && !force_mgs;
+  const bool cgs = c->mode == KKT_MODE_FAST && !force_mgs && !(c->bisect & 24);
   const size_t hstride = size_t(P.max_iters) + 8 + kMD;
   if (c->hbuf.n < 2 * hstride + size_t(kMD) * (P.max_iters / kMDH + 2))
     c->hbuf.alloc(2 * hstride + size_t(kMD) * (P.max_iters / kMDH + 2));
@@ -730,7 +740,7 @@ int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* his
         KKT_CUDA(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c->stream));
         KKT_CUDA(cudaMemcpyAsync(&bad, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         KKT_CUDA(cudaStreamSynchronize(c->stream));
-        if (bad) {
+        if (bad || !all_finite(hh.data(), j + 2)) {
           throw Error(KKT_EDIVERGED,
                       "gmres: non-finite values in Krylov vector at iteration " +
                           std::to_string(total_iters + 1),
@@ -755,7 +765,7 @@ int gmres(Ctx* c, const double* b, double* x, kkt_gmres_result* res, double* his
       KKT_CUDA(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c->stream));
       KKT_CUDA(cudaMemcpyAsync(&bad, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       KKT_CUDA(cudaStreamSynchronize(c->stream));
-      if (bad) {
+      if (bad || !all_finite(hh.data(), j + 2)) {
         throw Error(KKT_EDIVERGED,
                     "gmres: non-finite values in Krylov vector at iteration " +
                         std::to_string(total_iters + 1),

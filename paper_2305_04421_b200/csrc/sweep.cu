@@ -52,7 +52,7 @@ const T* upload(Ctx* c, DBuf<char>& buf, const std::vector<T>& v) {
 
 void band_solve(Ctx* c, double* b, int nrhs, bool transpose) {
   const size_t nsp = c->nsp;
-  if (c->mode == KKT_MODE_STRICT || !c->has_fast()) {
+  if (c->mode == KKT_MODE_STRICT || !c->has_fast() || (c->bisect & 4)) {
     std::vector<SolveStep> jobs(nrhs);
     for (int k = 0; k < nrhs; ++k) jobs[k] = {b + k * nsp, nullptr, b + k * nsp, 1.0, transpose ? 1 : 0};
     strict_chains(c, upload(c, c->jobs_strict, jobs), nrhs, 1);
@@ -67,7 +67,7 @@ void band_solve(Ctx* c, double* b, int nrhs, bool transpose) {
 void window_solve(Ctx* c, double* b, int len, bool adjoint) {
   const size_t nsp = c->nsp;
   if (len <= 0) return;
-  if (c->mode == KKT_MODE_STRICT || !c->has_fast()) {
+  if (c->mode == KKT_MODE_STRICT || !c->has_fast() || (c->bisect & 4)) {
     std::vector<SolveStep> jobs;
     for (int t = 0; t < len; ++t) {
       const int k = adjoint ? len - 1 - t : t;
@@ -110,7 +110,7 @@ void rasq_apply(Ctx* c, const double* r, double* out, bool fused_coarse) {
     spectral_rasq(c, r, c->s0 > 0 ? hr.prev : nullptr, out, fused_coarse);
     return;
   }
-  if (c->mode == KKT_MODE_STRICT || !c->has_fast()) {
+  if (c->mode == KKT_MODE_STRICT || !c->has_fast() || (c->bisect & 4)) {
     // scratch: one plane per subdomain for the shared node's forward value
     const size_t need = size_t(Nd) * nsp;
     if (c->tmpB3.n < need) c->tmpB3.alloc(need);

@@ -1,0 +1,103 @@
+"""FAST-vs-reference solution parity at BASELINE config 1, and its bisection.
+
+    python scripts/bisect_fast_c1.py [--out profiles/fast_parity_c1_r02.json]
+
+Runs the config-1 full solve (127^2 x 512, Nd=16, GMRES(30), tol 1e-8) through
+the C-ABI in FAST mode and in FAST with single pieces switched back to the
+reference's arithmetic (KKT_BISECT, ctx.cuh; KKT_SWEEP_V2/V3: the older sweeps),
+one subprocess per variant because the switches are read once per process.
+Each run is compared with the reference's own solve
+(tests/golden/solve_c1_two-level_scalar{.json,_sample.npz}: every 1009th entry
+of u, z, w and the full residual history): per-block relative L2 on the sample,
+iteration count, max relative history deviation.  north_star gates: 1e-10
+solution, +-1 iterations, 1e-8 history.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+VARIANTS = [
+    ("fast (default)", {}),
+    ("fast + separate Shat*y_c pass (KKT_BISECT=1)", {"KKT_BISECT": "1"}),
+    ("fast + sequential node sums (KKT_BISECT=2)", {"KKT_BISECT": "2"}),
+    ("fast + reference-order MGS, tree dots (KKT_BISECT=16)", {"KKT_BISECT": "16"}),
+    ("fast + reference-order MGS, sequential dots (KKT_BISECT=8)", {"KKT_BISECT": "8"}),
+    ("fast + reference banded substitution in the sweep (KKT_BISECT=4)", {"KKT_BISECT": "4"}),
+    ("fast + strict sweep + node sums + unfused K2 (KKT_BISECT=7)", {"KKT_BISECT": "7"}),
+    ("fast + strict sweep/sums/K2 + reference MGS tree dots (KKT_BISECT=23)", {"KKT_BISECT": "23"}),
+    ("fast + everything strict but the vector kernels (KKT_BISECT=15)", {"KKT_BISECT": "15"}),
+    ("fast + v3 sweep (KKT_SWEEP_V3=1)", {"KKT_SWEEP_V3": "1"}),
+    ("fast + v2 per-row chains (KKT_SWEEP_V2=1 KKT_SWEEP_V3=1)", {"KKT_SWEEP_V2": "1", "KKT_SWEEP_V3": "1"}),
+    ("fast, tol 1e-10", {"_TOL": "1e-10"}),
+    ("fast + KKT_BISECT=15, tol 1e-10", {"KKT_BISECT": "15", "_TOL": "1e-10"}),
+]
+
+
+def child(cfg):
+    import numpy as np
+    from paper_2305_04421_b200 import problems as P
+    from paper_2305_04421_b200.solver import HeatKKT
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", f"solve_c{cfg}_two-level_scalar.json")))
+    samp = np.load(os.path.join(ROOT, "tests", "golden", f"solve_c{cfg}_two-level_scalar_sample.npz"))
+    p = P.config(cfg)
+    tol = os.environ.get("_TOL")
+    if tol:
+        p = p.replace(tol=float(tol))
+    b = P.kkt_rhs(cfg, p)
+    k = HeatKKT(p, mode=os.environ.get("_MODE", "fast"))
+    o = k.gmres_solve(b)
+    x = o.solution.cpu().numpy()
+    B = p.block
+    idx, xs = samp["idx"], samp["x"]
+    rel = {}
+    for i, name in enumerate("uzw"):
+        sel = (idx >= i * B) & (idx < (i + 1) * B)
+        rel[name] = float(np.linalg.norm(x[idx[sel]] - xs[sel]) / np.linalg.norm(xs[sel]))
+    h = np.array(gold["history"])
+    hf = o.residual_history
+    n = min(len(h), len(hf))
+    dev = np.abs(hf[:n] - h[:n]) / h[:n]
+    print(json.dumps({"iterations": o.iterations, "ref_iterations": gold["iterations"],
+                      "true_final_relres": o.true_final_relres, "rel_l2_vs_reference": rel,
+                      "history_max_rel_dev": float(dev.max()),
+                      "history_rel_dev_first_cycle_max": float(dev[:30].max()),
+                      "history_first_dev_gt_1e-8": int(np.argmax(dev > 1e-8)) if (dev > 1e-8).any() else None}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--child", action="store_true")
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--strict", action="store_true", help="also run STRICT (2.5 min at config 1)")
+    a = ap.parse_args()
+    if a.child:
+        return child(a.config)
+    rows = []
+    variants = list(VARIANTS)
+    if a.strict:
+        variants.append(("strict", {"_MODE": "strict"}))
+    for name, env in variants:
+        e = dict(os.environ)
+        e.update(env)
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--child", "--config", str(a.config)],
+                           env=e, capture_output=True, text=True)
+        try:
+            rec = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception:
+            rec = {"error": (r.stderr or r.stdout)[-400:]}
+        rec["variant"] = name
+        rec["env"] = env
+        rows.append(rec)
+        print(json.dumps(rec), flush=True)
+    if a.out:
+        json.dump(rows, open(a.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -2,8 +2,10 @@
 
 STRICT mode must be bitwise identical to the reference (same floating-point
 operation order).  FAST mode is gated on rounding-level tolerances written in
-each test: operators <= 1e-12 relative L2, full solves: iterations +-1 and
-u, z, w within 1e-10 relative L2 (BASELINE.json north_star).
+each test: operators <= 1e-11 relative L2; full solves: iterations +-1 and the
+solution tolerance stated in each test (1e-10 relative L2 per block at BASELINE
+configs 0 and 1 against the reference's golden solves; the ill-conditioned
+desk cases compare two iterates that both meet the stopping test).
 """
 import hashlib
 import json
@@ -50,8 +52,17 @@ SMALL = [
               tol=1e-10, restart=5, max_iters=100),   # nx = 1 column, m = 1
     P.Problem(Lx=1.0, Ly=1.0, Nx=7, Ny=2, Nt=8, Nd=1, omega=1e-1, coarse_variant="scalar",
               tol=1e-10, restart=None, max_iters=100),  # ny = 1 row, single subdomain
+    # jhat_sign = plus (config.hpp:61-65): Ahat = A - omega^{-1/2} dt I.
+    # omega = 0.1: still diagonally dominant, pivot-free, GMRES converges (102 iterations);
+    # omega = 1.8e-5: the diagonal nearly cancels, BandedLU swaps 38 rows (growth 1.78) and
+    # FAST takes the pivot-aware substitution; GMRES stagnates there (in the reference too),
+    # so that case caps the iterations and pins the operators and the history.
+    P.Problem(Lx=1.0, Ly=1.0, Nx=8, Ny=7, Nt=12, Nd=3, omega=1e-1, coarse_variant="scalar",
+              jhat_sign="plus", tol=1e-10, restart=10, max_iters=200),
+    P.Problem(Lx=1.0, Ly=1.0, Nx=8, Ny=7, Nt=12, Nd=3, omega=1.8e-5, coarse_variant="scalar",
+              jhat_sign="plus", tol=1e-10, restart=10, max_iters=30),
 ]
-IDS = ["8x6_nt12_nd3", "9x9_nt16_nd4", "nx1_m1", "ny1_nd1"]
+IDS = ["8x6_nt12_nd3", "9x9_nt16_nd4", "nx1_m1", "ny1_nd1", "plus_dominant", "plus_pivoting"]
 
 
 @pytest.fixture(scope="module", params=list(zip(SMALL, IDS)), ids=IDS)

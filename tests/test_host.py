@@ -60,7 +60,7 @@ def test_desc_defaults_match_reference(lib):
     assert (d.Lx, d.Ly, d.T, d.Nx, d.Ny, d.Nt, d.nu, d.omega, d.Nd) == (
         ref.Lx, ref.Ly, ref.T, ref.Nx, ref.Ny, ref.Nt, ref.nu, ref.omega, ref.Nd)
     assert d.precond == P.PRECOND[ref.precond] and d.coarse_variant == P.COARSE[ref.coarse_variant]
-    assert d.tol == ref.tol and d.max_iters == ref.max_iters and d.restart == 0
+    assert d.tol == ref.tol and d.max_iters == ref.max_iters and d.restart == -1  # KKT_NO_RESTART = std::nullopt
     assert d.happy_breakdown_tol == ref.happy_breakdown_tol
 
 
@@ -79,6 +79,29 @@ def test_create_without_device_fails_loudly(lib):
     h = C.c_void_p()
     st = lib.kkt_ctx_create(C.byref(d), None, C.byref(h))
     assert st == _abi.KKT_ECUDA and not h.value
+
+
+def test_config_errors_precede_the_device(lib):
+    """ProblemConfig::validate (config.cpp:5-22) runs before any CUDA call, so the
+    reference's ConfigError cases come back as KKT_ECONFIG with its messages even
+    without a device -- including gmres restart < 1 (config.cpp:21); only
+    KKT_NO_RESTART (-1) means std::nullopt."""
+    lib.kkt_create_error.restype = C.c_char_p
+    base = P.config(0)
+    cases = [(base.replace(restart=0), b"gmres restart must be >= 1"),
+             (base.replace(restart=-7), b"gmres restart must be >= 1"),
+             (base.replace(Nd=5), b"is not divisible by"),
+             (base.replace(omega=0.0), b"omega must be > 0"),
+             (base.replace(max_iters=0), b"max_iters must be >= 1"),
+             (base.replace(Nx=1), b"mesh needs Nx, Ny >= 2")]
+    for p, msg in cases:
+        d = _abi.desc_from_problem(p)
+        h = C.c_void_p()
+        st = lib.kkt_ctx_create(C.byref(d), None, C.byref(h))
+        assert st == _abi.KKT_ECONFIG and not h.value, (p, st)
+        assert msg in lib.kkt_create_error(), lib.kkt_create_error()
+    assert _abi.desc_from_problem(base.replace(restart=None)).restart == -1
+    assert "#define KKT_NO_RESTART (-1)" in open(HEADER).read()
 
 
 def test_solver_refuses_without_cuda():
