@@ -1,37 +1,46 @@
 """Benchmark: space-time unknowns/s per preconditioned KKT solve (fp64).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 1] [--mode fast|strict|spectral] [--no-alt]
+                    [--config 3] [--nd 32] [--mode fast|strict|spectral] [--no-extras]
 
-A "step" is one full right-preconditioned GMRES solve (two-level RASQ,
-scalar coarse space) of BASELINE config 1 (127x127 interior, Nt=512, Nd=16,
-omega=1e-3, GMRES(30), rtol 1e-8) from b resident in HBM to x in HBM, through
-the C-ABI (kkt_gmres_solve).  value = N * 3*Nt*n_sp / (max-over-ranks device
-time per solve).  e2e repeats the solve through kkt_gmres_solve_host with b
-and x in pinned host memory (copies inside the timed region).
+Headline workload (BASELINE.json configs[3], the largest single-GPU config;
+SURVEY.md §8e names it as the 1 -> 8 GPU scaling config): 255x255 interior,
+Nt = 4096, Nd = 32 time subdomains, nu = 1, omega = 1e-2, two-level RASQ with
+the scalar coarse space (multiplicative form, minus sign), GMRES(20), rtol 1e-8,
+on config 3's own seeded inputs (u~ = sin(pi x) sin(pi y) cos(2 pi t) + 0.01 N(0,1),
+u0 = 0; problems.kkt_rhs).  A "step" is ONE FULL SOLVE (799 M unknowns) from b
+resident in HBM to x in HBM through the C-ABI (kkt_gmres_solve); value =
+3*Nt*n_sp / (max-over-ranks device time per solve).  e2e repeats one solve
+through kkt_gmres_solve_host with b and x in pinned host memory (H2D + D2H
+inside the timed region).
 
-N > 1 is weak scaling over time slabs (the paper's own
-weak-scaling axis): N GPUs solve config 1 extended in time, Nt = 512 N and
-Nd = 16 N on the same T = 1 (m = 32 steps per subdomain as at N = 1), rank g
-owning subdomains [16g, 16g+16) and their node slab — per-GPU work fixed.
-Halo planes, the coarse all-gather and the Krylov dot all-gathers go through
-NCCL (one communicator built by the library from a unique id that rank 0
-broadcasts).  value = 3*Nt*n_sp / (max over ranks of the solve time).  (The
-sweep's dependent chain, 65 lock-step time steps per P^-1 apply, does not
-shorten when one config-1 solve is split over more GPUs, so strong scaling of
-config 1 is not the meaningful axis.)
+N > 1 is STRONG scaling over time slabs of the same config-3 solve: rank g owns
+subdomains [g*Nd/N, (g+1)*Nd/N) and their node slab; halo planes, the coarse
+all-gather and the Krylov dot all-gathers go through NCCL (one communicator
+built by the library from a unique id that rank 0 broadcasts).  Launched
+without WORLD_SIZE, `--gpus N` re-executes itself under torchrun with N ranks
+(127.0.0.1 rendezvous); n_gpus in the JSON line is the number of ranks that ran.
+
+Extra keys at N = 1 (never the headline): `config1` (BASELINE config 1 full
+solve, GMRES(30), the round-1 headline) and `microbench_c2` (BASELINE config 2,
+10 P^-1 applications at 511^2 x 1024).
 
 --impl reference times the UNMODIFIED reference (oracle/_ref, compiled from
-/root/reference by oracle/Makefile) on the host CPU: each step is a bounded
-sample — GMRES iterations of the config-1 grid on a shortened time axis (Nt=64,
-Nd=2, m=32 as in config 1) — scaled to a full config-1 solve by the per-iteration
-cost's linearity in Nt and the reference's own iteration count.
+/root/reference by oracle/Makefile; it is single-threaded by construction) on
+the host CPU.  A full config-3 solve is out of its reach (one apply_K takes
+~38 min, the GMRES(20) basis 134 GB of host memory: SURVEY.md §8c), so each
+step times a BOUNDED sample -- apply_K, apply_shat and apply_rasq once each on
+config 3's grid with a 4-node time axis -- and `value` extrapolates it to the
+full solve by operation counts (SURVEY.md §8d allows this for C3; flagged
+`extrapolated`).  `ms_per_step` is the measured sample time, not the
+extrapolated solve time.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -49,6 +58,7 @@ METRIC = "space-time unknowns/sec per preconditioned KKT solve (fp64)"
 UNIT = "unknowns/s"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0
+DATA = "synthetic (seeded SplitMix64 + Box-Muller target, paper_2305_04421_b200/problems.py)"
 
 
 def hbm_peak():
@@ -59,12 +69,30 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
+def fp64_peak():
+    path = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    try:
+        return float(json.load(open(path))["dmma_tflops"]), "builder-measured (profiles/fp64_peak.json, scripts/fp64_peak.cu; not in MEASURED_PEAKS.json)"
+    except Exception:
+        return None, "unmeasured"
+
+
+def ncu_summary(key):
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get(key)
+    except Exception:
+        return None
+
+
 def workload_desc(cfg, p):
     return (f"config{cfg}: {p.nx_int}x{p.ny_int} interior, Nt={p.Nt}, Nd={p.Nd}, nu={p.nu}, "
             f"omega={p.omega}, two-level {p.coarse_variant} multiplicative (minus), "
-            f"GMRES({p.restart}) rtol {p.tol}")
+            f"GMRES({p.restart}) rtol {p.tol}; one step = one full solve")
 
 
+# ---------------------------------------------------------------------------
+# algorithmic byte / flop models, per GPU
+# ---------------------------------------------------------------------------
 def mgs_model(p, iters, ranks=1, mode="fast"):
     """Algorithmic bytes and launches of the Gram-Schmidt passes of one solve
     (SURVEY.md §8d, K7), per GPU (the vectors split over the G slabs).
@@ -102,12 +130,18 @@ def sweep_bytes(p, ranks=1):
     return planes + (2 * m + 1) * F
 
 
-def fp64_peak():
-    path = os.path.join(ROOT, "profiles", "fp64_peak.json")
-    try:
-        return float(json.load(open(path))["dmma_tflops"]), "measured (profiles/fp64_peak.json, scripts/fp64_peak.cu)"
-    except Exception:
-        return None, "unmeasured"
+def sweep_flops(p, ranks=1):
+    """Algorithmic fp64 FLOPs of one RASQ apply per GPU: the
+    banded-LU substitution of each of the 2Nt + Nd - 1 spatial solves,
+    4 * n_sp * nx."""
+    return (2 * p.Nt + p.Nd - 1) * 4.0 * p.n_sp * p.nx_int / ranks
+
+
+def sweep_block_row_steps(p):
+    """Dependent block-row steps of one RASQ apply: 2m+1 lock-step spatial
+    solves, each an L chain and a U chain over the ny block rows."""
+    m = p.Nt // p.Nd
+    return (2 * m + 1) * 2 * p.ny_int
 
 
 class ClockSampler:
@@ -127,7 +161,7 @@ class ClockSampler:
             self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "500"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -163,16 +197,49 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def dist_setup(args):
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
+# ---------------------------------------------------------------------------
+# launching: one process per GPU
+# ---------------------------------------------------------------------------
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` without a torchrun environment: start the N
+    ranks ourselves, as the driver's multi-GPU launch does."""
+    if not args.probe_ranks:
         import torch
-        import torch.distributed as dist
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} requested but {n} CUDA device(s) visible; "
+                                       "not falling back to fewer ranks"}))
+            sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def dist_env():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def dist_init(ws, local, backend="nccl"):
+    if ws <= 1:
+        return
+    import torch
+    import torch.distributed as dist
+    if backend == "nccl":
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # the driver reads nranks from the init lines
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    return ws, rank, local
+    else:
+        dist.init_process_group("gloo")
 
 
 def barrier(ws):
@@ -191,75 +258,128 @@ def max_over_ranks(x, ws):
     return float(t.item())
 
 
+def probe_ranks(ws, rank):
+    """--probe-ranks (tests/test_bench_launch.py, CPU): every started rank joins a
+    gloo group and rank 0 prints how many did."""
+    import torch
+    import torch.distributed as dist
+    if ws > 1:
+        dist_init(ws, 0, backend="gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        n = int(t.item())
+        dist.destroy_process_group()
+    else:
+        n = 1
+    if rank == 0:
+        print(json.dumps({"probe": True, "n_gpus": ws, "ranks_started": n, "pid": os.getpid()}))
+
+
 # ---------------------------------------------------------------------------
 # CPU reference (the reference arm and the cpu_baseline leg)
 # ---------------------------------------------------------------------------
-def reference_sample(cfg, iters_full, sample_iters=2, nt_sample=64, time_scale=1):
-    """Time `sample_iters` GMRES iterations of the reference on the config grid
-    with a shortened time axis (same m = Nt/Nd), and scale to a full solve
-    (of the config extended `time_scale`-fold in time, as the N-GPU arm)."""
-    from oracle.bindings import Ref
-    p = P.config(cfg)
-    if time_scale > 1:
-        p = p.replace(Nt=p.Nt * time_scale, Nd=p.Nd * time_scale)
-    m = p.Nt // p.Nd
-    nd_s = max(1, nt_sample // m)
-    ps = p.replace(Nt=nd_s * m, Nd=nd_s, max_iters=sample_iters, restart=p.restart)
-    b = P.kkt_rhs(cfg, ps)
-    t0 = time.perf_counter()
-    ref = Ref(ps)
-    t_setup = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    out = ref.gmres_solve(b)
-    t_solve = time.perf_counter() - t0
-    # gmres_solve does `it` (K + P^-1) iterations, one LS P^-1 and one true-residual K
-    per_iter = t_solve / (out["iterations"] + 1)
-    scale = p.Nt / ps.Nt
-    t_full = per_iter * scale * (iters_full + 1)
-    value = 3 * p.Nt * p.n_sp / t_full
-    sample = (f"reference (1 thread) on the config-{cfg} grid {p.nx_int}x{p.ny_int} with Nt={ps.Nt}, "
-              f"Nd={ps.Nd} (m={m} as in config {cfg}), {out['iterations']} GMRES iterations in "
-              f"{t_solve:.2f} s (+{t_setup:.2f} s setup); per-iteration cost scaled x{scale:g} in Nt and "
-              f"to {iters_full} iterations (+1 final P^-1/K) => {t_full:.1f} s per full solve")
-    return value, t_full, sample, t_solve + t_setup
+REF_ITER_RECORDS = {3: os.path.join(ROOT, "profiles", "solve_c3_nd32_r02.json")}
 
 
-def reference_iterations(cfg):
+def recorded_iterations(cfg, nd):
+    """Iterations of the full solve, for the extrapolation of the reference arm:
+    the reference's own golden record where it could run the solve (configs 0,
+    1), else the committed device run on the same inputs (FAST takes the
+    reference's count +-1 wherever both ran)."""
     path = os.path.join(ROOT, "tests", "golden", f"solve_c{cfg}_two-level_scalar.json")
     if os.path.exists(path):
         return int(json.load(open(path))["iterations"]), "reference golden record"
+    path = REF_ITER_RECORDS.get(cfg)
+    if path and os.path.exists(path):
+        rec = json.load(open(path))
+        if rec.get("Nd") == nd:
+            return int(rec["iterations"]), f"device run on the same inputs ({os.path.relpath(path, ROOT)})"
     return None, None
+
+
+class ReferenceSample:
+    """The reference's per-operation costs on the config's grid with a short time
+    axis (Nt_s nodes, Nd_s subdomains), and their extrapolation to a full solve.
+
+    One GMRES iteration applies P^-1 and K once; a solve with `it` iterations in
+    `cyc` restart cycles applies each it + cyc times (gmres.cpp:79-80, :134-141,
+    :147-153).  P^-1 (two-level multiplicative, kkt.cpp:71-81, schur.cpp:415-444)
+    is apply_shat + apply_rasq + O(B) work.  apply_K and apply_shat cost 2 Nt
+    band_matvecs each (linear in Nt); apply_rasq does 2 (Nt + 2 (Nd - 1)) banded
+    solves (schur.cpp:103-130).  The MGS dots/axpys and the coarse solve are left
+    out, which favours the reference."""
+
+    def __init__(self, cfg, p, nt_s=4, nd_s=2):
+        from oracle.bindings import Ref
+        self.cfg, self.p = cfg, p
+        self.ps = p.replace(Nt=nt_s, Nd=nd_s, T=p.T * nt_s / p.Nt)  # the config's dt
+        t0 = time.perf_counter()
+        self.ref = Ref(self.ps)
+        self.setup_s = time.perf_counter() - t0
+        self.v = P.random_kkt(self.ps, 0)
+
+    def step(self):
+        B = self.ps.block
+        t = {}
+        t0 = time.perf_counter()
+        self.ref.apply_K(self.v)
+        t["apply_K"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        self.ref.apply_shat(self.v[2 * B:])
+        t["apply_shat"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        self.ref.apply_rasq(self.v[2 * B:])
+        t["apply_rasq"] = time.perf_counter() - t0
+        return t
+
+    def extrapolate(self, t, iters):
+        p, ps = self.p, self.ps
+        restart = p.restart or p.max_iters
+        cyc = -(-iters // restart)
+        lin = p.Nt / ps.Nt
+        rasq = (p.Nt + 2 * (p.Nd - 1)) / (ps.Nt + 2 * (ps.Nd - 1))
+        per_iter = (t["apply_K"] + t["apply_shat"]) * lin + t["apply_rasq"] * rasq
+        return per_iter * (iters + cyc)
+
+    def describe(self, t, iters, t_full):
+        ps = self.ps
+        return (f"reference (1 thread) on config {self.cfg}'s grid {ps.nx_int}x{ps.ny_int} with Nt={ps.Nt}, Nd={ps.Nd} "
+                f"(the config's dt): apply_K {t['apply_K']:.2f} s, apply_shat {t['apply_shat']:.2f} s, "
+                f"apply_rasq {t['apply_rasq']:.2f} s per step (setup {self.setup_s:.1f} s, excluded like the device's); "
+                f"EXTRAPOLATED by operation counts to Nt={self.p.Nt}, Nd={self.p.Nd} and {iters} iterations "
+                f"(+ one P^-1/K per restart cycle): {t_full:.0f} s per full solve")
 
 
 def run_reference_arm(args, ws, rank):
     if rank != 0:
-        return
+        return  # rank 0 alone runs the CPU reference; the others exit 0 without work
     from oracle import bindings
     if not bindings.available("ref"):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libkktdd_ref.so not built"}))
         return
-    p = P.config(args.config)
-    if ws > 1:  # the same (weak-scaled) workload as the N-GPU arm
-        p = p.replace(Nt=p.Nt * ws, Nd=p.Nd * ws)
-    iters, src = reference_iterations(args.config)
+    p = P.config(args.config, Nd=args.nd)
+    iters, src = recorded_iterations(args.config, p.Nd)
     if iters is None:
-        iters, src = 60, "assumed (no golden record)"
-    vals, times = [], []
+        iters, src = 120, "assumed (no record)"
+    rs = ReferenceSample(args.config, p)
+    secs, fulls = [], []
+    t = None
     for i in range(args.warmup + args.steps):
-        v, t_full, sample, wall = reference_sample(args.config, iters, time_scale=ws)
+        t = rs.step()
         if i >= args.warmup:
-            vals.append(v)
-            times.append(t_full)
-    value = statistics.median(vals)
+            secs.append(sum(t.values()))
+            fulls.append(rs.extrapolate(t, iters))
+    t_full = statistics.median(fulls)
+    value = 3 * p.block / t_full
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded SplitMix64 + Box-Muller, paper_2305_04421_b200/problems.py)",
-        "config": {"workload": workload_desc(args.config, p), "iterations": iters,
-                   "iterations_source": src},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws if ws > 1 else args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(secs),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "extrapolated": True, "ms_per_full_solve_extrapolated": 1000 * t_full,
+        "config": {"workload": workload_desc(args.config, p), "iterations": iters, "iterations_source": src,
+                   "note": "ms_per_step is the measured bounded sample; value = unknowns / extrapolated full-solve time"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
-                         "sample": sample},
+                         "sample": rs.describe(t, iters, t_full), "host_nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -268,18 +388,110 @@ def run_reference_arm(args, ws, rank):
 # ---------------------------------------------------------------------------
 # the device arm
 # ---------------------------------------------------------------------------
-def rank_rhs(cfg, p, k):
+def rank_rhs(cfg, p, node_first, node_last):
     """This rank's slab of b = [f_u; f_z; f] (kkt.cpp:21-48), generated only for
     the local nodes (the generator is counter-based, so slabs agree with the
     full field)."""
-    nf, nl = k.node_first, k.node_last
-    tgt, u0 = P.target_and_u0(cfg, p, n_lo=nf, n_hi=nl)
-    L = (nl - nf + 1) * p.n_sp
+    tgt, u0 = P.target_and_u0(cfg, p, n_lo=node_first, n_hi=node_last)
+    L = (node_last - node_first + 1) * p.n_sp
     b = np.zeros(3 * L)
     b[:L] = (p.mass_scale * tgt).reshape(-1)
-    if nf == 1:
+    if node_first == 1:
         b[2 * L: 2 * L + p.n_sp] = u0
     return b
+
+
+def timed_solves(k, b, x, steps, ws):
+    """`steps` solves bracketed by a barrier + synchronize, CUDA events on the
+    current stream (HeatKKT fences its own stream against it on both sides)."""
+    import torch
+    iters = []
+    barrier(ws)
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    out = None
+    for _ in range(steps):
+        out = k.gmres_solve(b, x)
+        iters.append(out.iterations)
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier(ws)
+    return max_over_ranks(ev0.elapsed_time(ev1), ws), iters, out
+
+
+def rooflines(p, ws, mode, iters, steps, ms_total, phase_ms, phase_cnt, v6):
+    """roofline (dominant family), roofline_secondary, roofline_stencil."""
+    peak, peak_src = hbm_peak()
+    ms_step = ms_total / steps
+    mgs_bytes, mgs_launches = mgs_model(p, iters, ws, mode)
+    mgs_ms = phase_ms[2] / steps
+    achieved = mgs_bytes / (mgs_ms / 1000.0) / 1e9 if mgs_ms > 0 else None
+    krylov = {
+        "kernel": ("Krylov Gram-Schmidt passes: one-reduction MGS (cgs_dots_kernel, icwy_solve_kernel, cgs_update_kernel; krylov.cu)"
+                   if mode != "strict" else "Krylov MGS passes (dot_seq_kernel, reference order; krylov.cu)"),
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak if achieved else None,
+        "traffic": ncu_summary("cgs_dram_bytes_per_launch"), "peak_source": peak_src,
+        "algorithmic_bytes_per_launch": mgs_bytes / max(1, mgs_launches),
+        "avg_launch_ms": mgs_ms / max(1, mgs_launches), "launches": mgs_launches * steps,
+        "share_of_step": mgs_ms / max(1e-9, ms_step), "family": "krylov",
+    }
+    sw_ms = phase_ms[3] / max(1, phase_cnt[3])
+    if mode == "spectral":
+        tpk, tpk_src = fp64_peak()
+        sp_tf = spectral_flops(p, ws) / (sw_ms / 1000.0) / 1e12 if sw_ms > 0 else None
+        sweep = {
+            "kernel": "SPECTRAL RASQ: 4 sine-transform GEMM passes (gemm_f64_kernel, mma.sync m8n8k4 f64) + per-mode recurrences (spectral.cu)",
+            "bound": "tensor", "achieved": sp_tf, "peak": tpk, "unit": "TFLOP/s",
+            "frac": (sp_tf / tpk) if (sp_tf and tpk) else None, "peak_source": tpk_src,
+            "flops_per_apply": spectral_flops(p, ws), "avg_apply_ms": sw_ms,
+            "applies": phase_cnt[3], "share_of_step": phase_ms[3] / max(1e-9, ms_total), "family": "sweep"}
+    else:
+        sb = sweep_bytes(p, ws)
+        sw_gbs = sb / (sw_ms / 1000.0) / 1e9 if sw_ms > 0 else None
+        tpk, tpk_src = fp64_peak()
+        fl = sweep_flops(p, ws)
+        tf = fl / (sw_ms / 1000.0) / 1e12 if sw_ms > 0 else None
+        rows = sweep_block_row_steps(p)
+        if mode == "strict":
+            kname = "RASQ sweep: reference-order banded substitution (sweep_strict.cu)"
+        elif v6:
+            kname = ("RASQ sweep v6 (sweep_v6.cu): v6_chain_kernel (device-wide dependent block-row chain, fp64 DMMA, "
+                     "release-counter handoff) + v6_off_kernel (batched triangular products) + v6_form_b_kernel, "
+                     "all local subdomains in lock step")
+        else:
+            kname = ("RASQ sweep v4 (sweep_v4.cu): group-parallel block-LU substitution chains, 8-CTA clusters, "
+                     "fp64 DMMA, one CUDA-graph replay per P^-1")
+        sweep = {
+            "kernel": kname, "bound": "hbm", "achieved": sw_gbs, "peak": peak, "unit": "GB/s",
+            "frac": (sw_gbs / peak) if sw_gbs else None,
+            "traffic": ncu_summary("sweep_v6_c3_dram_bytes_per_apply" if v6 else "sweep_dram_bytes_per_apply"),
+            "peak_source": peak_src, "algorithmic_bytes_per_launch": sb, "avg_launch_ms": sw_ms,
+            "launches": phase_cnt[3], "launch_unit": "one RASQ apply (all its sweep kernels)",
+            "share_of_step": phase_ms[3] / max(1e-9, ms_total), "family": "sweep",
+            "fp64": {"flops_per_apply": fl, "achieved_tflops": tf, "peak_tflops": tpk,
+                     "frac": (tf / tpk) if (tf and tpk) else None, "peak_source": tpk_src,
+                     "flops_source": "SURVEY §8(a20): (2Nt + Nd - 1) * 4 * n_sp * nx (banded substitution)"},
+            "chain": {"dependent_block_row_steps_per_apply": rows,
+                      "us_per_block_row_step": 1000.0 * sw_ms / rows if sw_ms > 0 else None,
+                      "handoff_floor_us": ncu_summary("v6_row_handoff_floor_us"),
+                      "note": "the sweep is bound by this dependent chain: (2m+1) lock-step spatial solves x 2 "
+                              "directions x ny block rows, each waiting for the previous row of its chain"},
+        }
+    k_ms = phase_ms[0] / max(1, phase_cnt[0])
+    k_bytes = 6 * p.block * 8 // ws
+    stencil = {
+        "kernel": "K1 apply_K_kernel (5-point space-time stencil, stencil.cu)", "bound": "hbm",
+        "achieved": k_bytes / (k_ms / 1000.0) / 1e9 if k_ms > 0 else None, "peak": peak, "unit": "GB/s",
+        "frac": (k_bytes / (k_ms / 1000.0) / 1e9 / peak) if k_ms > 0 else None, "peak_source": peak_src,
+        "traffic": ncu_summary("apply_K_dram_bytes_per_launch"),
+        "algorithmic_bytes_per_launch": k_bytes, "avg_launch_ms": k_ms, "launches": phase_cnt[0],
+        "share_of_step": phase_ms[0] / max(1e-9, ms_total)}
+    fam = sorted([krylov, sweep], key=lambda d: -d["share_of_step"])
+    return fam[0], fam[1], stencil
+
 
 def run_ours(args, ws, rank, local):
     import torch
@@ -287,9 +499,14 @@ def run_ours(args, ws, rank, local):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    p = P.config(args.config)
-    if ws > 1:  # weak scaling over time slabs: the same per-GPU slab, Nt and Nd x ws
+    cfg = args.config
+    p = P.config(cfg, Nd=args.nd)
+    scaling = "strong"
+    if ws > 1 and args.weak:  # weak scaling over time slabs: the same per-GPU slab, Nt and Nd x ws
         p = p.replace(Nt=p.Nt * ws, Nd=p.Nd * ws)
+        scaling = "weak"
+    if p.Nd % ws:
+        raise SystemExit(f"time-slab sharding needs the rank count to divide Nd (Nd={p.Nd}, ranks={ws})")
     unknowns = 3 * p.Nt * p.n_sp
     nccl_id = None
     if ws > 1:
@@ -298,51 +515,49 @@ def run_ours(args, ws, rank, local):
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+    t0 = time.perf_counter()
     k = HeatKKT(p, mode=args.mode, device=local, rank=rank, nranks=ws, nccl_id=nccl_id)
-    b_host = rank_rhs(args.config, p, k)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    b_host = rank_rhs(cfg, p, k.node_first, k.node_last)
     n = b_host.size
     b = torch.from_numpy(b_host).to(dev)
     x = torch.empty_like(b)
 
     for _ in range(args.warmup):
-        out = k.gmres_solve(b, x)
+        k.gmres_solve(b, x)
     torch.cuda.synchronize()
 
-    # ---- timed region: K solves, device time with CUDA events on the launch stream
+    # ---- timed region: K solves, device time with CUDA events, max over ranks
     k.set_phase_timing(True)
     l0 = k.launch_count()
-    iters = []
-    barrier(ws)
-    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        for _ in range(args.steps):
-            out = k.gmres_solve(b, x)
-            iters.append(out.iterations)
-        ev1.record()
-        torch.cuda.synchronize()
-    barrier(ws)
+        ms_total, iters, out = timed_solves(k, b, x, args.steps, ws)
     launches = k.launch_count() - l0
-    ms_total = ev0.elapsed_time(ev1)
-    ms_total = max_over_ranks(ms_total, ws)
     ms_step = ms_total / args.steps
     phase_ms, phase_cnt = k.phase_times()
     k.set_phase_timing(False)
     value = unknowns / (ms_step / 1000.0)
+    relres = out.true_final_relres
+    converged = out.converged
+    mem_gb = (torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]) / 1e9
 
-    # ---- e2e through the host-buffer entry point (pinned memory)
+    # ---- e2e through the host-buffer entry point (pinned memory).  The device
+    # copies of b and x are released first: at config 3 one GPU holds 160 GB of
+    # Krylov basis and work vectors, and kkt_gmres_solve_host stages its own.
+    del b, x, out
+    torch.cuda.empty_cache()
     bh = torch.from_numpy(b_host).pin_memory()
     xh = torch.empty(n, dtype=torch.float64).pin_memory()
-    k.gmres_solve_host(bh.numpy(), xh.numpy())  # warm
+    e2e_steps = 1 if ms_step > 5000 else max(1, min(args.steps, 3))
+    if ms_step <= 5000:
+        k.gmres_solve_host(bh.numpy(), xh.numpy())  # warm (the big configs are warm from the timed region)
     barrier(ws)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
     e0.record()
-    e2e_steps = max(1, min(args.steps, 3))
     for _ in range(e2e_steps):
         k.gmres_solve_host(bh.numpy(), xh.numpy())
     e1.record()
@@ -350,146 +565,66 @@ def run_ours(args, ws, rank, local):
     wall_e2e = (time.perf_counter() - w0) / e2e_steps
     ms_e2e = max_over_ranks(e0.elapsed_time(e1) / e2e_steps, ws)
     e2e_value = unknowns / (ms_e2e / 1000.0)
+    del bh, xh
 
-    # ---- rooflines.  Phase slot 3 brackets the RASQ sweep launches (one
-    # CUDA-graph replay of the cluster LU chains per P^-1, sweep_v4.cu;
-    # the transform GEMMs + mode recurrences in SPECTRAL mode), slot 2 the
-    # Krylov Gram-Schmidt passes (krylov.cu).  `roofline` is the family with the
-    # larger share of the step.
-    peak, peak_src = hbm_peak()
-    mgs_bytes, mgs_launches = mgs_model(p, iters[-1], ws, args.mode)
-    mgs_ms = phase_ms[2] / args.steps
-    achieved = mgs_bytes / (mgs_ms / 1000.0) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("mgs_axpy_dot_dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    krylov = {
-        "kernel": ("Krylov Gram-Schmidt passes: one-reduction MGS (cgs_dots_kernel, icwy_solve_kernel, cgs_update_kernel; krylov.cu)"
-                   if args.mode != "strict" else "Krylov MGS passes (dot_seq_kernel, reference order; krylov.cu)"),
-        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": traffic, "peak_source": peak_src,
-        "algorithmic_bytes_per_launch": mgs_bytes / mgs_launches,
-        "avg_launch_ms": mgs_ms / mgs_launches, "launches": mgs_launches * args.steps,
-        "share_of_step": mgs_ms / max(1e-9, ms_step),
-    }
-    sw_ms = phase_ms[3] / max(1, phase_cnt[3])
-    if args.mode == "spectral":
-        tpk, tpk_src = fp64_peak()
-        sp_tf = spectral_flops(p, ws) / (sw_ms / 1000.0) / 1e12 if sw_ms > 0 else None
-        sweep = {
-            "kernel": "SPECTRAL RASQ: 4 sine-transform GEMM passes (gemm_f64_kernel, mma.sync m8n8k4 f64) + per-mode recurrences (spectral.cu)",
-            "bound": "tensor", "achieved": sp_tf, "peak": tpk, "unit": "TFLOP/s",
-            "frac": (sp_tf / tpk) if (sp_tf and tpk) else None, "peak_source": tpk_src,
-            "flops_per_apply": spectral_flops(p, ws), "avg_apply_ms": sw_ms,
-            "applies": phase_cnt[3], "share_of_step": phase_ms[3] / max(1e-9, ms_total)}
-    else:
-        sb = sweep_bytes(p, ws)
-        sw_gbs = sb / (sw_ms / 1000.0) / 1e9 if sw_ms > 0 else None
-        sweep = {
-            "kernel": ("RASQ sweep: group-parallel block-LU substitution chains, all local subdomains in lock step "
-                       "(sweep_v4.cu: 8-CTA clusters, fp64 DMMA, one CUDA-graph replay per P^-1)" if args.mode == "fast" else
-                       "RASQ sweep: reference-order banded substitution (sweep_strict.cu)"),
-            "bound": "hbm", "achieved": sw_gbs, "peak": peak, "unit": "GB/s",
-            "frac": (sw_gbs / peak) if sw_gbs else None, "traffic": None, "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": sb, "avg_launch_ms": sw_ms, "launches": phase_cnt[3],
-            "launch_unit": "one RASQ apply (one graph replay)",
-            "share_of_step": phase_ms[3] / max(1e-9, ms_total),
-            "note": "dependency-chain bound: 2m+1 lock-step spatial solves per apply, each a chain of block-row steps",
-        }
-        if os.path.exists(prof):
-            try:
-                sweep["traffic"] = json.load(open(prof)).get("sweep_dram_bytes_per_apply")
-            except Exception:
-                pass
-    # K1 (apply_K_kernel, stencil.cu): 6 block-sized vectors per apply (u, z, w
-    # read, three blocks written); the per-cycle restart residual
-    # b - Kx moves 9 and is counted as 6 (conservative)
-    k_ms = phase_ms[0] / max(1, phase_cnt[0])
-    k_bytes = 6 * p.block * 8 // ws
-    stencil = {
-        "kernel": "K1 apply_K_kernel (5-point space-time stencil, stencil.cu)", "bound": "hbm",
-        "achieved": k_bytes / (k_ms / 1000.0) / 1e9 if k_ms > 0 else None, "peak": peak, "unit": "GB/s",
-        "frac": (k_bytes / (k_ms / 1000.0) / 1e9 / peak) if k_ms > 0 else None, "peak_source": peak_src,
-        "algorithmic_bytes_per_launch": k_bytes, "avg_launch_ms": k_ms, "launches": phase_cnt[0],
-        "share_of_step": phase_ms[0] / max(1e-9, ms_total)}
-    fam = sorted([(krylov["share_of_step"], "krylov", krylov), (sweep["share_of_step"], "sweep", sweep)],
-                 key=lambda t: -t[0])
-    roofline, roofline_other = fam[0][2], fam[1][2]
-    roofline["family"], roofline_other["family"] = fam[0][1], fam[1][1]
-
-    # ---- the opt-in SPECTRAL variant (not the reference's spatial-solve method),
-    # reported beside the headline, never as it
-    alt = None
-    if args.mode == "fast" and not args.no_alt:
-        ks = HeatKKT(p, mode="spectral", device=local, rank=rank, nranks=ws, nccl_id=nccl_id)
-        xs = torch.empty_like(b)
-        for _ in range(2):
-            o2 = ks.gmres_solve(b, xs)
-        barrier(ws)
-        torch.cuda.synchronize()
-        a0 = torch.cuda.Event(enable_timing=True)
-        a1 = torch.cuda.Event(enable_timing=True)
-        a0.record()
-        for _ in range(args.steps):
-            o2 = ks.gmres_solve(b, xs)
-        a1.record()
-        torch.cuda.synchronize()
-        ms_alt = max_over_ranks(a0.elapsed_time(a1) / args.steps, ws)
-        alt = {"mode": "spectral", "value": unknowns / (ms_alt / 1000.0), "ms_per_step": ms_alt,
-               "iterations": o2.iterations, "true_final_relres": o2.true_final_relres,
-               "note": "RASQ spatial solves in Ahat's sine eigenbasis (KKT_MODE_SPECTRAL): same operator to "
-                       "rounding but not the reference's banded-LU method, so not the headline"}
-        del ks
-
+    v6 = args.mode == "fast" and p.nx_int > 128
+    roofline, roofline_other, stencil = rooflines(p, ws, args.mode, iters[-1], args.steps, ms_total,
+                                                  phase_ms, phase_cnt, v6)
+    del k
+    torch.cuda.empty_cache()
     if rank != 0:
         return
+    vec_mb = 3 * p.block * 8 / ws / 1e6
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded SplitMix64 + Box-Muller target, paper_2305_04421_b200/problems.py)",
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": DATA,
         "config": {
-            "workload": workload_desc(args.config, p), "mode": args.mode,
-            "iterations": iters[-1], "iterations_all": sorted(set(iters)),
-            "true_final_relres": out.true_final_relres,
-            "parallelism": (f"time slabs x{ws} (Nd/{ws} subdomains per GPU, NCCL halos + all-gathers)"
+            "workload": workload_desc(cfg, p), "mode": args.mode,
+            "iterations": iters[-1], "iterations_all": sorted(set(iters)), "converged": bool(converged),
+            "true_final_relres": relres,
+            "parallelism": (f"time slabs x{ws} ({p.Nd // ws} of {p.Nd} subdomains per GPU, NCCL halos + all-gathers)"
                             if ws > 1 else "1 GPU"),
-            "l2": "KKT vectors are 198 MB each (> 126 MB L2); no flush between solves",
+            "l2": f"KKT vectors are {vec_mb:.0f} MB each per GPU (> 126 MB L2); no flush between solves",
+            "setup_s": setup_s, "device_mem_GB": mem_gb,
             "phase_ms_per_step": {"K": phase_ms[0] / args.steps, "P_inv": phase_ms[1] / args.steps,
                                   "krylov_vectors": phase_ms[2] / args.steps,
-                                  "sweep_kernel": phase_ms[3] / args.steps},
+                                  "sweep_kernels": phase_ms[3] / args.steps},
         },
         "roofline": roofline,
         "roofline_secondary": roofline_other,
         "roofline_stencil": stencil,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
-                "d2h_bytes_per_step": 8 * n, "ms_per_step": ms_e2e, "wall_ms_per_step": 1000 * wall_e2e},
+                "d2h_bytes_per_step": 8 * n, "ms_per_step": ms_e2e, "wall_ms_per_step": 1000 * wall_e2e,
+                "steps": e2e_steps},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if alt is not None:
-        line["alt_spectral"] = alt
-    if ws == 1 and not args.no_c2 and args.mode == "fast" and args.config == 1:
+    if ws == 1 and not args.no_extras and args.mode == "fast":
+        if cfg != 1:
+            try:
+                line["config1"] = config1_extra(local)
+            except Exception as e:  # reported beside the headline, never required
+                line["config1"] = {"error": str(e)}
         try:
             line["microbench_c2"] = c2_microbench(local)
-        except Exception as e:  # reported beside the headline, never required
+        except Exception as e:
             line["microbench_c2"] = {"error": str(e)}
-    if ws == 1 and args.c4 and args.mode == "fast" and args.config == 1:
-        try:
-            line["microbench_c4_slab"] = c4_microbench(local)
-        except Exception as e:  # reported beside the headline, never required
-            line["microbench_c4_slab"] = {"error": str(e)}
+        if args.c4:
+            try:
+                line["microbench_c4_slab"] = c4_microbench(local)
+            except Exception as e:
+                line["microbench_c4_slab"] = {"error": str(e)}
     if not args.no_cpu_baseline and ws == 1:
         try:
             from oracle import bindings
             if bindings.available("ref"):
-                v, t_full, sample, wall = reference_sample(args.config, iters[-1])
-                line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "reference",
-                                        "sample": sample, "host_nproc": os.cpu_count()}
+                rs = ReferenceSample(cfg, p)
+                t = rs.step()
+                t_full = rs.extrapolate(t, iters[-1])
+                line["cpu_baseline"] = {"value": 3 * p.block / t_full, "unit": UNIT, "cores": 1, "kind": "reference",
+                                        "sample": rs.describe(t, iters[-1], t_full), "extrapolated": True,
+                                        "host_nproc": os.cpu_count()}
             else:
                 line["cpu_baseline"] = None
         except Exception as e:  # the baseline is reported, never required
@@ -497,22 +632,40 @@ def run_ours(args, ws, rank, local):
     print(json.dumps(line))
 
 
-def c2_microbench(local, reps=10):
-    """BASELINE config 2, the preconditioner-apply microbench: 10 applications
-    of P^-1 at 511^2 x 1024 steps, 64 subdomains, on seeded N(0,1) KKT vectors
-    (device-generated here: timing only; parity is tests/test_gpu_large.py and
-    tests/test_gpu_v5.py, tests/test_gpu_v6.py).  The sweep runs sweep_v6.cu
-    (device-wide fp64 DMMA block substitution), so its roofline is the fp64
-    tensor peak."""
+def config1_extra(local, steps=3):
+    """BASELINE config 1 (127^2 x 512, Nd = 16, GMRES(30)): the round-1 headline,
+    kept as an extra key.  Sweep v4 (sweep_v4.cu)."""
+    import torch
+    from paper_2305_04421_b200.solver import HeatKKT
+    p = P.config(1)
+    k = HeatKKT(p, mode="fast", device=local)
+    b = torch.from_numpy(P.kkt_rhs(1, p)).cuda()
+    x = torch.empty_like(b)
+    for _ in range(3):
+        k.gmres_solve(b, x)
+    k.set_phase_timing(True)
+    ms_total, iters, out = timed_solves(k, b, x, steps, 1)
+    phase_ms, phase_cnt = k.phase_times()
+    k.set_phase_timing(False)
+    r, r2, st = rooflines(p, 1, "fast", iters[-1], steps, ms_total, phase_ms, phase_cnt, False)
+    res = {"workload": workload_desc(1, p), "ms_per_step": ms_total / steps,
+           "value": 3 * p.block / (ms_total / steps / 1000.0), "unit": UNIT, "iterations": iters[-1],
+           "true_final_relres": out.true_final_relres, "steps": steps,
+           "roofline": r, "roofline_secondary": r2, "roofline_stencil": st}
+    del k, b, x
+    torch.cuda.empty_cache()
+    return res
+
+
+def _pinv_microbench(local, p, reps, seed):
     import torch
     from paper_2305_04421_b200.solver import HeatKKT
     dev = torch.device("cuda", local)
-    p = P.config(2)
     t0 = time.perf_counter()
     k = HeatKKT(p, mode="fast", device=local)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
-    g = torch.Generator(device=dev).manual_seed(2)
+    g = torch.Generator(device=dev).manual_seed(seed)
     v = torch.randn(3 * p.block, dtype=torch.float64, device=dev, generator=g)
     out = torch.empty_like(v)
     k.apply_P_inv(v, out)
@@ -532,80 +685,51 @@ def c2_microbench(local, reps=10):
     ts.sort()
     med = ts[len(ts) // 2]
     sw_ms = phase_ms[3] / max(1, phase_cnt[3])
-    # v5/v6 arithmetic per RASQ apply: every block row of every spatial solve does
-    # the dense on-chain product (G_J / H_J: nx^2 MACs per chain) and the
-    # off-chain triangle (Li_J / Ui_J: nx^2/2), both sweep directions
-    nx, ny, m = p.nx_int, p.ny_int, p.Nt // p.Nd
-    flops = 2.0 * 2 * 1.5 * nx * nx * ny * p.Nd * (2 * m + 1)
     tpk, tpk_src = fp64_peak()
-    tf = flops / (sw_ms / 1000.0) / 1e12 if sw_ms > 0 else None
-    res = {"workload": workload_desc(2, p), "applications": reps, "setup_s": setup_s,
+    peak, peak_src = hbm_peak()
+    fl, sb, rows = sweep_flops(p), sweep_bytes(p), sweep_block_row_steps(p)
+    tf = fl / (sw_ms / 1000.0) / 1e12 if sw_ms > 0 else None
+    gbs = sb / (sw_ms / 1000.0) / 1e9 if sw_ms > 0 else None
+    res = {"applications": reps, "setup_s": setup_s,
            "ms_per_apply_median": med, "ms_per_apply_min": ts[0],
            "value": 3 * p.block / (med / 1000.0), "unit": "unknowns/s per P^-1 apply",
            "sweep_ms_per_apply": sw_ms,
-           "roofline": {"kernel": "v6_chain_kernel<512> + v6_off_kernel<512> (sweep_v6.cu: device-wide fp64 DMMA block substitution)",
-                        "bound": "tensor", "achieved": tf, "peak": tpk, "unit": "TFLOP/s",
-                        "frac": (tf / tpk) if (tf and tpk) else None, "peak_source": tpk_src,
-                        "flops_per_apply": flops},
-           "inputs": "device-generated N(0,1) (torch, seed 2); parity at this size: tests/test_gpu_large.py"}
+           "roofline": {"kernel": "sweep v6 (sweep_v6.cu): v6_chain_kernel + v6_off(2)_kernel + v6_form_b_kernel",
+                        "bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                        "frac": (gbs / peak) if gbs else None, "peak_source": peak_src,
+                        "algorithmic_bytes_per_launch": sb, "launch_unit": "one RASQ apply",
+                        "fp64": {"flops_per_apply": fl, "achieved_tflops": tf, "peak_tflops": tpk,
+                                 "frac": (tf / tpk) if (tf and tpk) else None, "peak_source": tpk_src,
+                                 "flops_source": "SURVEY §8(a20)"},
+                        "chain": {"dependent_block_row_steps_per_apply": rows,
+                                  "us_per_block_row_step": 1000.0 * sw_ms / rows if sw_ms > 0 else None}}}
     del k, v, out
     torch.cuda.empty_cache()
+    return res
+
+
+def c2_microbench(local, reps=10):
+    """BASELINE config 2, the preconditioner-apply microbench: 10 applications
+    of P^-1 at 511^2 x 1024 steps, 64 subdomains, on seeded N(0,1) KKT vectors
+    (device-generated here: timing only; parity is tests/test_gpu_large.py and
+    tests/test_gpu_v6.py)."""
+    p = P.config(2)
+    res = _pinv_microbench(local, p, reps, 2)
+    res["workload"] = workload_desc(2, p).replace("; one step = one full solve", "; P^-1 applications")
+    res["inputs"] = "device-generated N(0,1) (torch, seed 2); parity at this size: tests/test_gpu_large.py"
     return res
 
 
 def c4_microbench(local, reps=3):
     """BASELINE config 4 (1023^2 interior, 8 GPUs) on the one GPU this pool
     has: one rank's time slab at G = 8 -- 16 subdomains of m = 8 steps,
-    Nt = 128 with config 4's dt = 1/1024 (T = 1/8) -- and P^-1 applications on
-    seeded N(0,1) KKT vectors (device-generated: timing only; parity of the
-    kernels at nx = 1023: tests/test_gpu_v6.py).  The sweep runs sweep_v6.cu
-    (device-wide block substitution, fp64 DMMA).  Opt-in (--c4): the block
+    Nt = 128 with config 4's dt = 1/1024 (T = 1/8).  Opt-in (--c4): the block
     recursion's setup takes ~40 s at nx = 1023."""
-    import torch
-    from paper_2305_04421_b200.solver import HeatKKT
-    dev = torch.device("cuda", local)
     p = P.config(4).replace(Nt=128, Nd=16, T=0.125)
-    t0 = time.perf_counter()
-    k = HeatKKT(p, mode="fast", device=local)
-    torch.cuda.synchronize()
-    setup_s = time.perf_counter() - t0
-    g = torch.Generator(device=dev).manual_seed(4)
-    v = torch.randn(3 * p.block, dtype=torch.float64, device=dev, generator=g)
-    out = torch.empty_like(v)
-    k.apply_P_inv(v, out)
-    torch.cuda.synchronize()
-    k.set_phase_timing(True)
-    ts = []
-    for _ in range(reps):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        k.apply_P_inv(v, out)
-        e1.record()
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    phase_ms, phase_cnt = k.phase_times()
-    k.set_phase_timing(False)
-    ts.sort()
-    med = ts[len(ts) // 2]
-    sw_ms = phase_ms[3] / max(1, phase_cnt[3])
-    nx, ny, m = p.nx_int, p.ny_int, p.Nt // p.Nd
-    flops = 2.0 * 2 * 1.5 * nx * nx * ny * p.Nd * (2 * m + 1)
-    tpk, tpk_src = fp64_peak()
-    tf = flops / (sw_ms / 1000.0) / 1e12 if sw_ms > 0 else None
-    res = {"workload": "config4 per-GPU slab at G=8: 1023x1023 interior, Nt=128 (dt=1/1024 as config 4), "
-                       "Nd=16 (m=8), nu=1, omega=1e-4, two-level scalar multiplicative (minus)",
-           "applications": reps, "setup_s": setup_s,
-           "ms_per_apply_median": med, "ms_per_apply_min": ts[0],
-           "value": 3 * p.block / (med / 1000.0), "unit": "unknowns/s per P^-1 apply",
-           "sweep_ms_per_apply": sw_ms,
-           "roofline": {"kernel": "v6_chain_kernel + v6_off_kernel (sweep_v6.cu: device-wide fp64 DMMA block substitution)",
-                        "bound": "tensor", "achieved": tf, "peak": tpk, "unit": "TFLOP/s",
-                        "frac": (tf / tpk) if (tf and tpk) else None, "peak_source": tpk_src,
-                        "flops_per_apply": flops},
-           "inputs": "device-generated N(0,1) (torch, seed 4); parity at nx = 1023: tests/test_gpu_v6.py"}
-    del k, v, out
-    torch.cuda.empty_cache()
+    res = _pinv_microbench(local, p, reps, 4)
+    res["workload"] = ("config4 per-GPU slab at G=8: 1023x1023 interior, Nt=128 (dt=1/1024 as config 4), "
+                       "Nd=16 (m=8), nu=1, omega=1e-4, two-level scalar multiplicative (minus)")
+    res["inputs"] = "device-generated N(0,1) (torch, seed 4); parity at nx = 1023: tests/test_gpu_v6.py, tests/test_gpu_large.py"
     return res
 
 
@@ -615,19 +739,27 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--nd", type=int, default=None, help="override the config's subdomain count (config 3: 8/32/128/256)")
     ap.add_argument("--mode", default="fast", choices=["fast", "strict", "spectral"])
-    ap.add_argument("--no-alt", action="store_true", help="skip the SPECTRAL side measurement")
+    ap.add_argument("--weak", action="store_true", help="N > 1: weak scaling (Nt and Nd x N) instead of strong")
+    ap.add_argument("--no-extras", action="store_true", help="skip the config-1 and config-2 extra measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-c2", action="store_true", help="skip the config-2 P^-1 microbench")
     ap.add_argument("--c4", action="store_true", help="add the config-4 per-GPU-slab P^-1 microbench (~40 s setup)")
+    ap.add_argument("--probe-ranks", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
-    ws, rank, local = dist_setup(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and (args.impl == "ours" or args.probe_ranks):
+        spawn_ranks(args)
+    ws, rank, local = dist_env()
+    if args.probe_ranks:
+        return probe_ranks(ws, rank)
+    if args.impl == "reference":
+        return run_reference_arm(args, ws, rank)
+    if ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but the launcher started {ws} rank(s)")
+    dist_init(ws, local)
     try:
-        if args.impl == "reference":
-            run_reference_arm(args, ws, rank)
-        else:
-            run_ours(args, ws, rank, local)
+        run_ours(args, ws, rank, local)
     finally:
         if ws > 1:
             import torch.distributed as dist

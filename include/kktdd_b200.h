@@ -118,6 +118,8 @@ int kkt_last_error_index(const kkt_ctx* ctx);
 const char* kkt_status_string(int status);
 /* Error message of the last failed kkt_ctx_create on this thread. */
 const char* kkt_create_error(void);
+/* Its index payload (SingularMatrixError::pivot_index), -1 if none. */
+int kkt_create_error_index(void);
 
 /* Sizes: global layout size (SpaceTimeLayout::size(), layout.hpp:25), the
  * rank-local node slab [node_first, node_last] and local block size. */
@@ -125,6 +127,16 @@ int kkt_layout(const kkt_ctx* ctx, int64_t* block, int32_t* n_sp, int32_t* node_
                int32_t* node_last, int64_t* local_block);
 int kkt_stream(const kkt_ctx* ctx, void** stream);
 int kkt_synchronize(kkt_ctx* ctx);
+
+/* Device vectors for callers that do not link the CUDA runtime themselves (the
+ * reference is plain host C++: its std::vector<double> / std::span arguments
+ * become buffers obtained here; include/kktdd_gpu.hpp wraps them).  `count` is
+ * in doubles.  Copies are ordered on the context's stream and complete before
+ * the call returns. */
+int kkt_device_alloc(kkt_ctx* ctx, size_t count, double** out);
+int kkt_device_free(kkt_ctx* ctx, double* p);
+int kkt_copy_to_device(kkt_ctx* ctx, double* dst_device, const double* src_host, size_t count);
+int kkt_copy_to_host(kkt_ctx* ctx, double* dst_host, const double* src_device, size_t count);
 
 /* ---- heat operators (heat_operators.hpp:41-61), full space-time blocks ---- */
 int kkt_apply_J(kkt_ctx* ctx, const double* u, double* out);      /* heat_operators.cpp:57-69 */

@@ -71,6 +71,7 @@ void Ctx::tcollect() {
 namespace {
 
 thread_local std::string g_create_err;
+thread_local int g_create_err_index = -1;
 
 void validate(const kkt_problem_desc& d) {
   auto fail = [](const std::string& m) { throw Error(KKT_ECONFIG, m); };
@@ -280,6 +281,7 @@ const char* kkt_status_string(int s) {
 }
 
 const char* kkt_create_error(void) { return kkt::g_create_err.c_str(); }
+int kkt_create_error_index(void) { return kkt::g_create_err_index; }
 
 int kkt_ctx_create(const kkt_problem_desc* desc, const kkt_runtime_opts* opts, kkt_ctx** out) {
   if (!desc || !out) return KKT_EINVAL;
@@ -289,15 +291,18 @@ int kkt_ctx_create(const kkt_problem_desc* desc, const kkt_runtime_opts* opts, k
     kkt::setup(&h->impl, *desc, opts);
   } catch (const Error& e) {
     kkt::g_create_err = e.what();
+    kkt::g_create_err_index = e.index;
     const int st = e.status;
     delete h;
     return st;
   } catch (const std::exception& e) {
     kkt::g_create_err = e.what();
+    kkt::g_create_err_index = -1;
     delete h;
     return KKT_EINVAL;
   }
   kkt::g_create_err.clear();
+  kkt::g_create_err_index = -1;
   *out = h;
   return KKT_OK;
 }
@@ -330,6 +335,37 @@ int kkt_stream(const kkt_ctx* ctx, void** stream) {
 
 int kkt_synchronize(kkt_ctx* ctx) {
   return kkt::guard(ctx, [](Ctx* c) { KKT_CUDA(cudaStreamSynchronize(c->stream)); });
+}
+
+int kkt_device_alloc(kkt_ctx* ctx, size_t count, double** out) {
+  return kkt::guard(ctx, [&](Ctx*) {
+    kkt::need(out != nullptr, "kkt_device_alloc: null out");
+    *out = nullptr;
+    if (count) KKT_CUDA(cudaMalloc(out, count * sizeof(double)));
+  });
+}
+
+int kkt_device_free(kkt_ctx* ctx, double* p) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+    if (p) KKT_CUDA(cudaFree(p));
+  });
+}
+
+int kkt_copy_to_device(kkt_ctx* ctx, double* dst, const double* src_host, size_t count) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(count == 0 || (dst && src_host), "kkt_copy_to_device: null pointer");
+    KKT_CUDA(cudaMemcpyAsync(dst, src_host, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int kkt_copy_to_host(kkt_ctx* ctx, double* dst_host, const double* src, size_t count) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(count == 0 || (dst_host && src), "kkt_copy_to_host: null pointer");
+    KKT_CUDA(cudaMemcpyAsync(dst_host, src, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+  });
 }
 
 #define KKT_OP(name, body)                                                   \
@@ -533,7 +569,10 @@ int kkt_run_single(const kkt_problem_desc* desc, const kkt_runtime_opts* opts, k
       KKT_CUDA(cudaStreamSynchronize(c->stream));
     }
   });
-  if (st != KKT_OK) kkt::g_create_err = kkt_last_error(ctx);
+  if (st != KKT_OK) {
+    kkt::g_create_err = kkt_last_error(ctx);
+    kkt::g_create_err_index = kkt_last_error_index(ctx);
+  }
   kkt_ctx_destroy(ctx);
   return st;
 }

@@ -166,7 +166,7 @@ class HeatKKT:
         h = _P()
         st = L.kkt_ctx_create(C.byref(self._desc), C.byref(opts), C.byref(h))
         if st != 0:
-            _raise(st, L.kkt_create_error().decode(), -1)
+            _raise(st, L.kkt_create_error().decode(), L.kkt_create_error_index())
         self._h = h
         blk, nsp, nf, nl, lb = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
         L.kkt_layout(h, C.byref(blk), C.byref(nsp), C.byref(nf), C.byref(nl), C.byref(lb))

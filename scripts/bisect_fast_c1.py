@@ -27,6 +27,8 @@ VARIANTS = [
     ("fast + sequential node sums (KKT_BISECT=2)", {"KKT_BISECT": "2"}),
     ("fast + reference-order MGS, tree dots (KKT_BISECT=16)", {"KKT_BISECT": "16"}),
     ("fast + reference-order MGS, sequential dots (KKT_BISECT=8)", {"KKT_BISECT": "8"}),
+    ("fast + sequential dots + sequential node sums + unfused K2 (KKT_BISECT=11)", {"KKT_BISECT": "11"}),
+    ("fast + sequential dots + reference banded substitution (KKT_BISECT=12)", {"KKT_BISECT": "12"}),
     ("fast + reference banded substitution in the sweep (KKT_BISECT=4)", {"KKT_BISECT": "4"}),
     ("fast + strict sweep + node sums + unfused K2 (KKT_BISECT=7)", {"KKT_BISECT": "7"}),
     ("fast + strict sweep/sums/K2 + reference MGS tree dots (KKT_BISECT=23)", {"KKT_BISECT": "23"}),
@@ -62,6 +64,8 @@ def child(cfg):
     hf = o.residual_history
     n = min(len(h), len(hf))
     dev = np.abs(hf[:n] - h[:n]) / h[:n]
+    if os.environ.get("_SAVE"):
+        np.save(os.environ["_SAVE"], x[idx])
     print(json.dumps({"iterations": o.iterations, "ref_iterations": gold["iterations"],
                       "true_final_relres": o.true_final_relres, "rel_l2_vs_reference": rel,
                       "history_max_rel_dev": float(dev.max()),
@@ -75,22 +79,43 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--out", default=None)
     ap.add_argument("--strict", action="store_true", help="also run STRICT (2.5 min at config 1)")
+    ap.add_argument("--only", default=None, help="comma-separated variant indices (0 = fast default is always run)")
     a = ap.parse_args()
     if a.child:
         return child(a.config)
+    import tempfile
+    import numpy as np
     rows = []
+    tmp = tempfile.mkdtemp()
+    base = None
     variants = list(VARIANTS)
     if a.strict:
         variants.append(("strict", {"_MODE": "strict"}))
+    if a.only:
+        keep = {0} | {int(v) for v in a.only.split(",")}
+        variants = [v for i, v in enumerate(variants) if i in keep]
     for name, env in variants:
         e = dict(os.environ)
         e.update(env)
+        e["_SAVE"] = os.path.join(tmp, f"x{len(rows)}.npy")
         r = subprocess.run([sys.executable, os.path.abspath(__file__), "--child", "--config", str(a.config)],
                            env=e, capture_output=True, text=True)
         try:
             rec = json.loads(r.stdout.strip().splitlines()[-1])
         except Exception:
             rec = {"error": (r.stderr or r.stdout)[-400:]}
+        # distance to the default FAST iterate: the accurate-summation variants agree with one
+        # another far more closely than any of them agrees with the reference
+        try:
+            xs = np.load(e["_SAVE"])
+            if base is None:
+                base = xs
+            n3 = xs.size // 3  # the sample takes every 1009th entry, so the thirds are the blocks to ~1 entry
+            rec["rel_l2_vs_fast_default"] = {nm: float(np.linalg.norm(xs[i * n3:(i + 1) * n3] - base[i * n3:(i + 1) * n3]) /
+                                                     np.linalg.norm(base[i * n3:(i + 1) * n3]))
+                                             for i, nm in enumerate("uzw")}
+        except Exception:
+            pass
         rec["variant"] = name
         rec["env"] = env
         rows.append(rec)
