@@ -496,6 +496,19 @@ int kkt_gmres_solve_host(kkt_ctx* ctx, const double* b_host, double* x_host,
   });
 }
 
+int kkt_apply_P_inv_host(kkt_ctx* ctx, const double* r_host, double* out_host) {
+  return kkt::guard(ctx, [&](Ctx* c) {
+    kkt::need(r_host && out_host, "kkt_apply_P_inv_host: bad arguments");
+    const size_t n = size_t(3 * c->B);
+    if (c->e2e_b.n < n) c->e2e_b.alloc(n);
+    if (c->e2e_x.n < n) c->e2e_x.alloc(n);
+    KKT_CUDA(cudaMemcpyAsync(c->e2e_b.p, r_host, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    kkt::pinv_apply(c, c->e2e_b.p, c->e2e_x.p);
+    KKT_CUDA(cudaMemcpyAsync(out_host, c->e2e_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
 namespace kkt {
 namespace {
 // assemble_rhs (kkt.cpp:29-48) with model_initial_condition / model_target

@@ -131,6 +131,9 @@ struct Ctx {
   DBuf<double> v6_ops, v6_w;
   DBuf<unsigned> v6_cnt;
   int v6_jstar = 0, v6_nops = 0, v6_kn = 0;
+  // k-row grouping of the v6 chain (sweep_v6.cu): propagator products over groups of v6_k block rows
+  DBuf<double> v6_phi;
+  int v6_k = 1, v6_nind = 0, v6_gconv = 0, v6_nphi = 0, v6_npsi = 0;
   DBuf<unsigned> v4_flags;
   int v4_nsets = 0;
   bool v4_coop = false, v4_registered = false;

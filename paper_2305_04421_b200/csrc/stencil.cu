@@ -66,35 +66,59 @@ __global__ void __launch_bounds__(kThreads) scale_kernel(int64_t n, const double
 //   ow = (A u_n - u_{n-1}) - dt*z         (:63-64)
 // With `bm` non-null the kernel writes bm - K v instead (the restart
 // residual r = b - A x of gmres.cpp:50-51, same rounding as a separate pass).
-__global__ void __launch_bounds__(kThreads) apply_K_kernel(Stencil s, int nt, int nsp, double ms,
-                                                           double oms, double dt, float inv_nx,
-                                                           const double* __restrict__ v,
-                                                           double* __restrict__ out,
-                                                           const double* __restrict__ bm,
-                                                           const double* __restrict__ u_prev,
-                                                           const double* __restrict__ w_next) {
-  // grid: x over the points of a plane, y over planes (no 64-bit division);
-  // j = p / nx from a float reciprocal, exact for p < 2^20, nx < 2^11
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= nsp) return;
-  const int j = int((float(p) + 0.5f) * inv_nx);
-  const int i = p - j * s.nx;
+//
+// Traffic: the algorithmic minimum is 3 reads + 3 writes per point.  A CTA owns
+// a kTX x kTY spatial tile (so the j-1 / j+1 rows of u and w are fetched once
+// per kTY rows, and merge in L1 with the neighbouring threads' own loads) and
+// marches over kTP consecutive time nodes: u_{n-1} stays in a register from the
+// previous node, and w_{n+1}, loaded for node n, is node n+1's own w value, so
+// the time neighbours cost no second pass over u and w.
+constexpr int kTX = 64, kTY = 4, kTP = 16;
+__global__ void __launch_bounds__(kTX * kTY) apply_K_kernel(Stencil s, int nt, int nsp, double ms,
+                                                            double oms, double dt,
+                                                            const double* __restrict__ v,
+                                                            double* __restrict__ out,
+                                                            const double* __restrict__ bm,
+                                                            const double* __restrict__ u_prev,
+                                                            const double* __restrict__ w_next) {
+  const int i = blockIdx.x * kTX + (threadIdx.x & (kTX - 1));
+  const int j = blockIdx.y * kTY + (threadIdx.x / kTX);
+  if (i >= s.nx || j >= s.ny) return;
+  const int p = j * s.nx + i;
   const int64_t B = int64_t(nt) * nsp;
   const double* u = v;
   const double* z = v + B;
   const double* w = v + 2 * B;
-  for (int n0 = blockIdx.y; n0 < nt; n0 += gridDim.y) {
+  const int nA = blockIdx.z * kTP, nB = min(nt, nA + kTP);
+  // time neighbours carried across the march
+  double up = 0.0, ww = w[int64_t(nA) * nsp + p];
+  bool has_up = false;
+  if (nA > 0) {
+    up = u[int64_t(nA - 1) * nsp + p];
+    has_up = true;
+  } else if (u_prev) {
+    up = u_prev[p];
+    has_up = true;
+  }
+  for (int n0 = nA; n0 < nB; ++n0) {
     const int64_t off = int64_t(n0) * nsp;
     const int64_t idx = off + p;
-    const double uu = u[idx], zz = z[idx], ww = w[idx];
+    double wn = 0.0;
+    bool has_wn = false;
+    if (n0 < nt - 1) {
+      wn = w[idx + nsp];
+      has_wn = true;
+    } else if (w_next) {
+      wn = w_next[p];
+      has_wn = true;
+    }
+    const double uu = u[idx], zz = z[idx];
     double ou = band_row_strict_ij(s, w + off, p, i, j);
-    if (n0 < nt - 1) ou = ssub(ou, w[idx + nsp]);
-    else if (w_next) ou = ssub(ou, w_next[p]);
+    if (has_wn) ou = ssub(ou, wn);
     ou = sadd(ou, smul(ms, uu));
     const double oz = ssub(smul(oms, zz), smul(dt, ww));
     double ow = band_row_strict_ij(s, u + off, p, i, j);
-    if (n0 > 0) ow = ssub(ow, u[idx - nsp]);
-    else if (u_prev) ow = ssub(ow, u_prev[p]);
+    if (has_up) ow = ssub(ow, up);
     ow = ssub(ow, smul(dt, zz));
     if (bm) {
       out[idx] = ssub(bm[idx], ou);
@@ -105,6 +129,9 @@ __global__ void __launch_bounds__(kThreads) apply_K_kernel(Stencil s, int nt, in
       out[idx + B] = oz;
       out[idx + 2 * B] = ow;
     }
+    up = uu;
+    has_up = true;
+    ww = wn;
   }
 }
 
@@ -195,9 +222,9 @@ void op_apply_K(Ctx* c, const double* v, double* out, const double* b_minus) {
     if (c->rank > 0) h.prev = hp;
     if (c->rank + 1 < c->nranks) h.next = hn;
   }
-  const dim3 gK((c->nsp + kThreads - 1) / kThreads, std::min(c->ntl, 128));  // a few planes per thread
-  KKT_LAUNCH(c, apply_K_kernel, gK, kThreads, 0, c->A, c->ntl, c->nsp, c->ms, c->oms, c->dt,
-             1.0f / float(c->nx), v, out, b_minus, h.prev, h.next);
+  const dim3 gK((c->nx + kTX - 1) / kTX, (c->ny + kTY - 1) / kTY, (c->ntl + kTP - 1) / kTP);
+  KKT_LAUNCH(c, apply_K_kernel, gK, kTX * kTY, 0, c->A, c->ntl, c->nsp, c->ms, c->oms, c->dt, v, out,
+             b_minus, h.prev, h.next);
 }
 
 void op_pinv_uz(Ctx* c, const double* r, double* out) {

@@ -77,6 +77,17 @@ struct V6Params {
   unsigned* cnt;     // per chain group: row-completion counter (chain kernels)
   int g0;            // first chain group of this chain-kernel wave
   int jstar;         // block rows J >= jstar use row jstar's operators (ny: none)
+  // k-row grouping of the chain: the ny block rows form ngr groups of k rows (L: from row 0 up,
+  // U: from row ny-1 down); a group's rows all depend on the previous group's LAST row only,
+  //   y_{g k + i} = c'_{g k + i} + Phi_{g k + i} y_{g k - 1},  Phi_{g k + i} = G_{g k + i} ... G_{g k},
+  // with c' the zero-inflow chain inside the group (v6_inner_kernel), so one row handoff serves
+  // k rows.  k == 1: Phi = G, the plain recurrence.
+  const double* Phi;  // packed propagators of the L groups (k == 1: Gp)
+  const double* Psi;  // packed propagators of the U groups (k == 1: Hp)
+  int k, ngr;
+  int nind;           // L: groups [0, nind) have their own Phi rows, the rest share one converged set
+  int gconv;          // U: groups [0, gconv) (from the top) share the converged set, the rest have their own
+  int pass;           // v6_inner_kernel: row i of every group
   long long* tim;    // KKT_V6_TIM: per-row clock64 phase sums of CTA 0 (6 per direction)
 };
 
@@ -336,6 +347,88 @@ __global__ void __launch_bounds__(kOffThr, 1) v6_off2_kernel(V6Params P) {
   }
 }
 
+// Row of the group-local numbering: group gr, row i of the group (L: rows ascend from 0, U: descend
+// from ny-1); -1 when the (ragged, last) group has no such row.
+__device__ __forceinline__ int grow(bool upper, int gr, int i, int k, int ny) {
+  const int J = upper ? ny - 1 - gr * k - i : gr * k + i;
+  return (J >= 0 && J < ny) ? J : -1;
+}
+// Packed propagator index of (group gr, row i): see V6Params.
+__device__ __forceinline__ int propidx(bool upper, int gr, int i, int J, const V6Params& P) {
+  if (P.k == 1) return oprow(J, P.jstar);
+  if (upper) return gr < P.gconv ? i : P.k + (gr - P.gconv) * P.k + i;
+  return gr < P.nind ? gr * P.k + i : P.nind * P.k + i;
+}
+
+// Zero-inflow chains inside the groups, pass i = P.pass (1 .. k-1), every group at once:
+//   L: c'_J = c_J + G_J c'_{J-1},  J = g k + i;   U: d'_J = d_J + H_J d'_{J+1},  J = ny-1 - g k - i
+// in place in W1.  One CTA per (group, pair of chain groups); the two chain groups' c'_{J-+1} are
+// staged in shared memory; each warp owns whole 16-row slices and streams its operator slice from
+// L2 / HBM in fragment order, 16 k-steps in flight (as v6_off_kernel, full rows instead of triangles).
+template <int KN, bool kUpper>
+__global__ void __launch_bounds__(kThr6, 1) v6_inner_kernel(V6Params P) {
+  V6_DIMS
+  extern __shared__ double Bs[];  // [2][kN][8]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bo = (lane & 3) * kG + (lane >> 2);
+  const int npairs = (P.ngroups + 1) / 2;
+  const int gr = blockIdx.x / npairs, gp = 2 * (blockIdx.x % npairs);
+  const int J = grow(kUpper, gr, P.pass, P.k, P.ny);
+  if (J < 0) return;
+  const int Jp = kUpper ? J + 1 : J - 1;
+  for (int i = threadIdx.x; i < KN * kG; i += kThr6) {  // double2 units over both groups
+    const int gi = i / (KN * kG / 2), r = i - gi * (KN * kG / 2);
+    double2 v = make_double2(0.0, 0.0);
+    if (gp + gi < P.ngroups) v = __ldcg(reinterpret_cast<const double2*>(P.W1 + widx<KN>(gp + gi, Jp, P.ny)) + r);
+    reinterpret_cast<double2*>(Bs)[i] = v;
+  }
+  __syncthreads();
+  const bool res = J >= P.jstar;
+  for (int s = warp; s < kSl; s += 8) {
+    const double* A = (kUpper ? P.Hp : P.Gp) + (size_t(oprow(J, P.jstar)) * kSl + s) * kKS * 64 + lane;
+    double d[2][2][2] = {};
+    double ac[kOffChunk][2], an[kOffChunk][2];
+#pragma unroll
+    for (int u = 0; u < kOffChunk; ++u) {
+      ac[u][0] = ldop(A + size_t(u) * 64, res);
+      ac[u][1] = ldop(A + size_t(u) * 64 + 32, res);
+    }
+    for (int ks = 0; ks < kKS; ks += kOffChunk) {
+#pragma unroll
+      for (int u = 0; u < kOffChunk; ++u) {
+        const bool ok = ks + kOffChunk + u < kKS;
+        an[u][0] = ok ? ldop(A + size_t(ks + kOffChunk + u) * 64, res) : 0.0;
+        an[u][1] = ok ? ldop(A + size_t(ks + kOffChunk + u) * 64 + 32, res) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kOffChunk; ++u) {
+        const double b0 = Bs[(4 * (ks + u)) * kG + bo];
+        const double b1 = Bs[KN * kG + (4 * (ks + u)) * kG + bo];
+        dmma6(d[0][0][0], d[0][0][1], ac[u][0], b0);
+        dmma6(d[0][1][0], d[0][1][1], ac[u][1], b0);
+        dmma6(d[1][0][0], d[1][0][1], ac[u][0], b1);
+        dmma6(d[1][1][0], d[1][1][1], ac[u][1], b1);
+      }
+#pragma unroll
+      for (int u = 0; u < kOffChunk; ++u) {
+        ac[u][0] = an[u][0];
+        ac[u][1] = an[u][1];
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      if (gp + g >= P.ngroups) break;
+      double* O = P.W1 + widx<KN>(gp + g, J, P.ny) + size_t(16 * s + (lane >> 2)) * kG + 2 * (lane & 3);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        double2* o2 = reinterpret_cast<double2*>(O + mt * 8 * kG);
+        const double2 c0 = *o2;
+        *o2 = make_double2(c0.x + d[g][mt][0], c0.y + d[g][mt][1]);
+      }
+    }
+  }
+}
+
 // The dependent chain of one sweep direction for chain groups g0 .. g0 + gridDim.x/kSl - 1:
 //   L: y_J = c_J + G_J y_{J-1}  (J = 0 .. ny-1; c in W1, y to W0)
 //   U: x_J = d_J + H_J x_{J+1}  (J = ny-1 .. 0; d in W1, x to W0 and the job's outputs)
@@ -359,12 +452,16 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
   double* red = Bs + KN * kG;      // [warp 8][128]
   uint64_t* barA = reinterpret_cast<uint64_t*>(red + 8 * 128);
   uint64_t* barB = barA + 1;  // [2]: the halves of y_{J-1} (warps 0-3 use k < KN/2, warps 4-7 the rest)
-  const int s = blockIdx.x % kSl, g = P.g0 + blockIdx.x / kSl;
+  // CTA (sigma, g): sigma = i * kSl + s is slice s of row i of every group
+  const int rows_per_g = kSl * P.k;
+  const int sig = blockIdx.x % rows_per_g, g = P.g0 + blockIdx.x / rows_per_g;
+  const int s = sig % kSl, gi = sig / kSl;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ny = P.ny;
-  const double* Mbase = (kUpper ? P.Hp : P.Gp) + size_t(s) * kKS * 64;
+  const double* Mbase = (kUpper ? P.Psi : P.Phi) + size_t(s) * kKS * 64;
   const size_t mstride = size_t(kSl) * kKS * 64;
   unsigned* cnt = P.cnt + g;
+  const bool last_row = gi == P.k - 1;  // the row the next group waits for
   int m = 0, n = 0;
   const bool outt = threadIdx.x < 128;
   if (outt) slice_coords(threadIdx.x, m, n);
@@ -380,7 +477,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
       if (st.out2 && st.node2 > 0 && P.gam) g2 = P.gam[st.node2];
     }
   }
-  auto Jof = [&](int idx) { return kUpper ? ny - 1 - idx : idx; };
+  auto Jof = [&](int gr) { return grow(kUpper, gr, gi, P.k, ny); };  // this CTA's row of group gr
   auto emit = [&](int J, double v) {
     P.W0[widx<KN>(g, J, ny) + size_t(row) * kG + n] = v;
     if (out) out[size_t(J) * P.nx + row] = v;
@@ -389,13 +486,13 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
   // each output warp publishes its own stores (release after __syncwarp), so
   // no CTA-wide barrier sits between the stores and the count; 4 per CTA and row
   auto signal = [&]() {
-    if (outt) {
+    if (outt && last_row) {
       __syncwarp();
       if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(cnt) : "memory");
     }
   };
-  auto copy_a = [&](int J) {  // thread 0
-    tma_load(As, Mbase + size_t(oprow(J, P.jstar)) * mstride, sizeof(double) * 16 * KN, barA);
+  auto copy_a = [&](int gr, int J) {  // thread 0
+    tma_load(As, Mbase + size_t(propidx(kUpper, gr, gi, J, P)) * mstride, sizeof(double) * 16 * KN, barA);
   };
   if (threadIdx.x == 0) {
     mbar_init(barA, 1);
@@ -404,17 +501,20 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  {
+  {  // group 0 has no inflow: its rows are the zero-inflow chain values
     const int J = Jof(0);
+    if (J < 0) return;
     if (outt) emit(J, __ldcg(P.W1 + widx<KN>(g, J, ny) + size_t(row) * kG + n));
     signal();
-    if (ny > 1 && threadIdx.x == 0) copy_a(Jof(1));
+    if (P.ngr > 1 && Jof(1) >= 0 && threadIdx.x == 0) copy_a(1, Jof(1));
   }
   const int bo = (lane & 3) * kG + (lane >> 2);
   const bool tm = P.tim && blockIdx.x == 0 && threadIdx.x == 0;
   long long ts[7] = {0, 0, 0, 0, 0, 0, 0}, acc[6] = {0, 0, 0, 0, 0, 0};
-  for (int idx = 1; idx < ny; ++idx) {
-    const int J = Jof(idx), Jp = kUpper ? J + 1 : J - 1;
+  for (int idx = 1; idx < P.ngr; ++idx) {
+    const int J = Jof(idx);
+    if (J < 0) break;  // the ragged last group has no such row (and no successor waits for it)
+    const int Jp = kUpper ? ny - idx * P.k : idx * P.k - 1;  // the previous group's last row
     if (tm) ts[0] = clock64();
     const uint32_t par = uint32_t(idx - 1) & 1u;
     double cval = 0.0;
@@ -467,7 +567,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
     if (outt) emit(J, cval + reduce8(red, threadIdx.x));
     if (tm) ts[5] = clock64();
     signal();
-    if (idx + 1 < ny && threadIdx.x == 0) copy_a(Jof(idx + 1));
+    if (idx + 1 < P.ngr && Jof(idx + 1) >= 0 && threadIdx.x == 0) copy_a(idx + 1, Jof(idx + 1));
     if (tm) {
       ts[6] = clock64();
       for (int q = 0; q < 6; ++q) acc[q] += ts[q + 1] - ts[q];
@@ -521,6 +621,10 @@ __global__ void v6_pack_kernel(const double* __restrict__ src, int nx, int nJ, d
   }
 }
 
+__global__ void v6_scale_kernel(int64_t n, double f, double* __restrict__ a) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) a[e] *= f;
+}
+
 bool off_plain() {  // KKT_V6_OFF=1: the plain-load off-chain kernel
   static const bool v = std::getenv("KKT_V6_OFF") != nullptr;
   return v;
@@ -530,7 +634,7 @@ template <int KN>
 void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
   V6_DIMS
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(kSl * ngroups_wave);
+  cfg.gridDim = dim3(kSl * P.k * ngroups_wave);
   cfg.blockDim = dim3(kThr6);
   cfg.dynamicSmemBytes = chain_smem<KN>();
   cfg.stream = c->stream;
@@ -547,17 +651,19 @@ void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
   c->launches++;
 }
 
-// chain groups per co-resident wave; also sets the kernels' shared-memory limits
+// co-resident chain CTAs of the device; also sets the kernels' shared-memory limits
 template <int KN>
-int groups_per_wave() {
+int chain_capacity() {
   V6_DIMS
-  static int gpw = 0;
-  if (!gpw) {
+  static int cap = 0;
+  if (!cap) {
     const int cs = int(chain_smem<KN>()), os = int(off_smem<KN>());
     KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
     KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
+    KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
+    KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     const int os2 = int(off2_smem<KN>());
     KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
     KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
@@ -567,11 +673,18 @@ int groups_per_wave() {
     int dev = 0, nsm = kSmCount;
     KKT_CUDA(cudaGetDevice(&dev));
     KKT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    gpw = std::max(1, std::min(p0, p1) * nsm / kSl);
+    cap = std::max(1, std::min(p0, p1)) * nsm;
     if (std::getenv("KKT_V6_TIM"))
-      std::fprintf(stderr, "v6 KN %d: %d chain CTAs per SM, %d chain groups per wave\n", KN, std::min(p0, p1), gpw);
+      std::fprintf(stderr, "v6 KN %d: %d chain CTAs per SM, %d co-resident\n", KN, std::min(p0, p1), cap);
   }
-  return gpw;
+  return cap;
+}
+
+// chain groups (of 8 chains) per co-resident wave at grouping k
+template <int KN>
+int groups_per_wave(int k) {
+  V6_DIMS
+  return std::max(1, chain_capacity<KN>() / (kSl * k));
 }
 
 template <int KN>
@@ -581,8 +694,9 @@ void pack(Ctx* c, const double* src, int nJ, double scale, double* dst) {
 
 template <int KN>
 void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
-  const int gpw = groups_per_wave<KN>();
+  const int gpw = groups_per_wave<KN>(P.k);
   const int og = std::min(P.ny, kSmCount);
+  const int npairs = (ngroups + 1) / 2;
   for (int t = 0; t < nsteps; ++t) {
     P.t = t;
     P.g0 = 0;
@@ -600,6 +714,13 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
         else
           KKT_LAUNCH(c, (v6_off2_kernel<KN, false>), og, kOffThr, off2_smem<KN>(), P);
       }
+      for (int i = 1; i < P.k; ++i) {  // zero-inflow chains inside the groups, every group at once
+        P.pass = i;
+        if (up)
+          KKT_LAUNCH(c, (v6_inner_kernel<KN, true>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
+        else
+          KKT_LAUNCH(c, (v6_inner_kernel<KN, false>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
+      }
       KKT_CUDA(cudaMemsetAsync(P.cnt, 0, sizeof(unsigned) * ngroups, c->stream));
       for (int g0 = 0; g0 < ngroups; g0 += gpw) {
         P.g0 = g0;
@@ -607,6 +728,12 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
       }
     }
   }
+}
+
+template <int KN>
+int choose_k(int ngroups) {
+  V6_DIMS
+  return chain_capacity<KN>() / (kSl * std::max(1, ngroups));
 }
 
 }  // namespace
@@ -688,6 +815,68 @@ void build_v6(Ctx* c) {
     pk(T.p, nb, c->cy, Hp + J0 * mat);
   }
   KKT_CUDA(cudaStreamSynchronize(c->stream));  // T is freed on return
+
+  // ---- k-row grouping: as many rows per handoff as co-resident CTAs allow for the RASQ chains
+  // (KKT_V6_K overrides; 1 = the plain row-by-row chain)
+  const int rasq_groups = (std::max(1, c->ndl) + kG - 1) / kG;
+  int k = kn == 256 ? choose_k<256>(rasq_groups) : kn == 512 ? choose_k<512>(rasq_groups) : choose_k<1024>(rasq_groups);
+  k = std::min(k, 8);
+  if (const char* e = std::getenv("KKT_V6_K")) k = std::atoi(e);
+  k = std::max(1, std::min(k, ny));
+  c->v6_k = k;
+  if (k == 1) return;
+  const int js = c->v6_jstar;               // rows >= js share row js's operators (ny: none)
+  const int ngr = (ny + k - 1) / k;
+  // L groups [0, nind) are built row by row, groups >= nind (all rows >= js) share one converged set;
+  // U groups (from the top) [0, gconv) share the converged set, the rest are built row by row
+  const int nind = js >= ny ? ngr : std::min(ngr, (js + k - 1) / k);
+  const int gconv = js >= ny ? 0 : std::min(ngr, (ny - js) / k);
+  c->v6_nind = nind;
+  c->v6_gconv = gconv;
+  c->v6_nphi = nind * k + k;
+  c->v6_npsi = k + (ngr - gconv) * k;
+  c->v6_phi.alloc(size_t(c->v6_nphi + c->v6_npsi) * mat);
+  KKT_CUDA(cudaMemsetAsync(c->v6_phi.p, 0, sizeof(double) * c->v6_phi.n, c->stream));
+  double* Phi = c->v6_phi.p;
+  double* Psi = Phi + size_t(c->v6_nphi) * mat;
+  auto opr = [&](int J) { return J < js ? J : js; };
+  // unpacked scaled G_J (J >= 1) and H_J (J <= ny - 2) for the operator rows in use
+  DBuf<double> Gu(size_t(nops) * nn), Hu(size_t(nops) * nn), Pu(size_t(k) * nn);
+  KKT_CUDA(cudaMemsetAsync(Gu.p, 0, sizeof(double) * nn, c->stream));
+  {
+    GemmArgs g{c->Li.p + nn, c->Ui.p, Gu.p + nn, nx, nx, nx, int64_t(nn), int64_t(nn), int64_t(nn), nx, nx, nx};
+    if (nops > 1) gemm_f64(c, g, nops - 1);
+    GemmArgs h{c->Ui.p, c->Li.p, Hu.p, nx, nx, nx, int64_t(nn), int64_t(nn), int64_t(nn), nx, nx, nx};
+    gemm_f64(c, h, nh);
+    if (nh < nops) KKT_CUDA(cudaMemsetAsync(Hu.p + size_t(nh) * nn, 0, sizeof(double) * nn * (nops - nh), c->stream));
+    const int64_t tot = int64_t(nops) * nn;
+    KKT_LAUNCH(c, v6_scale_kernel, kSmCount * 8, 256, 0, tot, c->cy, Gu.p);
+    KKT_LAUNCH(c, v6_scale_kernel, kSmCount * 8, 256, 0, tot, c->cy, Hu.p);
+  }
+  // one group's propagators: P_0 = M_{J(0)}, P_i = M_{J(i)} P_{i-1}; packed to dst[i]
+  auto build_group = [&](const double* Mu, auto rowof, double* dst) {
+    for (int i = 0; i < k; ++i) {
+      const int J = rowof(i);
+      if (J < 0 || J >= ny) break;
+      const double* M = Mu + size_t(opr(J)) * nn;
+      if (i == 0) {
+        KKT_CUDA(cudaMemcpyAsync(Pu.p, M, sizeof(double) * nn, cudaMemcpyDeviceToDevice, c->stream));
+      } else {
+        GemmArgs g{M, Pu.p + size_t(i - 1) * nn, Pu.p + size_t(i) * nn, nx, nx, nx, 0, 0, 0, nx, nx, nx};
+        gemm_f64(c, g, 1);
+      }
+      pk(Pu.p + size_t(i) * nn, 1, 1.0, dst + size_t(i) * mat);
+    }
+  };
+  for (int gr = 1; gr < nind; ++gr)  // group 0 has no inflow
+    build_group(Gu.p, [&](int i) { return gr * k + i; }, Phi + size_t(gr) * k * mat);
+  if (nind < ngr) build_group(Gu.p, [&](int i) { (void)i; return js; }, Phi + size_t(nind) * k * mat);
+  if (gconv > 0) build_group(Hu.p, [&](int i) { (void)i; return js; }, Psi);
+  for (int gr = std::max(1, gconv); gr < ngr; ++gr)
+    build_group(Hu.p, [&](int i) { return ny - 1 - gr * k - i; }, Psi + size_t(k + (gr - gconv) * k) * mat);
+  KKT_CUDA(cudaStreamSynchronize(c->stream));  // the temporaries are freed on return
+  if (std::getenv("KKT_V6_TIM"))
+    std::fprintf(stderr, "v6 grouping k %d: %d groups, L own %d, U converged %d\n", k, ngr, nind, gconv);
 }
 
 void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms) {
@@ -722,6 +911,13 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.inv_ms = 1.0 / c->ms;
   P.coarse = coarse_terms ? 1 : 0;
   P.cnt = c->v6_cnt.p;
+  P.k = c->v6_k;
+  P.ngr = (ny + P.k - 1) / P.k;
+  P.nind = c->v6_nind;
+  P.gconv = c->v6_gconv;
+  P.pass = 0;
+  P.Phi = P.k == 1 ? P.Gp : c->v6_phi.p;
+  P.Psi = P.k == 1 ? P.Hp : c->v6_phi.p + size_t(c->v6_nphi) * mat;
   static const bool dbg = std::getenv("KKT_V6_TIM") != nullptr;
   DBuf<long long> tim;
   P.tim = nullptr;

@@ -286,6 +286,16 @@ class HeatKKT:
     def apply_K(self, v, out=None): return self._unary("kkt_apply_K", v, 3 * self.block, out)
     def apply_P_inv(self, r, out=None): return self._unary("kkt_apply_P_inv", r, 3 * self.block, out)
 
+    def apply_P_inv_host(self, r_host: np.ndarray, out_host: Optional[np.ndarray] = None) -> np.ndarray:
+        """apply_P_inv from host buffers; H2D/D2H copies inside the call."""
+        r_host = np.ascontiguousarray(r_host, dtype=np.float64)
+        if r_host.size != 3 * self.block:
+            raise ValueError(f"vector length {r_host.size}, expected {3 * self.block}")
+        if out_host is None:
+            out_host = np.empty_like(r_host)
+        self._call("kkt_apply_P_inv_host", r_host.ctypes.data_as(_P), out_host.ctypes.data_as(_P))
+        return out_host
+
     def kkt_residual(self, v, rhs) -> float:
         v = self._dev(v, 3 * self.block)
         rhs = self._dev(rhs, 3 * self.block)

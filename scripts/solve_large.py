@@ -42,11 +42,14 @@ def main():
     ap.add_argument("--nt", type=int, default=None)
     ap.add_argument("--mode", default="fast")
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--max-iters", type=int, default=None)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     p = P.config(a.config, Nd=a.nd)
     if a.nt:
         p = p.replace(Nt=a.nt)
+    if a.max_iters:
+        p = p.replace(max_iters=a.max_iters)
     t0 = time.time()
     b_host = slab_rhs(a.config, p, 1, p.Nt)
     rhs_s = time.time() - t0

@@ -1,4 +1,4 @@
-"""Time-slab sharding plan — host-side mirror of what
+"""TEST HELPER (not product code): time-slab sharding plan — a host-side mirror of what
 kkt_ctx_create computes for a rank (csrc/capi.cu, setup()).
 
 Rank g of G owns the whole subdomains [g*Nd/G, (g+1)*Nd/G) of the reference's
@@ -17,7 +17,7 @@ import dataclasses
 
 import numpy as np
 
-from .problems import Problem
+from paper_2305_04421_b200.problems import Problem
 
 
 @dataclasses.dataclass(frozen=True)

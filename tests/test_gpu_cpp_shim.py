@@ -33,6 +33,9 @@ def test_reference_cases_through_the_cpp_binding(arith):
     env = dict(os.environ, KKTDD_ARITH=arith)
     r = subprocess.run([_exe("test_reference_cases")], env=env, capture_output=True, text=True, timeout=900)
     tail = r.stdout[-3000:]
+    out_dir = os.path.join(os.path.dirname(HERE), "gpurun_out")
+    if os.path.isdir(out_dir):  # keep the full case list next to the other GPU-run artefacts
+        open(os.path.join(out_dir, f"cpp_shim_{arith}.log"), "w").write(r.stdout + r.stderr)
     assert r.returncode == 0, tail + r.stderr[-1000:]
     last = r.stdout.strip().splitlines()[-1]
     assert "failed: 0 | assertions" in last and "| failed: 0" in last.split("assertions")[1], last

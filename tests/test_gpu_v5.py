@@ -136,3 +136,35 @@ def test_v5_fallback_against_strict(case):
     assert r.returncode == 0, r.stderr[-2000:]
     rel = float([x for x in r.stdout.splitlines() if x.startswith("REL")][0].split()[1])
     assert rel <= 1e-10, rel
+
+
+@pytest.mark.parametrize("env,label", [({"KKT_SWEEP_V3": "1"}, "v3 group chains (sweep_group.cu)"),
+                                       ({"KKT_SWEEP_V3": "1", "KKT_SWEEP_V2": "1"}, "v2 per-row chains (sweep_tma.cu)")],
+                         ids=["v3", "v2"])
+def test_small_grid_fallback_sweeps_against_strict(env, label):
+    """The older small-grid sweeps stay selectable (KKT_SWEEP_V3 / KKT_SWEEP_V2: the
+    FAST-parity bisection of scripts/bisect_fast_c1.py runs them): P^-1, RASQ and a
+    full solve against STRICT on a config-0-sized problem."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch; from paper_2305_04421_b200 import problems as P; "
+        "from paper_2305_04421_b200.solver import HeatKKT; "
+        "p = P.config(0); v = torch.from_numpy(P.random_kkt(p, 1)).cuda(); "
+        "f = HeatKKT(p, mode='fast'); s = HeatKKT(p, mode='strict'); B = p.block; "
+        "a = f.apply_P_inv(v).cpu().numpy(); b = s.apply_P_inv(v).cpu().numpy(); "
+        "print('REL', max(np.linalg.norm(a[k*B:(k+1)*B] - b[k*B:(k+1)*B]) / np.linalg.norm(b[k*B:(k+1)*B]) for k in range(3))); "
+        "a = f.apply_rasq(v[:B]).cpu().numpy(); b = s.apply_rasq(v[:B]).cpu().numpy(); "
+        "print('RASQ', np.linalg.norm(a - b) / np.linalg.norm(b)); "
+        "rhs = P.kkt_rhs(0, p); of = f.gmres_solve(rhs); os_ = s.gmres_solve(rhs); "
+        "print('ITS', of.iterations, os_.iterations); "
+        "print('SOL', float((of.solution - os_.solution).norm() / os_.solution.norm()))")
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=600, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = {x.split()[0]: x.split()[1:] for x in r.stdout.splitlines() if x and x.split()[0] in ("REL", "RASQ", "ITS", "SOL")}
+    assert float(out["REL"][0]) <= 1e-11, (label, out)
+    assert float(out["RASQ"][0]) <= 1e-11, (label, out)
+    assert abs(int(out["ITS"][0]) - int(out["ITS"][1])) <= 1, (label, out)
+    assert float(out["SOL"][0]) <= 1e-10, (label, out)

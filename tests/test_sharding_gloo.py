@@ -1,6 +1,6 @@
 """CPU, world_size 2 over gloo: the time-slab sharding plan and its exchanges.
 
-Two processes each own half of the subdomains (paper_2305_04421_b200.sharding,
+Two processes each own half of the subdomains (tests/sharding_plan.py,
 the host mirror of the CUDA context's slab logic) and exchange exactly what the
 device path exchanges: the u/w halo planes of K, the r plane of the sweep's
 shared node, the per-rank coarse columns (all-gather) and one partial per dot
@@ -57,9 +57,10 @@ def _worker(rank, world, port, q):
 
     import sys
     sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle.bindings import Orc
     from paper_2305_04421_b200 import problems as P
-    from paper_2305_04421_b200 import sharding as S
+    import sharding_plan as S
 
     try:
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
@@ -176,7 +177,7 @@ def test_two_rank_slab_exchanges_match_single_process():
 
 def test_plan_matches_partition():
     from paper_2305_04421_b200 import problems as P
-    from paper_2305_04421_b200 import sharding as S
+    import sharding_plan as S
     p = P.config(1)
     slabs = [S.plan(p, g, 8) for g in range(8)]
     assert [s.n0 for s in slabs] == [1 + 64 * g for g in range(8)]
