@@ -70,12 +70,12 @@ __global__ void __launch_bounds__(kThreads) scale_kernel(int64_t n, const double
 // Traffic: the algorithmic minimum is 3 reads + 3 writes per point.  A CTA owns
 // a kTX x kTY spatial tile (so the j-1 / j+1 rows of u and w are fetched once
 // per kTY rows, and merge in L1 with the neighbouring threads' own loads) and
-// marches over kTP consecutive time nodes: u_{n-1} stays in a register from the
+// marches over `tp` (<= kTPmax) consecutive time nodes: u_{n-1} stays in a register from the
 // previous node, and w_{n+1}, loaded for node n, is node n+1's own w value, so
 // the time neighbours cost no second pass over u and w.
-constexpr int kTX = 64, kTY = 4, kTP = 16;
+constexpr int kTX = 64, kTY = 4, kTPmax = 16;
 __global__ void __launch_bounds__(kTX * kTY) apply_K_kernel(Stencil s, int nt, int nsp, double ms,
-                                                            double oms, double dt,
+                                                            double oms, double dt, int tp,
                                                             const double* __restrict__ v,
                                                             double* __restrict__ out,
                                                             const double* __restrict__ bm,
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kTX * kTY) apply_K_kernel(Stencil s, int nt, i
   const double* u = v;
   const double* z = v + B;
   const double* w = v + 2 * B;
-  const int nA = blockIdx.z * kTP, nB = min(nt, nA + kTP);
+  const int nA = blockIdx.z * tp, nB = min(nt, nA + tp);
   // time neighbours carried across the march
   double up = 0.0, ww = w[int64_t(nA) * nsp + p];
   bool has_up = false;
@@ -222,8 +222,12 @@ void op_apply_K(Ctx* c, const double* v, double* out, const double* b_minus) {
     if (c->rank > 0) h.prev = hp;
     if (c->rank + 1 < c->nranks) h.next = hn;
   }
-  const dim3 gK((c->nx + kTX - 1) / kTX, (c->ny + kTY - 1) / kTY, (c->ntl + kTP - 1) / kTP);
-  KKT_LAUNCH(c, apply_K_kernel, gK, kTX * kTY, 0, c->A, c->ntl, c->nsp, c->ms, c->oms, c->dt, v, out,
+  // nodes per march: as long as the grid still fills the device several times over
+  const int tiles = ((c->nx + kTX - 1) / kTX) * ((c->ny + kTY - 1) / kTY);
+  int tp = kTPmax;
+  while (tp > 2 && int64_t(tiles) * ((c->ntl + tp - 1) / tp) < int64_t(kSmCount) * 32) tp >>= 1;
+  const dim3 gK((c->nx + kTX - 1) / kTX, (c->ny + kTY - 1) / kTY, (c->ntl + tp - 1) / tp);
+  KKT_LAUNCH(c, apply_K_kernel, gK, kTX * kTY, 0, c->A, c->ntl, c->nsp, c->ms, c->oms, c->dt, tp, v, out,
              b_minus, h.prev, h.next);
 }
 

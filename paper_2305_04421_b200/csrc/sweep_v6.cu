@@ -88,6 +88,12 @@ struct V6Params {
   int nind;           // L: groups [0, nind) have their own Phi rows, the rest share one converged set
   int gconv;          // U: groups [0, gconv) (from the top) share the converged set, the rest have their own
   int pass;           // v6_inner_kernel: row i of every group
+  // Low-latency row handoff (kLL): the last row of a group is published as 16-byte packets
+  // {value bits, tag}, one per (row, chain), slot [g][group step][KN][8]; consumers spin on the tag
+  // of the packets they need, so a handoff is one L2 write and one L2 read, with no release /
+  // acquire counter and no separate copy of y.  tag = seq | (group step + 1), seq new per launch.
+  ulonglong2* ll;
+  unsigned long long seq;
   long long* tim;    // KKT_V6_TIM: per-row clock64 phase sums of CTA 0 (6 per direction)
 };
 
@@ -443,7 +449,16 @@ __global__ void __launch_bounds__(kThr6, 1) v6_inner_kernel(V6Params P) {
 template <int KN>
 constexpr size_t chain_smem() { return sizeof(double) * (16 * KN + KN * kG + 8 * 128) + 3 * sizeof(uint64_t); }
 
-template <int KN, bool kUpper>
+__device__ __forceinline__ ulonglong2 ld_packet(const ulonglong2* p) {
+  ulonglong2 v;
+  asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];\n" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_packet(ulonglong2* p, double val, unsigned long long tag) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};\n" ::"l"(p), "l"(__double_as_longlong(val)), "l"(tag) : "memory");
+}
+
+template <int KN, bool kUpper, bool kLL>
 __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
   V6_DIMS
   extern __shared__ __align__(128) double sm6[];
@@ -478,7 +493,9 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
     }
   }
   auto Jof = [&](int gr) { return grow(kUpper, gr, gi, P.k, ny); };  // this CTA's row of group gr
-  auto emit = [&](int J, double v) {
+  auto emit = [&](int gr, int J, double v) {
+    if (kLL && last_row)
+      st_packet(P.ll + (size_t(g) * P.ngr + gr) * (KN * kG) + size_t(row) * kG + n, v, P.seq | (unsigned long long)(gr + 1));
     P.W0[widx<KN>(g, J, ny) + size_t(row) * kG + n] = v;
     if (out) out[size_t(J) * P.nx + row] = v;
     if (out2) out2[size_t(J) * P.nx + row] = v + g2;
@@ -486,7 +503,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
   // each output warp publishes its own stores (release after __syncwarp), so
   // no CTA-wide barrier sits between the stores and the count; 4 per CTA and row
   auto signal = [&]() {
-    if (outt && last_row) {
+    if (!kLL && outt && last_row) {
       __syncwarp();
       if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(cnt) : "memory");
     }
@@ -504,7 +521,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
   {  // group 0 has no inflow: its rows are the zero-inflow chain values
     const int J = Jof(0);
     if (J < 0) return;
-    if (outt) emit(J, __ldcg(P.W1 + widx<KN>(g, J, ny) + size_t(row) * kG + n));
+    if (outt) emit(0, J, __ldcg(P.W1 + widx<KN>(g, J, ny) + size_t(row) * kG + n));
     signal();
     if (P.ngr > 1 && Jof(1) >= 0 && threadIdx.x == 0) copy_a(1, Jof(1));
   }
@@ -519,7 +536,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
     const uint32_t par = uint32_t(idx - 1) & 1u;
     double cval = 0.0;
     if (outt) cval = __ldcg(P.W1 + widx<KN>(g, J, ny) + size_t(row) * kG + n);
-    if (threadIdx.x == 0) {
+    if (!kLL && threadIdx.x == 0) {
       const unsigned target = unsigned(idx) * kSl * 4;
       unsigned v;
       do {
@@ -532,14 +549,42 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
       tma_load(Bs, ysrc, sizeof(double) * KN * kG / 2, barB);
       tma_load(Bs + KN * kG / 2, ysrc + KN * kG / 2, sizeof(double) * KN * kG / 2, barB + 1);
     }
-    // the previous row's readers of red are done (costs nothing: every warp
-    // waits for thread 0's copy of y_{J-1} below anyway); one red buffer keeps
+    // the previous row's readers of red (and of Bs) are done; one red buffer keeps
     // the KN = 512 kernel at 2 CTAs per SM
     __syncthreads();
-    mbar_wait(barA, par);
-    if (tm) ts[2] = clock64();
-    mbar_wait(barB + (warp >> 2), par);  // this warp's half only: the other half may still be landing
-    if (tm) ts[3] = clock64();
+    if (kLL) {
+      // this warp's k-range of the previous group's last row: KN packets, KN / 32 per lane,
+      // 8 in flight; re-issue only the ones whose tag has not arrived yet
+      (void)Jp;
+      const unsigned long long tag = P.seq | (unsigned long long)idx;  // group step idx-1 -> tag idx
+      const ulonglong2* src = P.ll + (size_t(g) * P.ngr + (idx - 1)) * (KN * kG) + warp * KN + lane;
+      double* dstB = Bs + warp * KN + lane;
+#pragma unroll 1
+      for (int q0 = 0; q0 < KN / 32; q0 += 8) {
+        ulonglong2 v[8];
+        unsigned pending = 0xffu;
+        while (pending) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if ((pending >> u) & 1u) v[u] = ld_packet(src + (q0 + u) * 32);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (((pending >> u) & 1u) && v[u].y == tag) {
+              dstB[(q0 + u) * 32] = __longlong_as_double((long long)v[u].x);
+              pending &= ~(1u << u);
+            }
+        }
+      }
+      __syncwarp();
+      if (tm) ts[1] = ts[2] = clock64();
+      mbar_wait(barA, par);
+      if (tm) ts[3] = clock64();
+    } else {
+      mbar_wait(barA, par);
+      if (tm) ts[2] = clock64();
+      mbar_wait(barB + (warp >> 2), par);  // this warp's half only: the other half may still be landing
+      if (tm) ts[3] = clock64();
+    }
     double d[2][2][2] = {};
     const double* Aw = As + size_t(warp * kKW) * 64 + lane;
     const double* Bw = Bs + size_t(warp * kKW) * 4 * kG + bo;
@@ -564,7 +609,7 @@ __global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
       for (int e = 0; e < 2; ++e) red[warp * 128 + (mt * 32 + lane) * 2 + e] = d[0][mt][e] + d[1][mt][e];
     if (tm) ts[4] = clock64();
     __syncthreads();  // As / Bs consumed by every warp; red complete
-    if (outt) emit(J, cval + reduce8(red, threadIdx.x));
+    if (outt) emit(idx, J, cval + reduce8(red, threadIdx.x));
     if (tm) ts[5] = clock64();
     signal();
     if (idx + 1 < P.ngr && Jof(idx + 1) >= 0 && threadIdx.x == 0) copy_a(idx + 1, Jof(idx + 1));
@@ -644,9 +689,12 @@ void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   V6Params p = P;
+  p.seq = (++c->v6_seq) << 20;  // a fresh tag space per launch: packets of earlier launches never match
   void* args[] = {&p};
-  const void* fn = upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true>)
-                         : reinterpret_cast<const void*>(&v6_chain_kernel<KN, false>);
+  const void* fn = P.ll ? (upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true, true>)
+                                 : reinterpret_cast<const void*>(&v6_chain_kernel<KN, false, true>))
+                        : (upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true, false>)
+                                 : reinterpret_cast<const void*>(&v6_chain_kernel<KN, false, false>));
   KKT_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
   c->launches++;
 }
@@ -658,8 +706,10 @@ int chain_capacity() {
   static int cap = 0;
   if (!cap) {
     const int cs = int(chain_smem<KN>()), os = int(off_smem<KN>());
-    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
-    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
@@ -668,8 +718,13 @@ int chain_capacity() {
     KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
     KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
     int p0 = 0, p1 = 0;
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p0, v6_chain_kernel<KN, false>, kThr6, cs));
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, v6_chain_kernel<KN, true>, kThr6, cs));
+    int q0 = 0, q1 = 0;
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p0, v6_chain_kernel<KN, false, false>, kThr6, cs));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, v6_chain_kernel<KN, true, false>, kThr6, cs));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q0, v6_chain_kernel<KN, false, true>, kThr6, cs));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q1, v6_chain_kernel<KN, true, true>, kThr6, cs));
+    p0 = std::min(p0, q0);
+    p1 = std::min(p1, q1);
     int dev = 0, nsm = kSmCount;
     KKT_CUDA(cudaGetDevice(&dev));
     KKT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -913,6 +968,18 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.cnt = c->v6_cnt.p;
   P.k = c->v6_k;
   P.ngr = (ny + P.k - 1) / P.k;
+  static const bool ll_off = std::getenv("KKT_V6_LL") && std::atoi(std::getenv("KKT_V6_LL")) == 0;
+  P.ll = nullptr;
+  P.seq = 0;
+  if (!ll_off) {
+    const size_t npk = size_t(ngroups) * P.ngr * kn * kG;
+    if (c->v6_ll.n < npk) {
+      KKT_CUDA(cudaStreamSynchronize(c->stream));
+      c->v6_ll.alloc(npk);
+      KKT_CUDA(cudaMemsetAsync(c->v6_ll.p, 0, sizeof(ulonglong2) * npk, c->stream));  // tag 0 is never published
+    }
+    P.ll = c->v6_ll.p;
+  }
   P.nind = c->v6_nind;
   P.gconv = c->v6_gconv;
   P.pass = 0;

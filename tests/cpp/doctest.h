@@ -23,9 +23,10 @@ struct Approx {
   double value;
   double eps = 1e-12;
 };
+// doctest's rule: |a - b| < epsilon * (scale + max(|a|, |b|)) with scale = 1
 inline bool operator==(double a, const Approx& b) {
-  return std::abs(a - b.value) <= b.eps * (std::abs(a) > std::abs(b.value) ? std::abs(a) : std::abs(b.value)) ||
-         a == b.value;
+  const double m = std::abs(a) > std::abs(b.value) ? std::abs(a) : std::abs(b.value);
+  return std::abs(a - b.value) < b.eps * (1.0 + m) || a == b.value;
 }
 inline bool operator==(const Approx& b, double a) { return a == b; }
 
