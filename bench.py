@@ -175,7 +175,7 @@ class ClockSampler:
             self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "500"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -740,6 +740,9 @@ def run_pinv(args, ws, rank, local):
     # ---- timed region: K applications, CUDA events on the current stream, max over ranks
     k.set_phase_timing(True)
     l0 = k.launch_count()
+    prof = bool(os.environ.get("KKT_BENCH_PROFILE"))  # ncu --profile-from-start off: the timed region only
+    if prof:
+        torch.cuda.profiler.start()
     with ClockSampler(local) as clk:
         barrier(ws)
         torch.cuda.synchronize()
@@ -751,12 +754,38 @@ def run_pinv(args, ws, rank, local):
         ev1.record()
         torch.cuda.synchronize()
         barrier(ws)
+    if prof:
+        torch.cuda.profiler.stop()
     launches = k.launch_count() - l0
     ms_step = max_over_ranks(ev0.elapsed_time(ev1), ws) / args.steps
     phase_ms, phase_cnt = k.phase_times()
     k.set_phase_timing(False)
     value = unknowns / (ms_step / 1000.0)
     finite = bool(torch.isfinite(out).all().item())
+
+    # ---- K1 at this workload's vector size (not part of the step: P^-1 has no K; the stencil's
+    # roofline is reported beside the sweep's because north_star names both)
+    xk = torch.empty_like(v)
+    for _ in range(3):
+        k.apply_K(v, xk)
+    torch.cuda.synchronize()
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(10):
+        k.apply_K(v, xk)
+    s1.record()
+    torch.cuda.synchronize()
+    k_ms = s0.elapsed_time(s1) / 10
+    del xk
+    peak, peak_src = hbm_peak()
+    k_bytes = 6 * p.block * 8 // ws
+    stencil = {"kernel": "K1 apply_K_kernel (5-point space-time stencil, spatial tiles + time marching, stencil.cu)",
+               "bound": "hbm", "achieved": k_bytes / (k_ms / 1000.0) / 1e9, "peak": peak, "unit": "GB/s",
+               "frac": k_bytes / (k_ms / 1000.0) / 1e9 / peak, "peak_source": peak_src,
+               "traffic": ncu_summary("apply_K_dram_bytes_per_launch_c2"),
+               "algorithmic_bytes_per_launch": k_bytes, "avg_launch_ms": k_ms, "launches": 10,
+               "note": "timed outside the step (10 launches on the step's vectors)"}
     mem_gb = (torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]) / 1e9
 
     # ---- e2e through the host-buffer entry point (pinned memory)
@@ -801,6 +830,7 @@ def run_pinv(args, ws, rank, local):
         },
         "roofline": roofline,
         "roofline_secondary": rest,
+        "roofline_stencil": stencil,
         "e2e": {"value": unknowns / (ms_e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": ms_e2e, "wall_ms_per_step": 1000 * wall_e2e,
                 "steps": e2e_steps, "equals_device_result": same},

@@ -6,6 +6,7 @@
 // 5-point stencil the unfused mul/add costs nothing, and it makes K v bitwise
 // equal to apply_K (kkt.cpp:50-65) — SURVEY.md §8a-5.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ctx.cuh"
 
@@ -70,12 +71,13 @@ __global__ void __launch_bounds__(kThreads) scale_kernel(int64_t n, const double
 // Traffic: the algorithmic minimum is 3 reads + 3 writes per point.  A CTA owns
 // a kTX x kTY spatial tile (so the j-1 / j+1 rows of u and w are fetched once
 // per kTY rows, and merge in L1 with the neighbouring threads' own loads) and
-// marches over `tp` (<= kTPmax) consecutive time nodes: u_{n-1} stays in a register from the
+// marches over kTP (16 or 8) consecutive time nodes: u_{n-1} stays in a register from the
 // previous node, and w_{n+1}, loaded for node n, is node n+1's own w value, so
 // the time neighbours cost no second pass over u and w.
-constexpr int kTX = 64, kTY = 4, kTPmax = 16;
+constexpr int kTX = 64, kTY = 4;
+template <int kTP>
 __global__ void __launch_bounds__(kTX * kTY) apply_K_kernel(Stencil s, int nt, int nsp, double ms,
-                                                            double oms, double dt, int tp,
+                                                            double oms, double dt,
                                                             const double* __restrict__ v,
                                                             double* __restrict__ out,
                                                             const double* __restrict__ bm,
@@ -89,7 +91,7 @@ __global__ void __launch_bounds__(kTX * kTY) apply_K_kernel(Stencil s, int nt, i
   const double* u = v;
   const double* z = v + B;
   const double* w = v + 2 * B;
-  const int nA = blockIdx.z * tp, nB = min(nt, nA + tp);
+  const int nA = blockIdx.z * kTP, nB = min(nt, nA + kTP);
   // time neighbours carried across the march
   double up = 0.0, ww = w[int64_t(nA) * nsp + p];
   bool has_up = false;
@@ -222,13 +224,19 @@ void op_apply_K(Ctx* c, const double* v, double* out, const double* b_minus) {
     if (c->rank > 0) h.prev = hp;
     if (c->rank + 1 < c->nranks) h.next = hn;
   }
-  // nodes per march: as long as the grid still fills the device several times over
+  // nodes per march (compile-time so that the march unrolls): 16, or 8 when 16 would leave the grid
+  // with too few CTAs to fill the device several times over (config 1)
   const int tiles = ((c->nx + kTX - 1) / kTX) * ((c->ny + kTY - 1) / kTY);
-  int tp = kTPmax;
-  while (tp > 2 && int64_t(tiles) * ((c->ntl + tp - 1) / tp) < int64_t(kSmCount) * 32) tp >>= 1;
+  static const int force_tp = std::getenv("KKT_K1_TP") ? std::atoi(std::getenv("KKT_K1_TP")) : 0;
+  const bool small = force_tp ? force_tp < 16 : int64_t(tiles) * ((c->ntl + 15) / 16) < int64_t(kSmCount) * 32;
+  const int tp = small ? 8 : 16;
   const dim3 gK((c->nx + kTX - 1) / kTX, (c->ny + kTY - 1) / kTY, (c->ntl + tp - 1) / tp);
-  KKT_LAUNCH(c, apply_K_kernel, gK, kTX * kTY, 0, c->A, c->ntl, c->nsp, c->ms, c->oms, c->dt, tp, v, out,
-             b_minus, h.prev, h.next);
+  if (small)
+    KKT_LAUNCH(c, apply_K_kernel<8>, gK, kTX * kTY, 0, c->A, c->ntl, c->nsp, c->ms, c->oms, c->dt, v, out,
+               b_minus, h.prev, h.next);
+  else
+    KKT_LAUNCH(c, apply_K_kernel<16>, gK, kTX * kTY, 0, c->A, c->ntl, c->nsp, c->ms, c->oms, c->dt, v, out,
+               b_minus, h.prev, h.next);
 }
 
 void op_pinv_uz(Ctx* c, const double* r, double* out) {

@@ -458,8 +458,14 @@ __device__ __forceinline__ void st_packet(ulonglong2* p, double val, unsigned lo
   asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};\n" ::"l"(p), "l"(__double_as_longlong(val)), "l"(tag) : "memory");
 }
 
+// co-resident CTAs per SM the register budget must allow (shared memory would allow 3 / 2 / 1 at
+// KN = 256 / 512 / 1024); without it the KN = 512 packet-handoff kernel takes 130 registers, one
+// CTA per SM, and config 2's 256 CTAs run in two waves (measured: P^-1 170 -> 200 ms)
+template <int KN>
+constexpr int chain_min_blocks() { return KN <= 512 ? 2 : 1; }  // 3 at KN = 256 spills (80 registers)
+
 template <int KN, bool kUpper, bool kLL>
-__global__ void __launch_bounds__(kThr6, 1) v6_chain_kernel(V6Params P) {
+__global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel(V6Params P) {
   V6_DIMS
   extern __shared__ __align__(128) double sm6[];
   double* As = sm6;                 // [ks KN/4][mt 2][lane 32]
@@ -968,10 +974,14 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.cnt = c->v6_cnt.p;
   P.k = c->v6_k;
   P.ngr = (ny + P.k - 1) / P.k;
-  static const bool ll_off = std::getenv("KKT_V6_LL") && std::atoi(std::getenv("KKT_V6_LL")) == 0;
+  // packet handoff: measured ahead of the release counter at KN = 256 (config 3: 150 -> 128 ms);
+  // at KN = 1024 a warp's 1024 packets take four dependent batches and the counter + bulk copy wins
+  // (config-4 slab 164 vs 181 ms).  KKT_V6_LL=0/1 forces the choice.
+  static const char* ll_env = std::getenv("KKT_V6_LL");
+  const bool ll_on = ll_env ? std::atoi(ll_env) != 0 : kn <= 512;
   P.ll = nullptr;
   P.seq = 0;
-  if (!ll_off) {
+  if (ll_on) {
     const size_t npk = size_t(ngroups) * P.ngr * kn * kG;
     if (c->v6_ll.n < npk) {
       KKT_CUDA(cudaStreamSynchronize(c->stream));
