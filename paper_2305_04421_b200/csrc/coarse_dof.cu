@@ -279,6 +279,57 @@ void h2d(Ctx* c, DBuf<T>& d, const std::vector<T>& h) {
 
 }  // namespace
 
+bool perdof_kron_wanted(const Ctx* c, double dense_bytes);                                    // coarse_kron.cu
+void build_coarse_perdof_kron(Ctx* c, const std::vector<std::array<int, 2>>& col_start);      // coarse_kron.cu
+void perdof_solve_kron(Ctx* c, double* cdev);                                                  // coarse_kron.cu
+
+// per-column / per-node tables of restrict and prolong (column ids of a (subdomain, kind) are
+// dof-contiguous), and the work vectors
+void perdof_tables(Ctx* c, const std::vector<std::array<int, 2>>& col_start) {
+  (void)col_start;
+  const int Nd = c->Nd, nsp = c->nsp, Nt = c->Nt, dim = c->cdim;
+  c->m_max = 0;
+  for (int s = 0; s < Nd; ++s) c->m_max = std::max(c->m_max, c->owned[s].count());
+  std::vector<int> cf(dim), cc(dim);
+  std::vector<double> cphi(size_t(dim / nsp) * c->m_max, 0.0);
+  std::vector<int> ncol(2 * size_t(Nt), -1);
+  std::vector<double> nphi(2 * size_t(Nt), 0.0);
+  for (int ci = 0; ci < dim; ++ci) {
+    const CoarseColumn& col = c->cols[ci];
+    const auto& phi = col.kind == 0 ? c->phi_const[col.s] : c->phi_lin[col.s];
+    cf[ci] = c->owned[col.s].first;
+    cc[ci] = c->owned[col.s].count();
+    if (col.dof == 0) {
+      for (int k = 0; k < cc[ci]; ++k) {
+        cphi[size_t(ci / nsp) * c->m_max + k] = phi[k];
+        const int n = cf[ci] + k;
+        ncol[2 * (n - 1) + col.kind] = ci;
+        nphi[2 * (n - 1) + col.kind] = phi[k];
+      }
+    }
+  }
+  c->col_lo = dim;
+  c->col_hi = 0;
+  for (int ci = 0; ci < dim; ++ci) {
+    const int sd = c->cols[ci].s;
+    if (sd >= c->s0 && sd < c->s0 + c->ndl) {
+      c->col_lo = std::min(c->col_lo, ci);
+      c->col_hi = std::max(c->col_hi, ci + 1);
+    }
+  }
+  if (c->col_hi < c->col_lo) c->col_lo = c->col_hi = 0;
+  h2d(c, c->col_first, cf);
+  h2d(c, c->col_count, cc);
+  h2d(c, c->col_phi, cphi);
+  h2d(c, c->node_col, ncol);
+  h2d(c, c->node_phi, nphi);
+  c->cvec.alloc(dim);
+  c->call.alloc(size_t(dim) * c->nranks);
+  c->gam.alloc(Nt + 2);
+  c->has_coarse = true;
+  c->perdof = true;
+}
+
 void build_coarse_perdof(Ctx* c) {
   const int Nd = c->Nd, nsp = c->nsp, Nt = c->Nt;
   c->phi_const.clear();
@@ -312,6 +363,10 @@ void build_coarse_perdof(Ctx* c) {
   }
   const double win_bytes = 3.0 * 8.0 * double(nsp) * wmax * nsp;
   const double dense_bytes = 8.0 * double(dim) * dim;
+  if (perdof_kron_wanted(c, win_bytes + dense_bytes)) {  // FAST beyond desk scale: S0 from its Kronecker structure
+    build_coarse_perdof_kron(c, col_start);
+    return;
+  }
   if (win_bytes + dense_bytes > 24e9)
     throw Error(KKT_EUNSUPPORTED,
                 "per-dof coarse space too large for the device build (dim " + std::to_string(dim) +
@@ -401,47 +456,7 @@ void build_coarse_perdof(Ctx* c) {
     throw Error(KKT_ECONFIG,
                 "coarse operator (per-dof variant) is rank deficient: banded LU: pivot below tolerance "
                 "at index " + std::to_string(hst), hst);
-  // ---- per-column / per-node tables (column ids of a (subdomain, kind) are dof-contiguous)
-  c->m_max = 0;
-  for (int s = 0; s < Nd; ++s) c->m_max = std::max(c->m_max, c->owned[s].count());
-  std::vector<int> cf(dim), cc(dim);
-  std::vector<double> cphi(size_t(dim / nsp) * c->m_max, 0.0);
-  std::vector<int> ncol(2 * size_t(Nt), -1);
-  std::vector<double> nphi(2 * size_t(Nt), 0.0);
-  for (int ci = 0; ci < dim; ++ci) {
-    const CoarseColumn& col = c->cols[ci];
-    const auto& phi = col.kind == 0 ? c->phi_const[col.s] : c->phi_lin[col.s];
-    cf[ci] = c->owned[col.s].first;
-    cc[ci] = c->owned[col.s].count();
-    if (col.dof == 0) {
-      for (int k = 0; k < cc[ci]; ++k) {
-        cphi[size_t(ci / nsp) * c->m_max + k] = phi[k];
-        const int n = cf[ci] + k;
-        ncol[2 * (n - 1) + col.kind] = ci;
-        nphi[2 * (n - 1) + col.kind] = phi[k];
-      }
-    }
-  }
-  c->col_lo = dim;
-  c->col_hi = 0;
-  for (int ci = 0; ci < dim; ++ci) {
-    const int sd = c->cols[ci].s;
-    if (sd >= c->s0 && sd < c->s0 + c->ndl) {
-      c->col_lo = std::min(c->col_lo, ci);
-      c->col_hi = std::max(c->col_hi, ci + 1);
-    }
-  }
-  if (c->col_hi < c->col_lo) c->col_lo = c->col_hi = 0;
-  h2d(c, c->col_first, cf);
-  h2d(c, c->col_count, cc);
-  h2d(c, c->col_phi, cphi);
-  h2d(c, c->node_col, ncol);
-  h2d(c, c->node_phi, nphi);
-  c->cvec.alloc(dim);
-  c->call.alloc(size_t(dim) * c->nranks);
-  c->gam.alloc(Nt + 2);
-  c->has_coarse = true;
-  c->perdof = true;
+  perdof_tables(c, col_start);
 }
 
 void perdof_restrict(Ctx* c, const double* r, double* cdev) {
@@ -455,6 +470,7 @@ void perdof_restrict(Ctx* c, const double* r, double* cdev) {
 }
 
 void perdof_solve(Ctx* c, double* cdev) {
+  if (c->kron) return perdof_solve_kron(c, cdev);
   const size_t smem = sizeof(double) * size_t(c->cdim);
   static bool attr = false;
   if (!attr) {

@@ -155,6 +155,10 @@ struct Ctx {
   int cb_kl = 0, cb_kuf = 0, cb_ld = 0;
   DBuf<double> cb_ab;             // factor, entry(i,j) at j*cb_ld + i-j+cb_kuf
   DBuf<int> cb_piv;
+  // per-dof variant beyond desk scale (coarse_kron.cu): S0 in Ahat's eigenbasis, banded LDL^T per mode
+  bool kron = false;
+  int kron_D = 0;
+  DBuf<double> kron_w, kron_tmp;
   // per-node coarse tables: for node n (1..Nt): column ids and profile values
   DBuf<int> node_col;             // 2 per node: column of (owner, kind 0/1), -1 if absent
   DBuf<double> node_phi;          // 2 per node

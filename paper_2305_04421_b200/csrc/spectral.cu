@@ -248,6 +248,9 @@ void build_spectral(Ctx* c) {
   KKT_CUDA(cudaStreamSynchronize(c->stream));
 }
 
+// P planes (ny x nx each, contiguous): out = Sy X Sx per plane; S is its own inverse.
+void spectral_transform(Ctx* c, const double* in, double* tmp, double* out, int P) { transform(c, in, tmp, out, P); }
+
 // out = RASQ(r) or, fused, RASQ(r - Shat y_c) + y_c (see sweep.cu rasq_apply).
 void spectral_rasq(Ctx* c, const double* r, const double* halo_prev, double* out, bool fused) {
   const size_t B = size_t(c->B);

@@ -238,21 +238,26 @@ __global__ void __launch_bounds__(kThr6, 1) v6_off_kernel(V6Params P) {
 // in registers and reduce it through shared memory (double-buffered by slice
 // parity, one named barrier per slice) in a fixed order.
 constexpr int kOffRing = 2;      // ring slots
-constexpr int kOffCk = 64;       // k-steps per chunk (32 KB)
 constexpr int kOffThr = 288;     // 8 consumer warps + 1 producer warp
-template <int KN>
+// NG chain groups share one pass over the triangle (their block vectors staged side by side), so
+// 8 chain groups (config 2) stream it twice instead of four times; the ring chunk shrinks to keep
+// the CTA under the shared-memory limit.
+template <int NG>
+constexpr int off_ck() { return NG == 2 ? 64 : 32; }  // k-steps per chunk (32 KB / 16 KB)
+template <int KN, int NG>
 constexpr size_t off2_smem() {
-  return sizeof(double) * (2 * KN * kG + kOffRing * kOffCk * 64 + 2 * 8 * 256) + 8 * sizeof(uint64_t);
+  return sizeof(double) * (NG * KN * kG + kOffRing * off_ck<NG>() * 64 + 2 * 8 * NG * 128) + 8 * sizeof(uint64_t);
 }
 
-template <int KN, bool kUpper>
+template <int KN, bool kUpper, int NG>
 __global__ void __launch_bounds__(kOffThr, 1) v6_off2_kernel(V6Params P) {
   V6_DIMS
+  constexpr int CK = off_ck<NG>();
   extern __shared__ __align__(128) double so[];
-  double* Bs = so;                               // [2][KN][8]
-  double* ring = Bs + 2 * KN * kG;               // [slot][kOffCk][64]
-  double* red = ring + kOffRing * kOffCk * 64;   // [slice parity 2][warp 8][256]
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * 8 * 256);
+  double* Bs = so;                               // [NG][KN][8]
+  double* ring = Bs + NG * KN * kG;              // [slot][CK][64]
+  double* red = ring + kOffRing * CK * 64;       // [slice parity 2][warp 8][NG * 128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * 8 * NG * 128);
   uint64_t* empty = full + kOffRing;
   uint64_t* barB = empty + kOffRing;
   uint64_t* bfree = barB + 1;
@@ -273,25 +278,26 @@ __global__ void __launch_bounds__(kOffThr, 1) v6_off2_kernel(V6Params P) {
       int it = 0, item = 0;
       for (int J = blockIdx.x; J < P.ny; J += gridDim.x) {
         const double* TJ = T + size_t(oprow(J, P.jstar)) * kSl * kKS * 64;
-        for (int gp = 0; gp < P.ngroups; gp += 2, ++item) {
+        for (int gp = 0; gp < P.ngroups; gp += NG, ++item) {
           if (item > 0) mbar_wait(bfree, uint32_t(item - 1) & 1u);
-          const int g1 = gp + 1 < P.ngroups ? gp + 1 : gp;  // a missing partner reads gp (outputs not written)
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tma::smem_u32(barB)),
-                       "r"(uint32_t(sizeof(double) * 2 * KN * kG))
+                       "r"(uint32_t(sizeof(double) * NG * KN * kG))
                        : "memory");
           const uint32_t vb = uint32_t(sizeof(double) * KN * kG);
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                           tma::smem_u32(Bs)), "l"(P.W0 + widx<KN>(gp, J, P.ny)), "r"(vb), "r"(tma::smem_u32(barB))
-                       : "memory");
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                           tma::smem_u32(Bs + KN * kG)), "l"(P.W0 + widx<KN>(g1, J, P.ny)), "r"(vb), "r"(tma::smem_u32(barB))
-                       : "memory");
+#pragma unroll
+          for (int g = 0; g < NG; ++g) {
+            const int gs = gp + g < P.ngroups ? gp + g : gp;  // a missing group reads gp (its outputs are not written)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             tma::smem_u32(Bs + size_t(g) * KN * kG)), "l"(P.W0 + widx<KN>(gs, J, P.ny)), "r"(vb),
+                         "r"(tma::smem_u32(barB))
+                         : "memory");
+          }
           for (int s = 0; s < kSl; ++s) {
             const int ks0 = kUpper ? 4 * s : 0, ks1 = kUpper ? kKS : 4 * s + 4;
-            for (int kb = ks0; kb < ks1; kb += kOffCk, ++it) {
-              const int slot = it % kOffRing, len = min(kOffCk, ks1 - kb);
+            for (int kb = ks0; kb < ks1; kb += CK, ++it) {
+              const int slot = it % kOffRing, len = min(CK, ks1 - kb);
               if (it >= kOffRing) mbar_wait(&empty[slot], uint32_t(it / kOffRing - 1) & 1u);
-              tma_load(ring + size_t(slot) * kOffCk * 64, TJ + (size_t(s) * kKS + kb) * 64,
+              tma_load(ring + size_t(slot) * CK * 64, TJ + (size_t(s) * kKS + kb) * 64,
                        uint32_t(sizeof(double) * 64 * len), &full[slot]);
             }
           }
@@ -303,47 +309,48 @@ __global__ void __launch_bounds__(kOffThr, 1) v6_off2_kernel(V6Params P) {
   const int bo = (lane & 3) * kG + (lane >> 2);
   int it = 0, item = 0, sl = 0;
   for (int J = blockIdx.x; J < P.ny; J += gridDim.x) {
-    for (int gp = 0; gp < P.ngroups; gp += 2, ++item) {
+    for (int gp = 0; gp < P.ngroups; gp += NG, ++item) {
       mbar_wait(barB, uint32_t(item) & 1u);
       for (int s = 0; s < kSl; ++s, ++sl) {
         const int ks0 = kUpper ? 4 * s : 0, ks1 = kUpper ? kKS : 4 * s + 4;
-        double d[2][2][2] = {};
-        for (int kb = ks0; kb < ks1; kb += kOffCk, ++it) {
-          const int slot = it % kOffRing, len = min(kOffCk, ks1 - kb);
+        double d[NG][2][2] = {};
+        for (int kb = ks0; kb < ks1; kb += CK, ++it) {
+          const int slot = it % kOffRing, len = min(CK, ks1 - kb);
           mbar_wait(&full[slot], uint32_t(it / kOffRing) & 1u);
-          const double* R = ring + size_t(slot) * kOffCk * 64 + lane;
+          const double* R = ring + size_t(slot) * CK * 64 + lane;
 #pragma unroll
-          for (int q = 0; q < kOffCk / 8; ++q) {
+          for (int q = 0; q < CK / 8; ++q) {
             const int u = warp + 8 * q;
             if (u < len) {
               const double a0 = R[u * 64], a1 = R[u * 64 + 32];
-              const double b0 = Bs[(4 * (kb + u)) * kG + bo];
-              const double b1 = Bs[KN * kG + (4 * (kb + u)) * kG + bo];
-              dmma6(d[0][0][0], d[0][0][1], a0, b0);
-              dmma6(d[0][1][0], d[0][1][1], a1, b0);
-              dmma6(d[1][0][0], d[1][0][1], a0, b1);
-              dmma6(d[1][1][0], d[1][1][1], a1, b1);
+#pragma unroll
+              for (int g = 0; g < NG; ++g) {
+                const double bg = Bs[size_t(g) * KN * kG + (4 * (kb + u)) * kG + bo];
+                dmma6(d[g][0][0], d[g][0][1], a0, bg);
+                dmma6(d[g][1][0], d[g][1][1], a1, bg);
+              }
             }
           }
           __syncwarp();
           if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tma::smem_u32(&empty[slot])) : "memory");
         }
-        double* rw = red + size_t(sl & 1) * 8 * 256 + warp * 256;
+        double* rw = red + size_t(sl & 1) * 8 * NG * 128 + warp * NG * 128;
 #pragma unroll
-        for (int g = 0; g < 2; ++g)
+        for (int g = 0; g < NG; ++g)
 #pragma unroll
           for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
             for (int e = 0; e < 2; ++e) rw[g * 128 + (mt * 32 + lane) * 2 + e] = d[g][mt][e];
         asm volatile("bar.sync 1, 256;\n" ::: "memory");
-        {
-          const int t = threadIdx.x, g = t >> 7, r = t & 127;
+#pragma unroll
+        for (int h = 0; h < NG / 2; ++h) {
+          const int t = threadIdx.x, g = 2 * h + (t >> 7), r = t & 127;
           int m, n;
           slice_coords(r, m, n);
-          const double* rr = red + size_t(sl & 1) * 8 * 256 + g * 128 + r;
+          const double* rr = red + size_t(sl & 1) * 8 * NG * 128 + g * 128 + r;
           double v = 0.0;
 #pragma unroll
-          for (int w = 0; w < 8; ++w) v += rr[w * 256];
+          for (int w = 0; w < 8; ++w) v += rr[w * NG * 128];
           if (gp + g < P.ngroups) P.W1[widx<KN>(gp + g, J, P.ny) + size_t(16 * s + m) * kG + n] = v;
         }
       }
@@ -720,9 +727,14 @@ int chain_capacity() {
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
-    const int os2 = int(off2_smem<KN>());
-    KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
-    KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
+    const int os2 = int(off2_smem<KN, 2>());
+    KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
+    KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
+    if constexpr (KN <= 512) {
+      const int os4 = int(off2_smem<KN, 4>());
+      KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, os4));
+      KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, os4));
+    }
     int p0 = 0, p1 = 0;
     int q0 = 0, q1 = 0;
     KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p0, v6_chain_kernel<KN, false, false>, kThr6, cs));
@@ -770,10 +782,23 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
         else
           KKT_LAUNCH(c, (v6_off_kernel<KN, false>), og, kThr6, off_smem<KN>(), P);
       } else {
-        if (up)
-          KKT_LAUNCH(c, (v6_off2_kernel<KN, true>), og, kOffThr, off2_smem<KN>(), P);
-        else
-          KKT_LAUNCH(c, (v6_off2_kernel<KN, false>), og, kOffThr, off2_smem<KN>(), P);
+        static const bool ng2 = std::getenv("KKT_V6_OFF_NG2") != nullptr;  // testing: two groups per triangle pass
+        bool four = false;
+        if constexpr (KN <= 512) four = ngroups > 2 && !ng2;
+        if constexpr (KN <= 512) {
+          if (four) {
+            if (up)
+              KKT_LAUNCH(c, (v6_off2_kernel<KN, true, 4>), og, kOffThr, (off2_smem<KN, 4>()), P);
+            else
+              KKT_LAUNCH(c, (v6_off2_kernel<KN, false, 4>), og, kOffThr, (off2_smem<KN, 4>()), P);
+          }
+        }
+        if (!four) {
+          if (up)
+            KKT_LAUNCH(c, (v6_off2_kernel<KN, true, 2>), og, kOffThr, (off2_smem<KN, 2>()), P);
+          else
+            KKT_LAUNCH(c, (v6_off2_kernel<KN, false, 2>), og, kOffThr, (off2_smem<KN, 2>()), P);
+        }
       }
       for (int i = 1; i < P.k; ++i) {  // zero-inflow chains inside the groups, every group at once
         P.pass = i;

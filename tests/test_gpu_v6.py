@@ -32,6 +32,9 @@ CASES = [
     (700, 12, 9, 3, "one-level"),     # 3 chains, one-level RASQ
     (520, 5, 40, 20, "two-level"),    # 20 chains: 3 groups, two chain-kernel waves
     (1024, 3, 16, 16, "two-level"),   # config 4's per-GPU shape at G = 8: 16 chains, m = 1
+    (400, 7, 56, 28, "two-level"),    # nx = 399 on 512-blocks, 28 chains: 4 groups in one off-chain pass, the last half full
+    (320, 5, 40, 40, "one-level"),    # 40 chains: 5 groups, off-chain passes of 4 + 1
+    (200, 23, 8, 4, "two-level"),     # nx = 199 on 256-blocks; ny = 23 is not a multiple of the chain's row grouping
 ]
 
 
@@ -198,3 +201,38 @@ def test_block_lu_grid_kernel_bitwise(tmp_path):
     _run_sub(code.replace("sys.argv[1]", repr(a)), {}, tmp_path)
     _run_sub(code.replace("sys.argv[1]", repr(b)), {"KKT_LU_SINGLE": "1"}, tmp_path)
     assert np.array_equal(np.load(a), np.load(b))
+
+
+@pytest.mark.parametrize("env", [{"KKT_V6_K": "1"}, {"KKT_V6_K": "3"}, {"KKT_V6_K": "8"},
+                                 {"KKT_V6_K": "5", "KKT_V6_LL": "0"}, {"KKT_V6_LL": "0"}, {"KKT_V6_OFF_NG2": "1"}],
+                         ids=["k1", "k3", "k8", "k5_counter", "counter", "off_ng2"])
+def test_v6_grouping_and_handoff_variants_against_strict(env):
+    """The chain's k-row grouping (propagator products over groups of k block rows, zero-inflow
+    chains inside the groups) and its two row handoffs (low-latency packets / release counter) are
+    re-associations of the same substitution: every variant agrees with STRICT to 1e-10, on a
+    256-block grid whose ny is not a multiple of k and on a tall 512-block grid where the block
+    recursion converges inside the grid (rows past jstar share one operator set, so the converged
+    propagator sets are exercised).  Subprocesses: the switches are read once per process."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch; from paper_2305_04421_b200 import problems as P; "
+        "from paper_2305_04421_b200.solver import HeatKKT\n"
+        "for (Nx, Ny, Nt, Nd, nu) in ((180, 38, 8, 4, 0.1), (300, 330, 4, 2, 1e-3)):\n"
+        "    p = P.Problem(Lx=1.0, Ly=1.0, Nx=Nx, Ny=Ny, Nt=Nt, Nd=Nd, nu=nu, omega=1e-2, "
+        "precond='two-level', coarse_variant='scalar', tol=1e-8, restart=20)\n"
+        "    v = torch.from_numpy(P.random_kkt(p, 1)).cuda()\n"
+        "    f = HeatKKT(p, mode='fast'); a = f.apply_P_inv(v).clone(); a2 = f.apply_P_inv(v)\n"
+        "    b = HeatKKT(p, mode='strict').apply_P_inv(v)\n"
+        "    B = p.block\n"
+        "    print('REL', max(float((a[k*B:(k+1)*B] - b[k*B:(k+1)*B]).norm() / b[k*B:(k+1)*B].norm()) for k in range(3)), "
+        "'DET', bool(torch.equal(a, a2)))\n")
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, KKT_V6_TIM="1", **env), capture_output=True,
+                       text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rows = [x.split() for x in r.stdout.splitlines() if x.startswith("REL")]
+    assert len(rows) == 2, r.stdout
+    for row in rows:
+        assert float(row[1]) <= 1e-10 and row[3] == "True", (env, rows)
+    if "KKT_V6_K" in env and env["KKT_V6_K"] != "1":
+        assert f"v6 grouping k {env['KKT_V6_K']}:" in r.stderr, r.stderr[-1500:]
