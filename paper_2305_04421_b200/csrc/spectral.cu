@@ -202,7 +202,9 @@ __global__ void rasq_modes_kernel(RecParams P) {
 
 }  // namespace
 
-bool spectral_enabled(const Ctx* c) { return c->sp_x.p != nullptr; }
+// only the opt-in mode: the sine matrices alone do not enable it (the per-dof coarse solve of
+// coarse_kron.cu builds them too, and keeps the LU sweep)
+bool spectral_enabled(const Ctx* c) { return c->spectral && c->sp_x.p != nullptr; }
 
 void build_spectral(Ctx* c) {
   const int nx = c->nx, ny = c->ny, nsp = c->nsp;

@@ -219,8 +219,10 @@ def test_per_dof_two_level_at_config1():
     out = k.gmres_solve(b)
     assert out.converged and out.true_final_relres <= 1.5 * p.tol
     assert out.iterations < 44, out.iterations
-    scal = HeatKKT(P.config(1), mode="fast").gmres_solve(b)
-    B = p.block
-    xs, xp = scal.solution, out.solution
-    for i in range(3):  # two tol-1e-8 solutions of the same system
-        assert float((xp[i * B:(i + 1) * B] - xs[i * B:(i + 1) * B]).norm() / xs[i * B:(i + 1) * B].norm()) <= 1e-5
+    # the solution solves the KKT system (independent residual evaluation), and the sweep is the
+    # LU block substitution, not the opt-in spectral one (the Kronecker solve shares its sine matrices)
+    assert k.kkt_residual(out.solution, b) <= 1.5 * p.tol
+    k.set_phase_timing(True)
+    k.apply_P_inv(torch.from_numpy(b).cuda())
+    ms, cnt = k.phase_times()
+    assert cnt[3] == 1 and ms[3] > 3.0, (ms, cnt)   # one v4 sweep (~4.2 ms); the spectral one takes ~1 ms
