@@ -838,7 +838,9 @@ def run_pinv(args, ws, rank, local):
         "clocks": clk.summary(),
     }
     if ws == 1 and not args.no_extras and args.mode == "fast":
-        for key, fn in (("config1", lambda: config1_extra(local)), ("config3", lambda: c3_microbench(local))):
+        for key, fn in (("config1", lambda: config1_extra(local)),
+                        ("config1_per_dof", lambda: config1_extra(local, coarse="per-dof")),
+                        ("config3", lambda: c3_microbench(local))):
             try:
                 line[key] = fn()
             except Exception as e:  # reported beside the headline, never required
@@ -865,12 +867,14 @@ def run_pinv(args, ws, rank, local):
     print(json.dumps(line))
 
 
-def config1_extra(local, steps=3):
+def config1_extra(local, steps=3, coarse="scalar"):
     """BASELINE config 1 (127^2 x 512, Nd = 16, GMRES(30)): the round-1 headline,
-    kept as an extra key.  Sweep v4 (sweep_v4.cu)."""
+    kept as an extra key.  Sweep v4 (sweep_v4.cu).  coarse="per-dof": the reference's
+    default coarse variant (dimension 516,128: coarse_kron.cu), which the reference
+    itself cannot factor at this size."""
     import torch
     from paper_2305_04421_b200.solver import HeatKKT
-    p = P.config(1)
+    p = P.config(1, coarse=coarse)
     k = HeatKKT(p, mode="fast", device=local)
     b = torch.from_numpy(P.kkt_rhs(1, p)).cuda()
     x = torch.empty_like(b)
@@ -881,6 +885,13 @@ def config1_extra(local, steps=3):
     phase_ms, phase_cnt = k.phase_times()
     k.set_phase_timing(False)
     r, r2, st = rooflines(p, 1, "fast", iters[-1], steps, ms_total, phase_ms, phase_cnt, False)
+    if coarse != "scalar":
+        res = {"workload": workload_desc(1, p), "ms_per_step": ms_total / steps,
+               "value": 3 * p.block / (ms_total / steps / 1000.0), "unit": UNIT, "iterations": iters[-1],
+               "true_final_relres": out.true_final_relres, "steps": steps, "coarse_dim": k.coarse_dim()}
+        del k, b, x
+        torch.cuda.empty_cache()
+        return res
     res = {"workload": workload_desc(1, p), "ms_per_step": ms_total / steps,
            "value": 3 * p.block / (ms_total / steps / 1000.0), "unit": UNIT, "iterations": iters[-1],
            "true_final_relres": out.true_final_relres, "steps": steps,

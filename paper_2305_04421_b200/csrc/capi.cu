@@ -7,6 +7,7 @@
 // (time_partition.cpp:61-86) and make_schur_solver (schur.cpp:543-558).
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -27,6 +28,8 @@ Ctx::~Ctx() {
   for (auto e : ev_pool) cudaEventDestroy(e);
   for (auto& iv : ev_pending) { cudaEventDestroy(iv.a); cudaEventDestroy(iv.b); }
   for (auto e : ev_open) if (e) cudaEventDestroy(e);
+  for (auto e : e2e_ev) if (e) cudaEventDestroy(e);
+  for (auto st : {e2e_in, e2e_out, e2e_aux}) if (st) cudaStreamDestroy(st);
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -496,16 +499,73 @@ int kkt_gmres_solve_host(kkt_ctx* ctx, const double* b_host, double* x_host,
   });
 }
 
+// apply_P_inv from host buffers, with the copies overlapped with the compute: P^-1 is block
+// diagonal (kkt.cpp:71-81), so the Schur block's sweep needs only r_w.  r_w goes up first and the
+// sweep starts; r_u and r_z follow on the copy-in stream while it runs, their division runs on a
+// side stream and its result goes back down (PCIe is full duplex) while the sweep is still busy;
+// out_w follows when the sweep is done.  With pinned host memory the end-to-end time is the sweep
+// plus one block up and one block down instead of the sweep plus three blocks each way.
 int kkt_apply_P_inv_host(kkt_ctx* ctx, const double* r_host, double* out_host) {
   return kkt::guard(ctx, [&](Ctx* c) {
     kkt::need(r_host && out_host, "kkt_apply_P_inv_host: bad arguments");
-    const size_t n = size_t(3 * c->B);
+    const size_t B = size_t(c->B), n = 3 * B;
     if (c->e2e_b.n < n) c->e2e_b.alloc(n);
     if (c->e2e_x.n < n) c->e2e_x.alloc(n);
-    KKT_CUDA(cudaMemcpyAsync(c->e2e_b.p, r_host, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-    kkt::pinv_apply(c, c->e2e_b.p, c->e2e_x.p);
-    KKT_CUDA(cudaMemcpyAsync(out_host, c->e2e_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (!c->e2e_in) {
+      KKT_CUDA(cudaStreamCreateWithFlags(&c->e2e_in, cudaStreamNonBlocking));
+      KKT_CUDA(cudaStreamCreateWithFlags(&c->e2e_out, cudaStreamNonBlocking));
+      KKT_CUDA(cudaStreamCreateWithFlags(&c->e2e_aux, cudaStreamNonBlocking));
+      for (auto& e : c->e2e_ev) KKT_CUDA(cudaEventCreate(&e));
+    }
+    double* in = c->e2e_b.p;
+    double* out = c->e2e_x.p;
+    const size_t bytes = sizeof(double) * B;
+    cudaEvent_t* ev = c->e2e_ev;  // 0: start, 1: r_w up, 2: r_u r_z up, 3: u z done, 4: w done
+    // the staging vectors may still be read by earlier work on the context stream
+    KKT_CUDA(cudaEventRecord(ev[0], c->stream));
+    KKT_CUDA(cudaStreamWaitEvent(c->e2e_in, ev[0], 0));
+    KKT_CUDA(cudaStreamWaitEvent(c->e2e_aux, ev[0], 0));
+    KKT_CUDA(cudaMemcpyAsync(in + 2 * B, r_host + 2 * B, bytes, cudaMemcpyHostToDevice, c->e2e_in));
+    KKT_CUDA(cudaEventRecord(ev[1], c->e2e_in));
+    KKT_CUDA(cudaMemcpyAsync(in, r_host, 2 * bytes, cudaMemcpyHostToDevice, c->e2e_in));
+    KKT_CUDA(cudaEventRecord(ev[2], c->e2e_in));
+    // Schur block on the context stream
+    KKT_CUDA(cudaStreamWaitEvent(c->stream, ev[1], 0));
+    kkt::schur_apply(c, in + 2 * B, out + 2 * B);
+    KKT_CUDA(cudaEventRecord(ev[4], c->stream));
+    // u and z blocks on the side stream (the kernels launch on c->stream: swap it for the call)
+    KKT_CUDA(cudaStreamWaitEvent(c->e2e_aux, ev[2], 0));
+    {
+      cudaStream_t keep = c->stream;
+      c->stream = c->e2e_aux;
+      try {
+        kkt::op_pinv_uz(c, in, out);
+      } catch (...) {
+        c->stream = keep;
+        throw;
+      }
+      c->stream = keep;
+    }
+    KKT_CUDA(cudaEventRecord(ev[3], c->e2e_aux));
+    KKT_CUDA(cudaStreamWaitEvent(c->e2e_out, ev[3], 0));
+    KKT_CUDA(cudaMemcpyAsync(out_host, out, 2 * bytes, cudaMemcpyDeviceToHost, c->e2e_out));
+    KKT_CUDA(cudaStreamWaitEvent(c->e2e_out, ev[4], 0));
+    KKT_CUDA(cudaMemcpyAsync(out_host + 2 * B, out + 2 * B, bytes, cudaMemcpyDeviceToHost, c->e2e_out));
+    KKT_CUDA(cudaStreamSynchronize(c->e2e_out));
     KKT_CUDA(cudaStreamSynchronize(c->stream));
+    static const bool tim = std::getenv("KKT_E2E_TIM") != nullptr;  // stage completion times since the start
+    if (tim) {
+      cudaEvent_t done;
+      KKT_CUDA(cudaEventCreate(&done));
+      KKT_CUDA(cudaEventRecord(done, c->e2e_out));
+      KKT_CUDA(cudaEventSynchronize(done));
+      float t[5] = {0, 0, 0, 0, 0};
+      for (int i = 1; i < 5; ++i) KKT_CUDA(cudaEventElapsedTime(&t[i], ev[0], ev[i]));
+      KKT_CUDA(cudaEventElapsedTime(&t[0], ev[0], done));
+      std::fprintf(stderr, "P_inv_host ms since start: r_w up %.1f, r_u r_z up %.1f, u z computed %.1f, sweep done %.1f, all down %.1f\n",
+                   t[1], t[2], t[3], t[4], t[0]);
+      cudaEventDestroy(done);
+    }
   });
 }
 

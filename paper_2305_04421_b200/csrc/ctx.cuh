@@ -188,6 +188,8 @@ struct Ctx {
   std::vector<DBuf<double>> basis;
   DBuf<double> g_r, g_w, g_z, g_scratch;
   DBuf<double> e2e_b, e2e_x;       // kkt_gmres_solve_host staging
+  cudaStream_t e2e_in = nullptr, e2e_out = nullptr, e2e_aux = nullptr;  // kkt_apply_P_inv_host: copy / side streams
+  cudaEvent_t e2e_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 
   // ---- instrumentation
   int64_t launches = 0;
