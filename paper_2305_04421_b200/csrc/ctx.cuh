@@ -133,8 +133,7 @@ struct Ctx {
   int v6_jstar = 0, v6_nops = 0, v6_kn = 0;
   // k-row grouping of the v6 chain (sweep_v6.cu): propagator products over groups of v6_k block rows
   DBuf<double> v6_phi;
-  DBuf<ulonglong2> v6_ll;          // low-latency row-handoff packets (sweep_v6.cu)
-  unsigned long long v6_seq = 0;   // chain-kernel launch counter (packet tag space)
+  DBuf<unsigned long long> v6_ll;  // low-latency row-handoff slots (sweep_v6.cu)
   int v6_k = 1, v6_nind = 0, v6_gconv = 0, v6_nphi = 0, v6_npsi = 0;
   DBuf<unsigned> v4_flags;
   int v4_nsets = 0;

@@ -88,12 +88,13 @@ struct V6Params {
   int nind;           // L: groups [0, nind) have their own Phi rows, the rest share one converged set
   int gconv;          // U: groups [0, gconv) (from the top) share the converged set, the rest have their own
   int pass;           // v6_inner_kernel: row i of every group
-  // Low-latency row handoff (kLL): the last row of a group is published as 16-byte packets
-  // {value bits, tag}, one per (row, chain), slot [g][group step][KN][8]; consumers spin on the tag
-  // of the packets they need, so a handoff is one L2 write and one L2 read, with no release /
-  // acquire counter and no separate copy of y.  tag = seq | (group step + 1), seq new per launch.
-  ulonglong2* ll;
-  unsigned long long seq;
+  // Low-latency row handoff (kLL): the last row of a group is published as bare 8-byte values, one
+  // per (row, chain), in a slot per (chain group, group step) that the host pre-fills with a
+  // sentinel bit pattern (all ones: a NaN no arithmetic produces) before every chain launch.
+  // Consumers spin on the slots of exactly the values they need until none is the sentinel, so a
+  // handoff is one L2 write and one L2 read: no release / acquire counter, no separate copy of y.
+  // Only 64-bit store atomicity is assumed.  Slots are not reused inside a launch.
+  unsigned long long* ll;
   long long* tim;    // KKT_V6_TIM: per-row clock64 phase sums of CTA 0 (6 per direction)
 };
 
@@ -456,13 +457,16 @@ __global__ void __launch_bounds__(kThr6, 1) v6_inner_kernel(V6Params P) {
 template <int KN>
 constexpr size_t chain_smem() { return sizeof(double) * (16 * KN + KN * kG + 8 * 128) + 3 * sizeof(uint64_t); }
 
-__device__ __forceinline__ ulonglong2 ld_packet(const ulonglong2* p) {
+constexpr unsigned long long kLLEmpty = 0xFFFFFFFFFFFFFFFFull;  // slot not yet written
+__device__ __forceinline__ ulonglong2 ld_slots(const unsigned long long* p) {  // two adjacent slots
   ulonglong2 v;
   asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];\n" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_packet(ulonglong2* p, double val, unsigned long long tag) {
-  asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};\n" ::"l"(p), "l"(__double_as_longlong(val)), "l"(tag) : "memory");
+__device__ __forceinline__ void st_slot(unsigned long long* p, double val) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(val);
+  if (b == kLLEmpty) b = 0x7FF8000000000000ull;  // a NaN with the sentinel's bits: publish the canonical one
+  asm volatile("st.volatile.global.u64 [%0], %1;\n" ::"l"(p), "l"(b) : "memory");
 }
 
 // co-resident CTAs per SM the register budget must allow (shared memory would allow 3 / 2 / 1 at
@@ -508,7 +512,7 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
   auto Jof = [&](int gr) { return grow(kUpper, gr, gi, P.k, ny); };  // this CTA's row of group gr
   auto emit = [&](int gr, int J, double v) {
     if (kLL && last_row)
-      st_packet(P.ll + (size_t(g) * P.ngr + gr) * (KN * kG) + size_t(row) * kG + n, v, P.seq | (unsigned long long)(gr + 1));
+      st_slot(P.ll + (size_t(g) * P.ngr + gr) * (KN * kG) + size_t(row) * kG + n, v);
     P.W0[widx<KN>(g, J, ny) + size_t(row) * kG + n] = v;
     if (out) out[size_t(J) * P.nx + row] = v;
     if (out2) out2[size_t(J) * P.nx + row] = v + g2;
@@ -566,24 +570,26 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
     // the KN = 512 kernel at 2 CTAs per SM
     __syncthreads();
     if (kLL) {
-      // this warp's k-range of the previous group's last row: KN packets, KN / 32 per lane,
-      // 8 in flight; re-issue only the ones whose tag has not arrived yet
+      // this warp's k-range of the previous group's last row: KN values, KN / 32 per lane, loaded
+      // as pairs (16 bytes), up to 8 loads in flight; re-issue only the pairs not yet complete
       (void)Jp;
-      const unsigned long long tag = P.seq | (unsigned long long)idx;  // group step idx-1 -> tag idx
-      const ulonglong2* src = P.ll + (size_t(g) * P.ngr + (idx - 1)) * (KN * kG) + warp * KN + lane;
-      double* dstB = Bs + warp * KN + lane;
+      const unsigned long long* src = P.ll + (size_t(g) * P.ngr + (idx - 1)) * (KN * kG) + warp * KN + 2 * lane;
+      double* dstB = Bs + warp * KN + 2 * lane;
+      constexpr int kPairs = KN / 64;              // 16-byte loads per lane
+      constexpr int kBatch = kPairs < 8 ? kPairs : 8;
 #pragma unroll 1
-      for (int q0 = 0; q0 < KN / 32; q0 += 8) {
-        ulonglong2 v[8];
-        unsigned pending = 0xffu;
+      for (int q0 = 0; q0 < kPairs; q0 += kBatch) {
+        ulonglong2 v[kBatch];
+        unsigned pending = (1u << kBatch) - 1u;
         while (pending) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if ((pending >> u) & 1u) v[u] = ld_packet(src + (q0 + u) * 32);
+          for (int u = 0; u < kBatch; ++u)
+            if ((pending >> u) & 1u) v[u] = ld_slots(src + (q0 + u) * 64);
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (((pending >> u) & 1u) && v[u].y == tag) {
-              dstB[(q0 + u) * 32] = __longlong_as_double((long long)v[u].x);
+          for (int u = 0; u < kBatch; ++u)
+            if (((pending >> u) & 1u) && v[u].x != kLLEmpty && v[u].y != kLLEmpty) {
+              *reinterpret_cast<double2*>(dstB + (q0 + u) * 64) =
+                  make_double2(__longlong_as_double((long long)v[u].x), __longlong_as_double((long long)v[u].y));
               pending &= ~(1u << u);
             }
         }
@@ -702,7 +708,6 @@ void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   V6Params p = P;
-  p.seq = (++c->v6_seq) << 20;  // a fresh tag space per launch: packets of earlier launches never match
   void* args[] = {&p};
   const void* fn = P.ll ? (upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true, true>)
                                  : reinterpret_cast<const void*>(&v6_chain_kernel<KN, false, true>))
@@ -808,6 +813,8 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
           KKT_LAUNCH(c, (v6_inner_kernel<KN, false>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
       }
       KKT_CUDA(cudaMemsetAsync(P.cnt, 0, sizeof(unsigned) * ngroups, c->stream));
+      if (P.ll)  // every handoff slot of this sweep direction back to "empty"
+        KKT_CUDA(cudaMemsetAsync(P.ll, 0xFF, sizeof(unsigned long long) * size_t(ngroups) * P.ngr * KN * kG, c->stream));
       for (int g0 = 0; g0 < ngroups; g0 += gpw) {
         P.g0 = g0;
         launch_chain<KN>(c, up, P, std::min(gpw, ngroups - g0));
@@ -999,19 +1006,15 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.cnt = c->v6_cnt.p;
   P.k = c->v6_k;
   P.ngr = (ny + P.k - 1) / P.k;
-  // packet handoff: measured ahead of the release counter at KN = 256 (config 3: 150 -> 128 ms);
-  // at KN = 1024 a warp's 1024 packets take four dependent batches and the counter + bulk copy wins
-  // (config-4 slab 164 vs 181 ms).  KKT_V6_LL=0/1 forces the choice.
+  // slot handoff instead of the release counter + bulk copy.  KKT_V6_LL=0/1 forces the choice.
   static const char* ll_env = std::getenv("KKT_V6_LL");
-  const bool ll_on = ll_env ? std::atoi(ll_env) != 0 : kn <= 512;
+  const bool ll_on = ll_env ? std::atoi(ll_env) != 0 : true;
   P.ll = nullptr;
-  P.seq = 0;
   if (ll_on) {
     const size_t npk = size_t(ngroups) * P.ngr * kn * kG;
     if (c->v6_ll.n < npk) {
       KKT_CUDA(cudaStreamSynchronize(c->stream));
       c->v6_ll.alloc(npk);
-      KKT_CUDA(cudaMemsetAsync(c->v6_ll.p, 0, sizeof(ulonglong2) * npk, c->stream));  // tag 0 is never published
     }
     P.ll = c->v6_ll.p;
   }
