@@ -134,6 +134,9 @@ struct Ctx {
   // k-row grouping of the v6 chain (sweep_v6.cu): propagator products over groups of v6_k block rows
   DBuf<double> v6_phi;
   DBuf<unsigned long long> v6_ll;  // low-latency row-handoff slots (sweep_v6.cu)
+  DBuf<int2> v6_band, v6_raw;      // numerical band of the operators: chain windows, raw k-step ranges
+  bool v6_band_on = false;         // the chain uses the windows (they are clearly narrower than the rows)
+  bool v6_raw_on[4] = {false, false, false, false};  // likewise the raw ranges of Li, Ui, G, H
   int v6_k = 1, v6_nind = 0, v6_gconv = 0, v6_nphi = 0, v6_npsi = 0;
   DBuf<unsigned> v4_flags;
   int v4_nsets = 0;

@@ -95,6 +95,18 @@ struct V6Params {
   // handoff is one L2 write and one L2 read: no release / acquire counter, no separate copy of y.
   // Only 64-bit store atomicity is assumed.  Slots are not reused inside a launch.
   unsigned long long* ll;
+  // Numerical band of the propagators: per (packed operator row, 16-row slice) the window of
+  // k-steps {first, per-warp count} outside which every entry is below KKT_V6_BTOL (1e-17) times
+  // the operator's largest entry.  The inverted blocks decay exponentially away from the diagonal
+  // (half-bandwidth ~144 of 511 at config 2); the chain multiplies only the window.
+  const int2* bandPhi;
+  const int2* bandPsi;
+  // raw {first k-step, one past the last} per (operator row, slice) of Li, Ui, G, H: the off-chain
+  // triangles and the in-group products skip the k-steps outside (null: none skipped)
+  const int2* rawL;
+  const int2* rawU;
+  const int2* rawG;
+  const int2* rawH;
   long long* tim;    // KKT_V6_TIM: per-row clock64 phase sums of CTA 0 (6 per direction)
 };
 
@@ -151,6 +163,26 @@ __device__ __forceinline__ void slice_coords(int t, int& m, int& n) {
   n = 2 * (lane & 3) + e;
 }
 
+// k-step range of slice s of a triangle (lower: Li, upper: Ui), cut to the operator's numerical band
+__device__ __forceinline__ void tri_range(bool upper, int s, int kKS, const int2* raw, int row, int kSl, int& ks0, int& ks1) {
+  ks0 = upper ? 4 * s : 0;
+  ks1 = upper ? kKS : 4 * s + 4;
+  if (raw) {
+    const int2 b = raw[size_t(row) * kSl + s];
+    ks0 = max(ks0, b.x);
+    ks1 = min(ks1, b.y);
+  }
+}
+// the same with the table entry fetched one slice ahead (b = this slice's entry)
+__device__ __forceinline__ void tri_range_b(bool upper, int s, int kKS, bool have, int2 b, int& ks0, int& ks1) {
+  ks0 = upper ? 4 * s : 0;
+  ks1 = upper ? kKS : 4 * s + 4;
+  if (have) {
+    ks0 = max(ks0, b.x);
+    ks1 = min(ks1, b.y);
+  }
+}
+
 // Batched triangular products for every block row: Out[g][J] = T_J In[g][J]
 // over the nonzero k-steps of the triangle (lower: Li, upper: Ui).  One CTA
 // per block row J; chain groups in pairs, their block vectors In[g][J] staged
@@ -181,8 +213,8 @@ __global__ void __launch_bounds__(kThr6, 1) v6_off_kernel(V6Params P) {
       __syncthreads();
       for (int i = 0; i < kSl / 8; ++i) {
         const int s = (i >> 1) * 16 + ((i & 1) ? 15 - warp : warp);
-        const int ks0 = kUpper ? 4 * s : 0;
-        const int ks1 = kUpper ? kKS : 4 * s + 4;
+        int ks0, ks1;
+        tri_range(kUpper, s, kKS, kUpper ? P.rawU : P.rawL, oprow(J, P.jstar), kSl, ks0, ks1);
         const bool res = J >= P.jstar;
         const double* A = (kUpper ? P.Up : P.Lp) + (size_t(oprow(J, P.jstar)) * kSl + s) * kKS * 64 + lane;
         double d[2][2][2] = {};
@@ -293,8 +325,13 @@ __global__ void __launch_bounds__(kOffThr, 1) v6_off2_kernel(V6Params P) {
                          "r"(tma::smem_u32(barB))
                          : "memory");
           }
+          const int2* rawrow = (kUpper ? P.rawU : P.rawL) ? (kUpper ? P.rawU : P.rawL) + size_t(oprow(J, P.jstar)) * kSl : nullptr;
+          int2 rb = rawrow ? rawrow[0] : make_int2(0, 0);
           for (int s = 0; s < kSl; ++s) {
-            const int ks0 = kUpper ? 4 * s : 0, ks1 = kUpper ? kKS : 4 * s + 4;
+            int ks0, ks1;
+            const int2 cur = rb;
+            if (rawrow && s + 1 < kSl) rb = rawrow[s + 1];  // one slice ahead: off the critical path
+            tri_range_b(kUpper, s, kKS, rawrow != nullptr, cur, ks0, ks1);
             for (int kb = ks0; kb < ks1; kb += CK, ++it) {
               const int slot = it % kOffRing, len = min(CK, ks1 - kb);
               if (it >= kOffRing) mbar_wait(&empty[slot], uint32_t(it / kOffRing - 1) & 1u);
@@ -312,8 +349,13 @@ __global__ void __launch_bounds__(kOffThr, 1) v6_off2_kernel(V6Params P) {
   for (int J = blockIdx.x; J < P.ny; J += gridDim.x) {
     for (int gp = 0; gp < P.ngroups; gp += NG, ++item) {
       mbar_wait(barB, uint32_t(item) & 1u);
+      const int2* rawrow = (kUpper ? P.rawU : P.rawL) ? (kUpper ? P.rawU : P.rawL) + size_t(oprow(J, P.jstar)) * kSl : nullptr;
+      int2 rb = rawrow ? rawrow[0] : make_int2(0, 0);
       for (int s = 0; s < kSl; ++s, ++sl) {
-        const int ks0 = kUpper ? 4 * s : 0, ks1 = kUpper ? kKS : 4 * s + 4;
+        int ks0, ks1;
+        const int2 cur = rb;
+        if (rawrow && s + 1 < kSl) rb = rawrow[s + 1];
+        tri_range_b(kUpper, s, kKS, rawrow != nullptr, cur, ks0, ks1);
         double d[NG][2][2] = {};
         for (int kb = ks0; kb < ks1; kb += CK, ++it) {
           const int slot = it % kOffRing, len = min(CK, ks1 - kb);
@@ -379,7 +421,7 @@ __device__ __forceinline__ int propidx(bool upper, int gr, int i, int J, const V
 // in place in W1.  One CTA per (group, pair of chain groups); the two chain groups' c'_{J-+1} are
 // staged in shared memory; each warp owns whole 16-row slices and streams its operator slice from
 // L2 / HBM in fragment order, 16 k-steps in flight (as v6_off_kernel, full rows instead of triangles).
-template <int KN, bool kUpper>
+template <int KN, bool kUpper, bool kBand>
 __global__ void __launch_bounds__(kThr6, 1) v6_inner_kernel(V6Params P) {
   V6_DIMS
   extern __shared__ double Bs[];  // [2][kN][8]
@@ -402,26 +444,47 @@ __global__ void __launch_bounds__(kThr6, 1) v6_inner_kernel(V6Params P) {
     const double* A = (kUpper ? P.Hp : P.Gp) + (size_t(oprow(J, P.jstar)) * kSl + s) * kKS * 64 + lane;
     double d[2][2][2] = {};
     double ac[kOffChunk][2], an[kOffChunk][2];
+    int ks0 = 0, ks1 = kKS;  // compile-time constants without the band
+    if constexpr (kBand) {
+      const int2 b = (kUpper ? P.rawH : P.rawG)[size_t(oprow(J, P.jstar)) * kSl + s];
+      ks0 = b.x;
+      ks1 = b.y;
+    }
 #pragma unroll
     for (int u = 0; u < kOffChunk; ++u) {
-      ac[u][0] = ldop(A + size_t(u) * 64, res);
-      ac[u][1] = ldop(A + size_t(u) * 64 + 32, res);
+      const bool ok = ks0 + u < ks1;
+      ac[u][0] = ok ? ldop(A + size_t(ks0 + u) * 64, res) : 0.0;
+      ac[u][1] = ok ? ldop(A + size_t(ks0 + u) * 64 + 32, res) : 0.0;
     }
-    for (int ks = 0; ks < kKS; ks += kOffChunk) {
+    for (int ks = ks0; ks < ks1; ks += kOffChunk) {
 #pragma unroll
       for (int u = 0; u < kOffChunk; ++u) {
-        const bool ok = ks + kOffChunk + u < kKS;
+        const bool ok = ks + kOffChunk + u < ks1;
         an[u][0] = ok ? ldop(A + size_t(ks + kOffChunk + u) * 64, res) : 0.0;
         an[u][1] = ok ? ldop(A + size_t(ks + kOffChunk + u) * 64 + 32, res) : 0.0;
       }
+      if (ks + kOffChunk <= ks1) {  // a whole chunk: no per-step guard
 #pragma unroll
-      for (int u = 0; u < kOffChunk; ++u) {
-        const double b0 = Bs[(4 * (ks + u)) * kG + bo];
-        const double b1 = Bs[KN * kG + (4 * (ks + u)) * kG + bo];
-        dmma6(d[0][0][0], d[0][0][1], ac[u][0], b0);
-        dmma6(d[0][1][0], d[0][1][1], ac[u][1], b0);
-        dmma6(d[1][0][0], d[1][0][1], ac[u][0], b1);
-        dmma6(d[1][1][0], d[1][1][1], ac[u][1], b1);
+        for (int u = 0; u < kOffChunk; ++u) {
+          const double b0 = Bs[(4 * (ks + u)) * kG + bo];
+          const double b1 = Bs[KN * kG + (4 * (ks + u)) * kG + bo];
+          dmma6(d[0][0][0], d[0][0][1], ac[u][0], b0);
+          dmma6(d[0][1][0], d[0][1][1], ac[u][1], b0);
+          dmma6(d[1][0][0], d[1][0][1], ac[u][0], b1);
+          dmma6(d[1][1][0], d[1][1][1], ac[u][1], b1);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kOffChunk; ++u) {
+          if (ks + u < ks1) {
+            const double b0 = Bs[(4 * (ks + u)) * kG + bo];
+            const double b1 = Bs[KN * kG + (4 * (ks + u)) * kG + bo];
+            dmma6(d[0][0][0], d[0][0][1], ac[u][0], b0);
+            dmma6(d[0][1][0], d[0][1][1], ac[u][1], b0);
+            dmma6(d[1][0][0], d[1][0][1], ac[u][0], b1);
+            dmma6(d[1][1][0], d[1][1][1], ac[u][1], b1);
+          }
+        }
       }
 #pragma unroll
       for (int u = 0; u < kOffChunk; ++u) {
@@ -475,7 +538,7 @@ __device__ __forceinline__ void st_slot(unsigned long long* p, double val) {
 template <int KN>
 constexpr int chain_min_blocks() { return KN <= 512 ? 2 : 1; }  // 3 at KN = 256 spills (80 registers)
 
-template <int KN, bool kUpper, bool kLL>
+template <int KN, bool kUpper, bool kLL, bool kWin>
 __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel(V6Params P) {
   V6_DIMS
   extern __shared__ __align__(128) double sm6[];
@@ -525,9 +588,16 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
       if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(cnt) : "memory");
     }
   };
-  auto copy_a = [&](int gr, int J) {  // thread 0
-    tma_load(As, Mbase + size_t(propidx(kUpper, gr, gi, J, P)) * mstride, sizeof(double) * 16 * KN, barA);
+  // windows only in the <kWin> instantiation (slot handoff; the counter path copies y in fixed halves)
+  const int2* band = kWin ? (kUpper ? P.bandPsi : P.bandPhi) : nullptr;
+  auto window = [&](int pidx) { return band ? band[size_t(pidx) * kSl + s] : make_int2(0, kKW); };
+  auto copy_a = [&](int gr, int J, int2 wn) {  // thread 0: this slice's window of the operator row
+    const int pidx = propidx(kUpper, gr, gi, J, P);
+    tma_load(As + size_t(wn.x) * 64, Mbase + size_t(pidx) * mstride + size_t(wn.x) * 64,
+             uint32_t(sizeof(double) * 64 * 8 * wn.y), barA);
   };
+  // the window of the next group step is fetched one step ahead, off the row's critical path
+  int2 wn_next = make_int2(0, kKW);
   if (threadIdx.x == 0) {
     mbar_init(barA, 1);
     mbar_init(barB, 1);
@@ -540,7 +610,10 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
     if (J < 0) return;
     if (outt) emit(0, J, __ldcg(P.W1 + widx<KN>(g, J, ny) + size_t(row) * kG + n));
     signal();
-    if (P.ngr > 1 && Jof(1) >= 0 && threadIdx.x == 0) copy_a(1, Jof(1));
+    if (P.ngr > 1 && Jof(1) >= 0) {
+      wn_next = window(propidx(kUpper, 1, gi, Jof(1), P));
+      if (threadIdx.x == 0) copy_a(1, Jof(1), wn_next);
+    }
   }
   const int bo = (lane & 3) * kG + (lane >> 2);
   const bool tm = P.tim && blockIdx.x == 0 && threadIdx.x == 0;
@@ -549,6 +622,9 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
     const int J = Jof(idx);
     if (J < 0) break;  // the ragged last group has no such row (and no successor waits for it)
     const int Jp = kUpper ? ny - idx * P.k : idx * P.k - 1;  // the previous group's last row
+    const int2 wn = wn_next;  // {first k-step, k-steps per warp}
+    const bool more = idx + 1 < P.ngr && Jof(idx + 1) >= 0;
+    if (more) wn_next = window(propidx(kUpper, idx + 1, gi, Jof(idx + 1), P));
     if (tm) ts[0] = clock64();
     const uint32_t par = uint32_t(idx - 1) & 1u;
     double cval = 0.0;
@@ -570,28 +646,50 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
     // the KN = 512 kernel at 2 CTAs per SM
     __syncthreads();
     if (kLL) {
-      // this warp's k-range of the previous group's last row: KN values, KN / 32 per lane, loaded
-      // as pairs (16 bytes), up to 8 loads in flight; re-issue only the pairs not yet complete
+      // this warp's k-steps of the previous group's last row: 32 values per k-step, loaded as
+      // pairs (16 bytes), up to 8 loads in flight; re-issue only the pairs not yet complete
       (void)Jp;
-      const unsigned long long* src = P.ll + (size_t(g) * P.ngr + (idx - 1)) * (KN * kG) + warp * KN + 2 * lane;
-      double* dstB = Bs + warp * KN + 2 * lane;
-      constexpr int kPairs = KN / 64;              // 16-byte loads per lane
-      constexpr int kBatch = kPairs < 8 ? kPairs : 8;
+      const size_t voff = size_t(wn.x + warp * wn.y) * 32 + 2 * lane;
+      const unsigned long long* src = P.ll + (size_t(g) * P.ngr + (idx - 1)) * (KN * kG) + voff;
+      double* dstB = Bs + voff;
+      if (!kWin) {  // full row: compile-time batches
+        constexpr int kPairs = KN / 64;  // 16-byte loads per lane
+        constexpr int kBatch = kPairs < 8 ? kPairs : 8;
 #pragma unroll 1
-      for (int q0 = 0; q0 < kPairs; q0 += kBatch) {
-        ulonglong2 v[kBatch];
-        unsigned pending = (1u << kBatch) - 1u;
-        while (pending) {
+        for (int q0 = 0; q0 < kPairs; q0 += kBatch) {
+          ulonglong2 v[kBatch];
+          unsigned pending = (1u << kBatch) - 1u;
+          while (pending) {
 #pragma unroll
-          for (int u = 0; u < kBatch; ++u)
-            if ((pending >> u) & 1u) v[u] = ld_slots(src + (q0 + u) * 64);
+            for (int u = 0; u < kBatch; ++u)
+              if ((pending >> u) & 1u) v[u] = ld_slots(src + (q0 + u) * 64);
 #pragma unroll
-          for (int u = 0; u < kBatch; ++u)
-            if (((pending >> u) & 1u) && v[u].x != kLLEmpty && v[u].y != kLLEmpty) {
-              *reinterpret_cast<double2*>(dstB + (q0 + u) * 64) =
-                  make_double2(__longlong_as_double((long long)v[u].x), __longlong_as_double((long long)v[u].y));
-              pending &= ~(1u << u);
-            }
+            for (int u = 0; u < kBatch; ++u)
+              if (((pending >> u) & 1u) && v[u].x != kLLEmpty && v[u].y != kLLEmpty) {
+                *reinterpret_cast<double2*>(dstB + (q0 + u) * 64) =
+                    make_double2(__longlong_as_double((long long)v[u].x), __longlong_as_double((long long)v[u].y));
+                pending &= ~(1u << u);
+              }
+          }
+        }
+      } else {
+        const int npairs = wn.y >> 1;
+#pragma unroll 1
+        for (int q0 = 0; q0 < npairs; q0 += 8) {
+          ulonglong2 v[8];
+          unsigned pending = npairs - q0 >= 8 ? 0xffu : (1u << (npairs - q0)) - 1u;
+          while (pending) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if ((pending >> u) & 1u) v[u] = ld_slots(src + (q0 + u) * 64);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (((pending >> u) & 1u) && v[u].x != kLLEmpty && v[u].y != kLLEmpty) {
+                *reinterpret_cast<double2*>(dstB + (q0 + u) * 64) =
+                    make_double2(__longlong_as_double((long long)v[u].x), __longlong_as_double((long long)v[u].y));
+                pending &= ~(1u << u);
+              }
+          }
         }
       }
       __syncwarp();
@@ -605,21 +703,41 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
       if (tm) ts[3] = clock64();
     }
     double d[2][2][2] = {};
-    const double* Aw = As + size_t(warp * kKW) * 64 + lane;
-    const double* Bw = Bs + size_t(warp * kKW) * 4 * kG + bo;
+    const double* Aw = As + size_t(wn.x + warp * wn.y) * 64 + lane;
+    const double* Bw = Bs + size_t(wn.x + warp * wn.y) * 4 * kG + bo;
+    if (!kWin) {  // full row: the fixed, fully unrolled product
 #pragma unroll
-    for (int i0 = 0; i0 < kKW; i0 += 8) {
+      for (int i0 = 0; i0 < kKW; i0 += 8) {
+        double a0[8], a1[8], b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a0[u] = Aw[(i0 + u) * 64];
+          a1[u] = Aw[(i0 + u) * 64 + 32];
+          b[u] = Bw[(i0 + u) * 4 * kG];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          dmma6(d[u & 1][0][0], d[u & 1][0][1], a0[u], b[u]);
+          dmma6(d[u & 1][1][0], d[u & 1][1][1], a1[u], b[u]);
+        }
+      }
+    } else
+#pragma unroll 1
+    for (int i0 = 0; i0 < wn.y; i0 += 8) {
       double a0[8], a1[8], b[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        a0[u] = Aw[(i0 + u) * 64];
-        a1[u] = Aw[(i0 + u) * 64 + 32];
-        b[u] = Bw[(i0 + u) * 4 * kG];
+        const bool ok = i0 + u < wn.y;
+        a0[u] = ok ? Aw[(i0 + u) * 64] : 0.0;
+        a1[u] = ok ? Aw[(i0 + u) * 64 + 32] : 0.0;
+        b[u] = ok ? Bw[(i0 + u) * 4 * kG] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        dmma6(d[u & 1][0][0], d[u & 1][0][1], a0[u], b[u]);
-        dmma6(d[u & 1][1][0], d[u & 1][1][1], a1[u], b[u]);
+        if (i0 + u < wn.y) {
+          dmma6(d[u & 1][0][0], d[u & 1][0][1], a0[u], b[u]);
+          dmma6(d[u & 1][1][0], d[u & 1][1][1], a1[u], b[u]);
+        }
       }
     }
 #pragma unroll
@@ -631,7 +749,7 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
     if (outt) emit(idx, J, cval + reduce8(red, threadIdx.x));
     if (tm) ts[5] = clock64();
     signal();
-    if (idx + 1 < P.ngr && Jof(idx + 1) >= 0 && threadIdx.x == 0) copy_a(idx + 1, Jof(idx + 1));
+    if (more && threadIdx.x == 0) copy_a(idx + 1, Jof(idx + 1), wn_next);
     if (tm) {
       ts[6] = clock64();
       for (int q = 0; q < 6; ++q) acc[q] += ts[q + 1] - ts[q];
@@ -667,6 +785,47 @@ __global__ void __launch_bounds__(256) v6_conv_kernel(const double* __restrict__
   if (threadIdx.x < 2) {
     dev[2 * J + threadIdx.x] = sh[threadIdx.x][0];
     mag[2 * J + threadIdx.x] = sh[2 + threadIdx.x][0];
+  }
+}
+
+// Window table of a packed operator set (see V6Params::bandPhi): one CTA per operator row.
+template <int KN>
+__global__ void __launch_bounds__(256) v6_band_kernel(const double* __restrict__ packed, double tol, int2* __restrict__ band,
+                                                      int2* __restrict__ raw) {
+  V6_DIMS
+  __shared__ double smax[256];
+  __shared__ int slo[kSl], shi[kSl];
+  const double* M = packed + size_t(blockIdx.x) * KN * KN;
+  double m = 0.0;
+  for (int e = threadIdx.x; e < KN * KN; e += 256) m = fmax(m, fabs(M[e]));
+  smax[threadIdx.x] = m;
+  for (int i = threadIdx.x; i < kSl; i += 256) {
+    slo[i] = kKS;
+    shi[i] = -1;
+  }
+  __syncthreads();
+  for (int w = 128; w; w >>= 1) {
+    if (threadIdx.x < w) smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + w]);
+    __syncthreads();
+  }
+  const double thr = tol * smax[0];
+  for (int e = threadIdx.x; e < KN * KN; e += 256) {
+    if (fabs(M[e]) > thr) {
+      const int ks = (e >> 6) % kKS, sl = (e >> 6) / kKS;
+      atomicMin(&slo[sl], ks);
+      atomicMax(&shi[sl], ks);
+    }
+  }
+  __syncthreads();
+  for (int sl = threadIdx.x; sl < kSl; sl += 256) {
+    const int lo = slo[sl], hi = shi[sl];
+    int cnt = 2, w0 = 0;
+    if (hi >= lo) {
+      cnt = min(kKW, 2 * ((hi - lo + 1 + 15) / 16));  // k-steps per warp, even
+      w0 = max(0, min(lo, kKS - 8 * cnt));
+    }
+    if (band) band[size_t(blockIdx.x) * kSl + sl] = make_int2(w0, cnt);
+    if (raw) raw[size_t(blockIdx.x) * kSl + sl] = hi >= lo ? make_int2(lo, hi + 1) : make_int2(0, 0);
   }
 }
 
@@ -709,10 +868,14 @@ void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
   cfg.numAttrs = 1;
   V6Params p = P;
   void* args[] = {&p};
-  const void* fn = P.ll ? (upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true, true>)
-                                 : reinterpret_cast<const void*>(&v6_chain_kernel<KN, false, true>))
-                        : (upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true, false>)
-                                 : reinterpret_cast<const void*>(&v6_chain_kernel<KN, false, false>));
+  const bool win = P.ll && P.bandPhi;
+  const void* fn =
+      win ? (upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true, true, true>)
+                   : reinterpret_cast<const void*>(&v6_chain_kernel<KN, false, true, true>))
+          : P.ll ? (upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true, true, false>)
+                          : reinterpret_cast<const void*>(&v6_chain_kernel<KN, false, true, false>))
+                 : (upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true, false, false>)
+                          : reinterpret_cast<const void*>(&v6_chain_kernel<KN, false, false, false>));
   KKT_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
   c->launches++;
 }
@@ -724,14 +887,18 @@ int chain_capacity() {
   static int cap = 0;
   if (!cap) {
     const int cs = int(chain_smem<KN>()), os = int(off_smem<KN>());
-    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
-    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
-    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
-    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
-    KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
-    KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
+    KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
+    KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
+    KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
+    KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     const int os2 = int(off2_smem<KN, 2>());
     KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
     KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
@@ -742,12 +909,15 @@ int chain_capacity() {
     }
     int p0 = 0, p1 = 0;
     int q0 = 0, q1 = 0;
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p0, v6_chain_kernel<KN, false, false>, kThr6, cs));
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, v6_chain_kernel<KN, true, false>, kThr6, cs));
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q0, v6_chain_kernel<KN, false, true>, kThr6, cs));
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q1, v6_chain_kernel<KN, true, true>, kThr6, cs));
-    p0 = std::min(p0, q0);
-    p1 = std::min(p1, q1);
+    int r0 = 0, r1 = 0;
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p0, v6_chain_kernel<KN, false, false, false>, kThr6, cs));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, v6_chain_kernel<KN, true, false, false>, kThr6, cs));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q0, v6_chain_kernel<KN, false, true, false>, kThr6, cs));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q1, v6_chain_kernel<KN, true, true, false>, kThr6, cs));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r0, v6_chain_kernel<KN, false, true, true>, kThr6, cs));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, v6_chain_kernel<KN, true, true, true>, kThr6, cs));
+    p0 = std::min(p0, std::min(q0, r0));
+    p1 = std::min(p1, std::min(q1, r1));
     int dev = 0, nsm = kSmCount;
     KKT_CUDA(cudaGetDevice(&dev));
     KKT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -807,10 +977,14 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
       }
       for (int i = 1; i < P.k; ++i) {  // zero-inflow chains inside the groups, every group at once
         P.pass = i;
-        if (up)
-          KKT_LAUNCH(c, (v6_inner_kernel<KN, true>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
+        if (up && P.rawH)
+          KKT_LAUNCH(c, (v6_inner_kernel<KN, true, true>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
+        else if (up)
+          KKT_LAUNCH(c, (v6_inner_kernel<KN, true, false>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
+        else if (P.rawG)
+          KKT_LAUNCH(c, (v6_inner_kernel<KN, false, true>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
         else
-          KKT_LAUNCH(c, (v6_inner_kernel<KN, false>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
+          KKT_LAUNCH(c, (v6_inner_kernel<KN, false, false>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
       }
       KKT_CUDA(cudaMemsetAsync(P.cnt, 0, sizeof(unsigned) * ngroups, c->stream));
       if (P.ll)  // every handoff slot of this sweep direction back to "empty"
@@ -908,6 +1082,58 @@ void build_v6(Ctx* c) {
     pk(T.p, nb, c->cy, Hp + J0 * mat);
   }
   KKT_CUDA(cudaStreamSynchronize(c->stream));  // T is freed on return
+  static const double bfrac = std::getenv("KKT_V6_BFRAC") ? std::atof(std::getenv("KKT_V6_BFRAC")) : 0.65;  // tuning
+  auto make_band = [&](const double* packed, int rows, int2* out, int2* raw) {
+    static const char* bt = std::getenv("KKT_V6_BTOL");
+    const double tol = bt ? std::atof(bt) : 1e-17;
+    if (kn == 256)
+      KKT_LAUNCH(c, v6_band_kernel<256>, rows, 256, 0, packed, tol, out, raw);
+    else if (kn == 512)
+      KKT_LAUNCH(c, v6_band_kernel<512>, rows, 256, 0, packed, tol, out, raw);
+    else
+      KKT_LAUNCH(c, v6_band_kernel<1024>, rows, 256, 0, packed, tol, out, raw);
+  };
+  const int ksl = kn / 16;
+  c->v6_band.alloc(size_t(2) * nops * ksl);  // k == 1: the windows of G and H
+  c->v6_raw.alloc(size_t(4) * nops * ksl);   // raw ranges of Li, Ui, G, H
+  make_band(Lp, nops, nullptr, c->v6_raw.p);
+  make_band(Up, nops, nullptr, c->v6_raw.p + size_t(nops) * ksl);
+  make_band(Gp, nops, c->v6_band.p, c->v6_raw.p + size_t(2) * nops * ksl);
+  make_band(Hp, nops, c->v6_band.p + size_t(nops) * ksl, c->v6_raw.p + size_t(3) * nops * ksl);
+  // the windowed product has a runtime trip count; it only pays where the band is clearly narrower
+  // than the row (config 2: 55% of the k-steps; config 3: 84%, the config-4 slab: 90%, where the
+  // windowed and range-cut kernels measured slower than the fixed ones)
+  auto windows_pay = [&](const int2* dev, size_t n) {
+    std::vector<int2> h(n);
+    KKT_CUDA(cudaMemcpyAsync(h.data(), dev, sizeof(int2) * n, cudaMemcpyDeviceToHost, c->stream));
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+    double sum = 0.0;
+    for (const int2& w : h) sum += w.y;
+    const double frac = sum / (double(n) * (kn / 32));
+    if (std::getenv("KKT_V6_TIM")) std::fprintf(stderr, "v6 band windows: %.0f%% of the k-steps\n", 100.0 * frac);
+    return frac < bfrac;
+  };
+  c->v6_band_on = windows_pay(c->v6_band.p, size_t(2) * nops * ksl);
+  {  // the raw ranges likewise: k-steps kept, relative to the triangle (Li, Ui) or the full row (G, H)
+    std::vector<int2> h(size_t(4) * nops * ksl);
+    KKT_CUDA(cudaMemcpyAsync(h.data(), c->v6_raw.p, sizeof(int2) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    KKT_CUDA(cudaStreamSynchronize(c->stream));
+    const int kks = kn / 4;
+    for (int set = 0; set < 4; ++set) {
+      double kept = 0.0, full = 0.0;
+      for (int r = 0; r < nops; ++r)
+        for (int sl = 0; sl < ksl; ++sl) {
+          const int2 b = h[(size_t(set) * nops + r) * ksl + sl];
+          int lo = set == 1 ? 4 * sl : 0, hi = set == 0 ? 4 * sl + 4 : kks;  // set 0: Li (lower), 1: Ui (upper)
+          full += hi - lo;
+          kept += std::max(0, std::min(hi, b.y) - std::max(lo, b.x));
+        }
+      c->v6_raw_on[set] = kept < bfrac * full;
+      if (std::getenv("KKT_V6_TIM"))
+        std::fprintf(stderr, "v6 band of %s: %.0f%% of the k-steps\n", set == 0 ? "Li" : set == 1 ? "Ui" : set == 2 ? "G" : "H",
+                     100.0 * kept / std::max(1.0, full));
+    }
+  }
 
   // ---- k-row grouping: as many rows per handoff as co-resident CTAs allow for the RASQ chains
   // (KKT_V6_K overrides; 1 = the plain row-by-row chain)
@@ -967,6 +1193,10 @@ void build_v6(Ctx* c) {
   if (gconv > 0) build_group(Hu.p, [&](int i) { (void)i; return js; }, Psi);
   for (int gr = std::max(1, gconv); gr < ngr; ++gr)
     build_group(Hu.p, [&](int i) { return ny - 1 - gr * k - i; }, Psi + size_t(k + (gr - gconv) * k) * mat);
+  c->v6_band.alloc(size_t(c->v6_nphi + c->v6_npsi) * ksl);  // k > 1: the windows of the propagator sets
+  make_band(Phi, c->v6_nphi, c->v6_band.p, nullptr);
+  make_band(Psi, c->v6_npsi, c->v6_band.p + size_t(c->v6_nphi) * ksl, nullptr);
+  c->v6_band_on = windows_pay(c->v6_band.p, size_t(c->v6_nphi + c->v6_npsi) * ksl);
   KKT_CUDA(cudaStreamSynchronize(c->stream));  // the temporaries are freed on return
   if (std::getenv("KKT_V6_TIM"))
     std::fprintf(stderr, "v6 grouping k %d: %d groups, L own %d, U converged %d\n", k, ngr, nind, gconv);
@@ -1023,6 +1253,17 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.pass = 0;
   P.Phi = P.k == 1 ? P.Gp : c->v6_phi.p;
   P.Psi = P.k == 1 ? P.Hp : c->v6_phi.p + size_t(c->v6_nphi) * mat;
+  static const bool band_off = std::getenv("KKT_V6_NOBAND") != nullptr;  // testing: full rows
+  {
+    const size_t rs = size_t(nops) * (kn / 16);
+    P.rawL = (band_off || !c->v6_raw_on[0]) ? nullptr : c->v6_raw.p;
+    P.rawU = (band_off || !c->v6_raw_on[1]) ? nullptr : c->v6_raw.p + rs;
+    P.rawG = (band_off || !c->v6_raw_on[2]) ? nullptr : c->v6_raw.p + 2 * rs;
+    P.rawH = (band_off || !c->v6_raw_on[3]) ? nullptr : c->v6_raw.p + 3 * rs;
+  }
+  const bool win = !band_off && c->v6_band_on;
+  P.bandPhi = win ? c->v6_band.p : nullptr;
+  P.bandPsi = win ? c->v6_band.p + size_t(P.k == 1 ? nops : c->v6_nphi) * (kn / 16) : nullptr;
   static const bool dbg = std::getenv("KKT_V6_TIM") != nullptr;
   DBuf<long long> tim;
   P.tim = nullptr;
