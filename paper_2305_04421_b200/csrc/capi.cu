@@ -29,7 +29,8 @@ Ctx::~Ctx() {
   for (auto& iv : ev_pending) { cudaEventDestroy(iv.a); cudaEventDestroy(iv.b); }
   for (auto e : ev_open) if (e) cudaEventDestroy(e);
   for (auto e : e2e_ev) if (e) cudaEventDestroy(e);
-  for (auto st : {e2e_in, e2e_out, e2e_aux}) if (st) cudaStreamDestroy(st);
+  for (auto st : {e2e_in, e2e_out, e2e_aux, e2e_trail}) if (st) cudaStreamDestroy(st);
+  if (e2e_step_ev) cudaEventDestroy(e2e_step_ev);
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -529,11 +530,8 @@ int kkt_apply_P_inv_host(kkt_ctx* ctx, const double* r_host, double* out_host) {
     KKT_CUDA(cudaEventRecord(ev[1], c->e2e_in));
     KKT_CUDA(cudaMemcpyAsync(in, r_host, 2 * bytes, cudaMemcpyHostToDevice, c->e2e_in));
     KKT_CUDA(cudaEventRecord(ev[2], c->e2e_in));
-    // Schur block on the context stream
-    KKT_CUDA(cudaStreamWaitEvent(c->stream, ev[1], 0));
-    kkt::schur_apply(c, in + 2 * B, out + 2 * B);
-    KKT_CUDA(cudaEventRecord(ev[4], c->stream));
-    // u and z blocks on the side stream (the kernels launch on c->stream: swap it for the call)
+    // u and z blocks on the side stream (the kernels launch on c->stream: swap it for the call),
+    // and their download: enqueued before the sweep so that they do not queue behind it
     KKT_CUDA(cudaStreamWaitEvent(c->e2e_aux, ev[2], 0));
     {
       cudaStream_t keep = c->stream;
@@ -549,8 +547,45 @@ int kkt_apply_P_inv_host(kkt_ctx* ctx, const double* r_host, double* out_host) {
     KKT_CUDA(cudaEventRecord(ev[3], c->e2e_aux));
     KKT_CUDA(cudaStreamWaitEvent(c->e2e_out, ev[3], 0));
     KKT_CUDA(cudaMemcpyAsync(out_host, out, 2 * bytes, cudaMemcpyDeviceToHost, c->e2e_out));
-    KKT_CUDA(cudaStreamWaitEvent(c->e2e_out, ev[4], 0));
-    KKT_CUDA(cudaMemcpyAsync(out_host + 2 * B, out + 2 * B, bytes, cudaMemcpyDeviceToHost, c->e2e_out));
+    // Schur block on the context stream.  Where the RASQ sweep's output is the final w block
+    // (one-level; two-level literal; the fused multiplicative form) and the host buffer is pinned,
+    // the sweep sends each adjoint step's finished planes to the host behind the step
+    // (rasq_apply's step hook, on its own copy stream), so the w download overlaps the sweep
+    // instead of following it.
+    KKT_CUDA(cudaStreamWaitEvent(c->stream, ev[1], 0));
+    {
+      static const bool trail_off = std::getenv("KKT_E2E_TRAIL_OFF") != nullptr;  // testing: one copy at the end
+      const auto& d = c->desc;
+      const bool fused = d.precond == KKT_PRECOND_TWO_LEVEL && d.two_level_form == KKT_FORM_MULTIPLICATIVE &&
+                         !c->perdof && c->mode == KKT_MODE_FAST && c->has_fast() && !(c->bisect & 5);
+      const bool final_rasq = d.precond == KKT_PRECOND_ONE_LEVEL || fused ||
+                              (d.precond == KKT_PRECOND_TWO_LEVEL && d.two_level_form == KKT_FORM_LITERAL);
+      cudaPointerAttributes pa{};
+      const bool pinned = cudaPointerGetAttributes(&pa, out_host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+      (void)cudaGetLastError();
+      c->e2e_trailed = false;
+      if (final_rasq && pinned && !trail_off) {
+        if (!c->e2e_step_ev) {
+          KKT_CUDA(cudaEventCreateWithFlags(&c->e2e_step_ev, cudaEventDisableTiming));
+          KKT_CUDA(cudaStreamCreateWithFlags(&c->e2e_trail, cudaStreamNonBlocking));
+        }
+        c->e2e_w_host = out_host + 2 * B;
+      }
+      try {
+        kkt::schur_apply(c, in + 2 * B, out + 2 * B);
+      } catch (...) {
+        c->e2e_w_host = nullptr;
+        throw;
+      }
+      c->e2e_w_host = nullptr;
+    }
+    KKT_CUDA(cudaEventRecord(ev[4], c->stream));
+    if (!c->e2e_trailed) {
+      KKT_CUDA(cudaStreamWaitEvent(c->e2e_out, ev[4], 0));
+      KKT_CUDA(cudaMemcpyAsync(out_host + 2 * B, out + 2 * B, bytes, cudaMemcpyDeviceToHost, c->e2e_out));
+    } else {
+      KKT_CUDA(cudaStreamSynchronize(c->e2e_trail));
+    }
     KKT_CUDA(cudaStreamSynchronize(c->e2e_out));
     KKT_CUDA(cudaStreamSynchronize(c->stream));
     static const bool tim = std::getenv("KKT_E2E_TIM") != nullptr;  // stage completion times since the start
@@ -562,8 +597,8 @@ int kkt_apply_P_inv_host(kkt_ctx* ctx, const double* r_host, double* out_host) {
       float t[5] = {0, 0, 0, 0, 0};
       for (int i = 1; i < 5; ++i) KKT_CUDA(cudaEventElapsedTime(&t[i], ev[0], ev[i]));
       KKT_CUDA(cudaEventElapsedTime(&t[0], ev[0], done));
-      std::fprintf(stderr, "P_inv_host ms since start: r_w up %.1f, r_u r_z up %.1f, u z computed %.1f, sweep done %.1f, all down %.1f\n",
-                   t[1], t[2], t[3], t[4], t[0]);
+      std::fprintf(stderr, "P_inv_host ms since start: r_w up %.1f, r_u r_z up %.1f, u z computed %.1f, sweep done %.1f, all down %.1f%s\n",
+                   t[1], t[2], t[3], t[4], t[0], c->e2e_trailed ? " (w planes trailed the adjoint sweep)" : "");
       cudaEventDestroy(done);
     }
   });

@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -135,9 +136,15 @@ struct Ctx {
   DBuf<double> v6_phi;
   DBuf<unsigned long long> v6_ll;  // low-latency row-handoff slots (sweep_v6.cu)
   DBuf<int2> v6_band, v6_raw;      // numerical band of the operators: chain windows, raw k-step ranges
+  int v6_wmax = 2;                 // the widest chain window, k-steps per warp
   bool v6_band_on = false;         // the chain uses the windows (they are clearly narrower than the rows)
   bool v6_raw_on[4] = {false, false, false, false};  // likewise the raw ranges of Li, Ui, G, H
   int v6_k = 1, v6_nind = 0, v6_gconv = 0, v6_nphi = 0, v6_npsi = 0;
+  // two-sided (twisted) elimination: block rows 0..M-1 and ny-1..M+1 run as two half-length chains
+  // that meet in the middle row M = (ny-1)/2 (ny odd); v6_nyv = rows per half chain (ny: off)
+  bool v6_twist = false;
+  int v6_nyv = 0;
+  DBuf<double> v6_mid;             // packed Dm^{-1} and E = cy Dm^{-1} Ui_{M-1} (factor_block.cu)
   DBuf<unsigned> v4_flags;
   int v4_nsets = 0;
   bool v4_coop = false, v4_registered = false;
@@ -192,6 +199,15 @@ struct Ctx {
   DBuf<double> e2e_b, e2e_x;       // kkt_gmres_solve_host staging
   cudaStream_t e2e_in = nullptr, e2e_out = nullptr, e2e_aux = nullptr;  // kkt_apply_P_inv_host: copy / side streams
   cudaEvent_t e2e_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  // kkt_apply_P_inv_host: the w block's planes go back to the host as the adjoint sweep finishes
+  // them.  e2e_w_host (pinned) is set for the duration of the call; rasq_apply installs step_hook
+  // when its output is the final w block, the step-by-step sweep (v6) calls it after every step,
+  // and e2e_trailed says the planes were sent (otherwise the caller copies the block whole).
+  double* e2e_w_host = nullptr;
+  bool e2e_trailed = false;
+  cudaEvent_t e2e_step_ev = nullptr;
+  cudaStream_t e2e_trail = nullptr;
+  std::function<void(int)> step_hook;
 
   // ---- instrumentation
   int64_t launches = 0;
@@ -221,6 +237,7 @@ struct Ctx {
 void build_factor(Ctx* c);
 void build_block_inverses(Ctx* c);
 void build_block_recursion(Ctx* c);
+void build_twist_middle(Ctx* c, int M, double* Dinv, double* E);
 void build_coarse(Ctx* c);
 
 // ---- operators (stencil.cu)

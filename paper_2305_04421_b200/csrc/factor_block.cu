@@ -160,12 +160,17 @@ __global__ void gemm_kernel(int n, const double* __restrict__ A, const double* _
   }
 }
 
+// B = f * A
+__global__ void scale_copy_kernel(int64_t n, double f, const double* __restrict__ A, double* __restrict__ B) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+    B[e] = f * A[e];
+}
+
 }  // namespace
 
-void build_block_recursion(Ctx* c) {
+// ||Ahat||_inf as in build_factor (linalg.cpp:35-43 order)
+static double ahat_inf_norm(const Ctx* c) {
   const int nx = c->nx, ny = c->ny;
-  const int64_t nn = int64_t(nx) * nx;
-  // ||Ahat||_inf as in build_factor (linalg.cpp:35-43 order)
   double anorm = 0.0;
   for (int j = 1; j <= ny; ++j)
     for (int i = 1; i <= nx; ++i) {
@@ -177,7 +182,44 @@ void build_block_recursion(Ctx* c) {
       if (j < ny) row += std::abs(c->Ahat.mcy);
       anorm = std::max(anorm, row);
     }
-  const double tol = 1e-14 * anorm;
+  return anorm;
+}
+
+// D (nx x nx, overwritten by its unpivoted LU) -> Li = L^{-1}, Ui = U^{-1}; returns the failing
+// pivot column or -1 (read back after the stream drains)
+static int lu_and_inverses(Ctx* c, double tol, double* D, double* Li, double* Ui, DBuf<int>& st, DBuf<unsigned>& bar) {
+  const int nx = c->nx;
+  static const bool single = getenv("KKT_LU_SINGLE") != nullptr;  // testing: the one-CTA kernel
+  if (single) {
+    KKT_LAUNCH(c, dense_lu_nopiv_kernel, 1, kLuThreads, 0, nx, tol, D, st.p);
+  } else {
+    KKT_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(unsigned), c->stream));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kSmCount);
+    cfg.blockDim = dim3(kLuCoopThreads);
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers: every CTA co-resident
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n_ = nx;
+    double tol_ = tol;
+    double* A_ = D;
+    int* st_ = st.p;
+    unsigned* bar_ = bar.p;
+    void* args[] = {&n_, &tol_, &A_, &st_, &bar_};
+    KKT_CUDA(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(&dense_lu_nopiv_coop_kernel), args));
+    c->launches++;
+  }
+  KKT_LAUNCH(c, tri_inverse_kernel, (2 * nx + 63) / 64, 64, 0, nx, D, Li, Ui);
+  return 0;
+}
+
+void build_block_recursion(Ctx* c) {
+  const int nx = c->nx, ny = c->ny;
+  const int64_t nn = int64_t(nx) * nx;
+  const double tol = 1e-14 * ahat_inf_norm(c);
   c->Li.alloc(size_t(ny) * nn);
   c->Ui.alloc(size_t(ny) * nn);
   DBuf<double> D(nn), S(nn);
@@ -188,32 +230,9 @@ void build_block_recursion(Ctx* c) {
   for (int J = 0; J < ny; ++J) {
     KKT_LAUNCH(c, form_d_kernel, kSmCount * 2, 256, 0, nx, c->Ahat.diag, c->Ahat.mcx, cy2,
                J > 0 ? S.p : nullptr, D.p);
-    static const bool single = getenv("KKT_LU_SINGLE") != nullptr;  // testing: the one-CTA kernel
-    if (single) {
-      KKT_LAUNCH(c, dense_lu_nopiv_kernel, 1, kLuThreads, 0, nx, tol, D.p, st.p);
-    } else {
-      KKT_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(unsigned), c->stream));
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(kSmCount);
-      cfg.blockDim = dim3(kLuCoopThreads);
-      cfg.stream = c->stream;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers: every CTA co-resident
-      attr[0].val.cooperative = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      int n_ = nx;
-      double tol_ = tol;
-      double* A_ = D.p;
-      int* st_ = st.p;
-      unsigned* bar_ = bar.p;
-      void* args[] = {&n_, &tol_, &A_, &st_, &bar_};
-      KKT_CUDA(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(&dense_lu_nopiv_coop_kernel), args));
-      c->launches++;
-    }
     double* Li = c->Li.p + J * nn;
     double* Ui = c->Ui.p + J * nn;
-    KKT_LAUNCH(c, tri_inverse_kernel, (2 * nx + 63) / 64, 64, 0, nx, D.p, Li, Ui);
+    lu_and_inverses(c, tol, D.p, Li, Ui, st, bar);
     if (J + 1 < ny) KKT_LAUNCH(c, gemm_kernel, gg, gb, 0, nx, Ui, Li, S.p);
     int hs = -1;
     KKT_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -225,6 +244,39 @@ void build_block_recursion(Ctx* c) {
                   J * nx + hs);
   }
   c->pivoted = false;
+}
+
+// Middle block of the two-sided (twisted) elimination, ny odd, M = (ny - 1) / 2 (sweep_v6.cu).
+// Ahat's block rows are all (-cy I, T, -cy I), so eliminating upward from the last block row
+// gives the mirror image of the downward recursion (D'_J = D_{ny-1-J}); the two eliminations
+// meet in block row M, whose Schur complement is
+//     Dm = T - cy^2 D_{M-1}^{-1} - cy^2 D'_{M+1}^{-1} = T - 2 cy^2 Ui_{M-1} Li_{M-1}.
+// Outputs (nx x nx, row-major): Dinv = Dm^{-1}, E = cy Dm^{-1} Ui_{M-1}, so that
+//     x_M = Dinv b_M + E (y_{M-1} + y'_{M+1}).
+void build_twist_middle(Ctx* c, int M, double* Dinv, double* E) {
+  const int nx = c->nx;
+  const int64_t nn = int64_t(nx) * nx;
+  const double tol = 1e-14 * ahat_inf_norm(c);
+  DBuf<double> D(nn), S(nn), Lm(nn), Um(nn);
+  DBuf<int> st(1);
+  DBuf<unsigned> bar(1);
+  const dim3 gg((nx + 31) / 32, (nx + 31) / 32), gb(32, 8);
+  const double* Lp = c->Li.p + int64_t(M - 1) * nn;
+  const double* Up = c->Ui.p + int64_t(M - 1) * nn;
+  KKT_LAUNCH(c, gemm_kernel, gg, gb, 0, nx, Up, Lp, S.p);
+  KKT_LAUNCH(c, form_d_kernel, kSmCount * 2, 256, 0, nx, c->Ahat.diag, c->Ahat.mcx, 2.0 * c->cy * c->cy, S.p, D.p);
+  lu_and_inverses(c, tol, D.p, Lm.p, Um.p, st, bar);
+  KKT_LAUNCH(c, gemm_kernel, gg, gb, 0, nx, Um.p, Lm.p, Dinv);
+  KKT_LAUNCH(c, gemm_kernel, gg, gb, 0, nx, Dinv, Up, S.p);
+  KKT_LAUNCH(c, scale_copy_kernel, kSmCount * 2, 256, 0, nn, c->cy, S.p, E);
+  int hs = -1;
+  KKT_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  KKT_CUDA(cudaStreamSynchronize(c->stream));
+  if (hs >= 0)
+    throw Error(KKT_ESINGULAR,
+                "block LU (middle block): pivot below tolerance " + std::to_string(tol) + " at index " +
+                    std::to_string(M * nx + hs),
+                M * nx + hs);
 }
 
 }  // namespace kkt

@@ -167,7 +167,29 @@ void rasq_apply(Ctx* c, const double* r, double* out, bool fused_coarse) {
     }
   }
   check_fast_jobs(jobs, Nd, nsteps);
-  fast_chains(c, upload(c, c->jobs_fast, jobs), Nd, nsteps, fused_coarse);
+  // kkt_apply_P_inv_host with this RASQ output as the final w block: adjoint step t writes the
+  // final planes of nodes (s+1) m - t, one per local subdomain and m planes apart, which no later
+  // step touches; a step-by-step sweep (v6) sends them to the host behind each step.
+  if (c->e2e_w_host && c->v6_ops.p && !c->v4_ops.p) {
+    double* host = c->e2e_w_host;
+    c->e2e_trailed = true;
+    c->step_hook = [c, host, out, Nd, m, nsp](int t) {
+      if (t <= m) return;
+      const int tp = t - (m + 1);
+      const size_t off = size_t(m - 1 - tp) * nsp;  // node (s0 + 1) m - tp of the local slab
+      KKT_CUDA(cudaEventRecord(c->e2e_step_ev, c->stream));
+      KKT_CUDA(cudaStreamWaitEvent(c->e2e_trail, c->e2e_step_ev, 0));
+      KKT_CUDA(cudaMemcpy2DAsync(host + off, sizeof(double) * size_t(m) * nsp, out + off, sizeof(double) * size_t(m) * nsp,
+                                 sizeof(double) * nsp, size_t(Nd), cudaMemcpyDeviceToHost, c->e2e_trail));
+    };
+  }
+  try {
+    fast_chains(c, upload(c, c->jobs_fast, jobs), Nd, nsteps, fused_coarse);
+  } catch (...) {
+    c->step_hook = nullptr;
+    throw;
+  }
+  c->step_hook = nullptr;
 }
 
 }  // namespace kkt

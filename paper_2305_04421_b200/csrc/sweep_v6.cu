@@ -59,6 +59,8 @@ __device__ __forceinline__ void dmma6(double& d0, double& d1, double a, double b
                : "d"(a), "d"(b));
 }
 
+constexpr unsigned long long kLLEmpty = 0xFFFFFFFFFFFFFFFFull;  // handoff slot not yet written
+
 struct V6Params {
   const double* Lp;  // packed Li_J
   const double* Up;  // packed Ui_J
@@ -95,6 +97,8 @@ struct V6Params {
   // handoff is one L2 write and one L2 read: no release / acquire counter, no separate copy of y.
   // Only 64-bit store atomicity is assumed.  Slots are not reused inside a launch.
   unsigned long long* ll;
+  size_t nll;               // slots
+  int nopoll;               // KKT_V6_NOPOLL (timing experiment only: WRONG results): take the slots as they are
   // Numerical band of the propagators: per (packed operator row, 16-row slice) the window of
   // k-steps {first, per-warp count} outside which every entry is below KKT_V6_BTOL (1e-17) times
   // the operator's largest entry.  The inverted blocks decay exponentially away from the diagonal
@@ -108,6 +112,22 @@ struct V6Params {
   const int2* rawG;
   const int2* rawH;
   long long* tim;    // KKT_V6_TIM: per-row clock64 phase sums of CTA 0 (6 per direction)
+  // Two-sided (twisted) elimination, ny odd (build_twist_middle, factor_block.cu): block rows
+  // 0..M-1 (downward) and nyA-1..M+1 (upward, the mirror image: the same operators) are two
+  // half-length "virtual" chains per real chain, M = (nyA-1)/2 rows each; ny above is then M and
+  // ngroups counts virtual chain groups: gv = g + h*nreal is half h (0: top, 1: bottom) of real
+  // group g, its row j is block row j (top) or nyA-1-j (bottom).  The two eliminations meet in
+  // row M (v6_mid_kernel), and the back substitution runs outward from it.  A chain CTA serves
+  // both halves of its group in turn, so each half's handoff latency hides behind the other's
+  // product and the dependent chain is half as long.
+  int twist, nyA, nreal;
+  int wmax;          // v6_chainw_kernel: the widest window's k-steps per warp (shared-memory extent)
+  int phase_ns;      // the later half of a wave's chain groups starts this much later (see v6_chainw_kernel)
+  int gwave;         // chain groups in this launch
+  int spin_ns;       // KKT_V6_SPIN_NS: pause between failed poll rounds (0: none)
+  double* Wm;        // [2][nreal][kN][8]: b_M, then x_M
+  const double* Dm;  // packed Dm^{-1}
+  const double* Em;  // packed cy Dm^{-1} Ui_{M-1}
 };
 
 // Operator row of block row J, and its load: rows past jstar share one
@@ -119,22 +139,41 @@ __device__ __forceinline__ double ldop(const double* p, bool res) { return res ?
 template <int KN>
 __device__ __forceinline__ size_t widx(int g, int J, int ny) { return (size_t(g) * ny + J) * KN * kG; }
 
-// b = in*scale + add - (Shat y_c)_node / ms, chain-interleaved (fast_chain_kernel's b)
+// b = in*scale + add - (Shat y_c)_node / ms, chain-interleaved (fast_chain_kernel's b).
+// One CTA per (virtual chain group, block row, 256-row chunk): the 8 chains' plane rows are read
+// coalesced (consecutive threads = consecutive grid points of one chain) into a padded shared
+// tile and written out chain-interleaved, again coalesced.  (One thread per output element read
+// the 8 planes 32 bytes at a time: 177 us per step at config 2 against ~70 us of traffic.)
+constexpr int kFbChunk = 256;
 template <int KN>
-__global__ void __launch_bounds__(256) v6_form_b_kernel(V6Params P) {
-  const size_t total = size_t(P.ngroups) * P.ny * KN * kG;
-  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
-    const int c = int(e % kG);
-    const size_t r = e / kG;
-    const int k = int(r % KN);
-    const size_t gj = r / KN;
-    const int J = int(gj % P.ny), g = int(gj / P.ny);
+__global__ void __launch_bounds__(kFbChunk) v6_form_b_kernel(V6Params P) {
+  __shared__ double tile[kFbChunk][kG + 1];
+  constexpr int kChunks = KN / kFbChunk;
+  const int chunk = blockIdx.x % kChunks;
+  const int rb = blockIdx.x / kChunks;             // row block: (gv, j), then the middle rows (g)
+  const int nrb = P.ngroups * P.ny;
+  int J, g;
+  double* dst;
+  if (rb < nrb) {
+    const int j = rb % P.ny, gv = rb / P.ny;
+    const int h = gv >= P.nreal ? 1 : 0;
+    g = gv - h * P.nreal;
+    J = h ? P.nyA - 1 - j : j;
+    dst = P.W0 + size_t(rb) * KN * kG;
+  } else {
+    g = rb - nrb;
+    J = P.ny;  // the middle row of the twisted elimination
+    dst = P.Wm + size_t(g) * KN * kG;
+  }
+  const int k = chunk * kFbChunk + threadIdx.x;
+  const int p = J * P.nx + k;
+#pragma unroll
+  for (int c = 0; c < kG; ++c) {
     const int ch = g * kG + c;
     double v = 0.0;
     if (k < P.nx && ch < P.nchains) {
       const FastStep st = P.jobs[size_t(ch) * P.nsteps + P.t];
       if (st.in) {
-        const int p = J * P.nx + k;
         v = st.in[p] * st.scale;
         if (st.add) v += st.add[p];
         if (P.coarse && st.node > 0) {
@@ -145,7 +184,14 @@ __global__ void __launch_bounds__(256) v6_form_b_kernel(V6Params P) {
         }
       }
     }
-    P.W0[e] = v;
+    tile[threadIdx.x][c] = v;
+  }
+  __syncthreads();
+  double* o = dst + size_t(chunk) * kFbChunk * kG;
+#pragma unroll
+  for (int r = 0; r < kG; ++r) {
+    const int e = threadIdx.x + kFbChunk * r;
+    o[e] = tile[e >> 3][e & 7];
   }
 }
 
@@ -518,18 +564,17 @@ __global__ void __launch_bounds__(kThr6, 1) v6_inner_kernel(V6Params P) {
 // output warp publishes its own stores (release after __syncwarp), 4 counts
 // per CTA and row, so no CTA barrier sits between the stores and the count.
 template <int KN>
-constexpr size_t chain_smem() { return sizeof(double) * (16 * KN + KN * kG + 8 * 128) + 3 * sizeof(uint64_t); }
+constexpr size_t chain_smem() { return sizeof(double) * (16 * KN + KN * kG + 2 * 8 * 128) + 3 * sizeof(uint64_t); }
 
-constexpr unsigned long long kLLEmpty = 0xFFFFFFFFFFFFFFFFull;  // slot not yet written
 __device__ __forceinline__ ulonglong2 ld_slots(const unsigned long long* p) {  // two adjacent slots
   ulonglong2 v;
-  asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];\n" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];\n" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_slot(unsigned long long* p, double val) {
   unsigned long long b = (unsigned long long)__double_as_longlong(val);
   if (b == kLLEmpty) b = 0x7FF8000000000000ull;  // a NaN with the sentinel's bits: publish the canonical one
-  asm volatile("st.volatile.global.u64 [%0], %1;\n" ::"l"(p), "l"(b) : "memory");
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(b) : "memory");
 }
 
 // co-resident CTAs per SM the register budget must allow (shared memory would allow 3 / 2 / 1 at
@@ -544,15 +589,17 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
   extern __shared__ __align__(128) double sm6[];
   double* As = sm6;                 // [ks KN/4][mt 2][lane 32]
   double* Bs = As + 16 * KN;       // [k KN][8]
-  double* red = Bs + KN * kG;      // [warp 8][128]
-  uint64_t* barA = reinterpret_cast<uint64_t*>(red + 8 * 128);
+  double* red = Bs + KN * kG;      // [2][warp 8][128]: alternating, so one CTA barrier per product
+  uint64_t* barA = reinterpret_cast<uint64_t*>(red + 2 * 8 * 128);
   uint64_t* barB = barA + 1;  // [2]: the halves of y_{J-1} (warps 0-3 use k < KN/2, warps 4-7 the rest)
-  // CTA (sigma, g): sigma = i * kSl + s is slice s of row i of every group
+  // CTA (sigma, g): sigma = i * kSl + s is slice s of row i of every group; g is the REAL chain
+  // group (with the twisted elimination the CTA serves its two virtual groups g, g + nreal in turn)
   const int rows_per_g = kSl * P.k;
   const int sig = blockIdx.x % rows_per_g, g = P.g0 + blockIdx.x / rows_per_g;
   const int s = sig % kSl, gi = sig / kSl;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ny = P.ny;
+  const int nh = (kLL && P.twist) ? 2 : 1;
   const double* Mbase = (kUpper ? P.Psi : P.Phi) + size_t(s) * kKS * 64;
   const size_t mstride = size_t(kSl) * kKS * 64;
   unsigned* cnt = P.cnt + g;
@@ -573,12 +620,14 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
     }
   }
   auto Jof = [&](int gr) { return grow(kUpper, gr, gi, P.k, ny); };  // this CTA's row of group gr
-  auto emit = [&](int gr, int J, double v) {
+  auto emit = [&](int h, int gr, int J, double v) {
+    const int gv = g + h * P.nreal;
     if (kLL && last_row)
-      st_slot(P.ll + (size_t(g) * P.ngr + gr) * (KN * kG) + size_t(row) * kG + n, v);
-    P.W0[widx<KN>(g, J, ny) + size_t(row) * kG + n] = v;
-    if (out) out[size_t(J) * P.nx + row] = v;
-    if (out2) out2[size_t(J) * P.nx + row] = v + g2;
+      st_slot(P.ll + (size_t(gv) * P.ngr + gr) * (KN * kG) + size_t(row) * kG + n, v);
+    P.W0[widx<KN>(gv, J, ny) + size_t(row) * kG + n] = v;
+    const int Ja = h ? P.nyA - 1 - J : J;  // the block row of the grid (bottom half: mirrored)
+    if (out) out[size_t(Ja) * P.nx + row] = v;
+    if (out2) out2[size_t(Ja) * P.nx + row] = v + g2;
   };
   // each output warp publishes its own stores (release after __syncwarp), so
   // no CTA-wide barrier sits between the stores and the count; 4 per CTA and row
@@ -608,7 +657,8 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
   {  // group 0 has no inflow: its rows are the zero-inflow chain values
     const int J = Jof(0);
     if (J < 0) return;
-    if (outt) emit(0, J, __ldcg(P.W1 + widx<KN>(g, J, ny) + size_t(row) * kG + n));
+    if (outt)
+      for (int h = 0; h < nh; ++h) emit(h, 0, J, __ldcg(P.W1 + widx<KN>(g + h * P.nreal, J, ny) + size_t(row) * kG + n));
     signal();
     if (P.ngr > 1 && Jof(1) >= 0) {
       wn_next = window(propidx(kUpper, 1, gi, Jof(1), P));
@@ -616,8 +666,9 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
     }
   }
   const int bo = (lane & 3) * kG + (lane >> 2);
-  const bool tm = P.tim && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool tm = P.tim && blockIdx.x == kSl / 2 && threadIdx.x == 0;  // a middle slice: the full band window
   long long ts[7] = {0, 0, 0, 0, 0, 0, 0}, acc[6] = {0, 0, 0, 0, 0, 0};
+  int rb = 0;  // reduction buffer in use
   for (int idx = 1; idx < P.ngr; ++idx) {
     const int J = Jof(idx);
     if (J < 0) break;  // the ragged last group has no such row (and no successor waits for it)
@@ -625,139 +676,409 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
     const int2 wn = wn_next;  // {first k-step, k-steps per warp}
     const bool more = idx + 1 < P.ngr && Jof(idx + 1) >= 0;
     if (more) wn_next = window(propidx(kUpper, idx + 1, gi, Jof(idx + 1), P));
-    if (tm) ts[0] = clock64();
     const uint32_t par = uint32_t(idx - 1) & 1u;
-    double cval = 0.0;
-    if (outt) cval = __ldcg(P.W1 + widx<KN>(g, J, ny) + size_t(row) * kG + n);
-    if (!kLL && threadIdx.x == 0) {
-      const unsigned target = unsigned(idx) * kSl * 4;
-      unsigned v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
-      } while (v < target);
-      if (tm) ts[1] = clock64();
-      // y_{J-1} was written by other CTAs through the generic proxy; the copy reads it through the async proxy
-      asm volatile("fence.proxy.async.global;\n" ::: "memory");
-      const double* ysrc = P.W0 + widx<KN>(g, Jp, ny);
-      tma_load(Bs, ysrc, sizeof(double) * KN * kG / 2, barB);
-      tma_load(Bs + KN * kG / 2, ysrc + KN * kG / 2, sizeof(double) * KN * kG / 2, barB + 1);
-    }
-    // the previous row's readers of red (and of Bs) are done; one red buffer keeps
-    // the KN = 512 kernel at 2 CTAs per SM
-    __syncthreads();
-    if (kLL) {
-      // this warp's k-steps of the previous group's last row: 32 values per k-step, loaded as
-      // pairs (16 bytes), up to 8 loads in flight; re-issue only the pairs not yet complete
-      (void)Jp;
-      const size_t voff = size_t(wn.x + warp * wn.y) * 32 + 2 * lane;
-      const unsigned long long* src = P.ll + (size_t(g) * P.ngr + (idx - 1)) * (KN * kG) + voff;
-      double* dstB = Bs + voff;
-      if (!kWin) {  // full row: compile-time batches
-        constexpr int kPairs = KN / 64;  // 16-byte loads per lane
-        constexpr int kBatch = kPairs < 8 ? kPairs : 8;
-#pragma unroll 1
-        for (int q0 = 0; q0 < kPairs; q0 += kBatch) {
-          ulonglong2 v[kBatch];
-          unsigned pending = (1u << kBatch) - 1u;
-          while (pending) {
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u)
-              if ((pending >> u) & 1u) v[u] = ld_slots(src + (q0 + u) * 64);
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u)
-              if (((pending >> u) & 1u) && v[u].x != kLLEmpty && v[u].y != kLLEmpty) {
-                *reinterpret_cast<double2*>(dstB + (q0 + u) * 64) =
-                    make_double2(__longlong_as_double((long long)v[u].x), __longlong_as_double((long long)v[u].y));
-                pending &= ~(1u << u);
-              }
-          }
+    for (int h = 0; h < nh; ++h) {
+      const int gv = g + h * P.nreal;
+      if (tm) ts[0] = clock64();
+      double cval = 0.0;
+      if (outt) cval = __ldcg(P.W1 + widx<KN>(gv, J, ny) + size_t(row) * kG + n);
+      if (!kLL) {
+        if (threadIdx.x == 0) {
+          const unsigned target = unsigned(idx) * kSl * 4;
+          unsigned v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
+          } while (v < target);
+          if (tm) ts[1] = clock64();
+          // y_{J-1} was written by other CTAs through the generic proxy; the copy reads it through the async proxy
+          asm volatile("fence.proxy.async.global;\n" ::: "memory");
+          const double* ysrc = P.W0 + widx<KN>(gv, Jp, ny);
+          tma_load(Bs, ysrc, sizeof(double) * KN * kG / 2, barB);
+          tma_load(Bs + KN * kG / 2, ysrc + KN * kG / 2, sizeof(double) * KN * kG / 2, barB + 1);
         }
-      } else {
-        const int npairs = wn.y >> 1;
-#pragma unroll 1
-        for (int q0 = 0; q0 < npairs; q0 += 8) {
-          ulonglong2 v[8];
-          unsigned pending = npairs - q0 >= 8 ? 0xffu : (1u << (npairs - q0)) - 1u;
-          while (pending) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if ((pending >> u) & 1u) v[u] = ld_slots(src + (q0 + u) * 64);
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (((pending >> u) & 1u) && v[u].x != kLLEmpty && v[u].y != kLLEmpty) {
-                *reinterpret_cast<double2*>(dstB + (q0 + u) * 64) =
-                    make_double2(__longlong_as_double((long long)v[u].x), __longlong_as_double((long long)v[u].y));
-                pending &= ~(1u << u);
-              }
-          }
-        }
+        __syncthreads();
       }
-      __syncwarp();
-      if (tm) ts[1] = ts[2] = clock64();
-      mbar_wait(barA, par);
-      if (tm) ts[3] = clock64();
-    } else {
-      mbar_wait(barA, par);
-      if (tm) ts[2] = clock64();
-      mbar_wait(barB + (warp >> 2), par);  // this warp's half only: the other half may still be landing
-      if (tm) ts[3] = clock64();
-    }
-    double d[2][2][2] = {};
-    const double* Aw = As + size_t(wn.x + warp * wn.y) * 64 + lane;
-    const double* Bw = Bs + size_t(wn.x + warp * wn.y) * 4 * kG + bo;
-    if (!kWin) {  // full row: the fixed, fully unrolled product
+      if (kLL) {
+        // this warp's k-steps of the previous group's last row: 32 values per k-step, loaded as
+        // pairs (16 bytes), up to 8 loads in flight; re-issue only the pairs not yet complete.
+        // A warp reads and writes only its own k-range of Bs, so no CTA barrier guards Bs here.
+        (void)Jp;
+        const size_t voff = size_t(wn.x + warp * wn.y) * 32 + 2 * lane;
+        const unsigned long long* src = P.ll + (size_t(gv) * P.ngr + (idx - 1)) * (KN * kG) + voff;
+        double* dstB = Bs + voff;
+        if (!kWin) {  // full row: compile-time batches
+          constexpr int kPairs = KN / 64;  // 16-byte loads per lane
+          constexpr int kBatch = kPairs < 8 ? kPairs : 8;
+#pragma unroll 1
+          for (int q0 = 0; q0 < kPairs; q0 += kBatch) {
+            ulonglong2 v[kBatch];
+            unsigned pending = (1u << kBatch) - 1u;
+            while (pending) {
 #pragma unroll
-      for (int i0 = 0; i0 < kKW; i0 += 8) {
+              for (int u = 0; u < kBatch; ++u)
+                if ((pending >> u) & 1u) v[u] = ld_slots(src + (q0 + u) * 64);
+#pragma unroll
+              for (int u = 0; u < kBatch; ++u)
+                if (((pending >> u) & 1u) && ((v[u].x != kLLEmpty && v[u].y != kLLEmpty) || P.nopoll)) {
+                  *reinterpret_cast<double2*>(dstB + (q0 + u) * 64) =
+                      make_double2(__longlong_as_double((long long)v[u].x), __longlong_as_double((long long)v[u].y));
+                  pending &= ~(1u << u);
+                }
+              if (pending && P.spin_ns) __nanosleep(P.spin_ns);
+            }
+          }
+        } else {
+          const int npairs = wn.y >> 1;
+#pragma unroll 1
+          for (int q0 = 0; q0 < npairs; q0 += 8) {
+            ulonglong2 v[8];
+            unsigned pending = npairs - q0 >= 8 ? 0xffu : (1u << (npairs - q0)) - 1u;
+            while (pending) {
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if ((pending >> u) & 1u) v[u] = ld_slots(src + (q0 + u) * 64);
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (((pending >> u) & 1u) && ((v[u].x != kLLEmpty && v[u].y != kLLEmpty) || P.nopoll)) {
+                  *reinterpret_cast<double2*>(dstB + (q0 + u) * 64) =
+                      make_double2(__longlong_as_double((long long)v[u].x), __longlong_as_double((long long)v[u].y));
+                  pending &= ~(1u << u);
+                }
+              if (pending && P.spin_ns) __nanosleep(P.spin_ns);
+            }
+          }
+        }
+        __syncwarp();
+        if (tm) ts[1] = ts[2] = clock64();
+        if (h == 0) mbar_wait(barA, par);  // the operator slice serves both halves
+        if (tm) ts[3] = clock64();
+      } else {
+        mbar_wait(barA, par);
+        if (tm) ts[2] = clock64();
+        mbar_wait(barB + (warp >> 2), par);  // this warp's half only: the other half may still be landing
+        if (tm) ts[3] = clock64();
+      }
+      double d[2][2][2] = {};
+      const double* Aw = As + size_t(wn.x + warp * wn.y) * 64 + lane;
+      const double* Bw = Bs + size_t(wn.x + warp * wn.y) * 4 * kG + bo;
+      if (!kWin) {  // full row: the fixed, fully unrolled product
+#pragma unroll
+        for (int i0 = 0; i0 < kKW; i0 += 8) {
+          double a0[8], a1[8], b[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            a0[u] = Aw[(i0 + u) * 64];
+            a1[u] = Aw[(i0 + u) * 64 + 32];
+            b[u] = Bw[(i0 + u) * 4 * kG];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            dmma6(d[u & 1][0][0], d[u & 1][0][1], a0[u], b[u]);
+            dmma6(d[u & 1][1][0], d[u & 1][1][1], a1[u], b[u]);
+          }
+        }
+      } else
+#pragma unroll 1
+      for (int i0 = 0; i0 < wn.y; i0 += 8) {
         double a0[8], a1[8], b[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          a0[u] = Aw[(i0 + u) * 64];
-          a1[u] = Aw[(i0 + u) * 64 + 32];
-          b[u] = Bw[(i0 + u) * 4 * kG];
+          const bool ok = i0 + u < wn.y;
+          a0[u] = ok ? Aw[(i0 + u) * 64] : 0.0;
+          a1[u] = ok ? Aw[(i0 + u) * 64 + 32] : 0.0;
+          b[u] = ok ? Bw[(i0 + u) * 4 * kG] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          dmma6(d[u & 1][0][0], d[u & 1][0][1], a0[u], b[u]);
-          dmma6(d[u & 1][1][0], d[u & 1][1][1], a1[u], b[u]);
+          if (i0 + u < wn.y) {
+            dmma6(d[u & 1][0][0], d[u & 1][0][1], a0[u], b[u]);
+            dmma6(d[u & 1][1][0], d[u & 1][1][1], a1[u], b[u]);
+          }
         }
       }
-    } else
-#pragma unroll 1
-    for (int i0 = 0; i0 < wn.y; i0 += 8) {
-      double a0[8], a1[8], b[8];
+      double* redw = red + rb * (8 * 128);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const bool ok = i0 + u < wn.y;
-        a0[u] = ok ? Aw[(i0 + u) * 64] : 0.0;
-        a1[u] = ok ? Aw[(i0 + u) * 64 + 32] : 0.0;
-        b[u] = ok ? Bw[(i0 + u) * 4 * kG] : 0.0;
-      }
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (i0 + u < wn.y) {
-          dmma6(d[u & 1][0][0], d[u & 1][0][1], a0[u], b[u]);
-          dmma6(d[u & 1][1][0], d[u & 1][1][1], a1[u], b[u]);
-        }
+        for (int e = 0; e < 2; ++e) redw[warp * 128 + (mt * 32 + lane) * 2 + e] = d[0][mt][e] + d[1][mt][e];
+      if (tm) ts[4] = clock64();
+      // As / Bs consumed by every warp, red[rb] complete.  The other buffer is written next, after
+      // this barrier, which every reader of its previous contents has passed: one barrier per product.
+      __syncthreads();
+      if (outt) emit(h, idx, J, cval + reduce8(redw, threadIdx.x));
+      rb ^= 1;
+      if (tm) {
+        ts[5] = ts[6] = clock64();
+        for (int q = 0; q < 6; ++q) acc[q] += ts[q + 1] - ts[q];
       }
     }
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) red[warp * 128 + (mt * 32 + lane) * 2 + e] = d[0][mt][e] + d[1][mt][e];
-    if (tm) ts[4] = clock64();
-    __syncthreads();  // As / Bs consumed by every warp; red complete
-    if (outt) emit(idx, J, cval + reduce8(red, threadIdx.x));
-    if (tm) ts[5] = clock64();
     signal();
     if (more && threadIdx.x == 0) copy_a(idx + 1, Jof(idx + 1), wn_next);
-    if (tm) {
-      ts[6] = clock64();
-      for (int q = 0; q < 6; ++q) acc[q] += ts[q + 1] - ts[q];
-    }
   }
   if (tm)
     for (int q = 0; q < 6; ++q) atomicAdd(reinterpret_cast<unsigned long long*>(P.tim + (kUpper ? 6 : 0) + q),
                                           (unsigned long long)acc[q]);
+}
+
+// The windowed chain (slot handoff + numerical band, config 2's case) with the NEXT product's slots
+// prefetched: shared memory holds only the band window (As: 8 wmax k-steps, two Bs buffers of the
+// same extent), and each warp copies its k-range of the next product's slots global -> shared with
+// cp.async.cg (L2, no registers) before (same row, other half) or right after (next row) the
+// current product's DMMA loop, so the slot loads -- ~1.6k cycles per product when issued and
+// awaited in place, even with every value already published (KKT_V6_NOPOLL) -- overlap the
+// product, its reduction and its stores.  On arrival the warp checks its own pairs for the
+// sentinel and polls the (rare) missing ones synchronously, exactly as v6_chain_kernel does.
+template <int KN>
+constexpr size_t chainw_smem(int wmax) {
+  return sizeof(double) * (size_t(8) * wmax * 64 + 2 * size_t(8) * wmax * 32 + 2 * 8 * 128) + 3 * sizeof(uint64_t);
+}
+
+template <int KN, bool kUpper>
+__global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kernel(V6Params P) {
+  V6_DIMS
+  extern __shared__ __align__(128) double sm6[];
+  const int wmax = P.wmax;
+  double* As = sm6;                          // [8 wmax k-steps][mt 2][lane 32], window-relative
+  double* Bs0 = As + size_t(8) * wmax * 64;  // [2][warp 8][wmax k-steps][4][8], window-relative
+  const size_t bsz = size_t(8) * wmax * 32;
+  double* red = Bs0 + 2 * bsz;               // [2][warp 8][128]
+  uint64_t* barA = reinterpret_cast<uint64_t*>(red + 2 * 8 * 128);
+  const int rows_per_g = kSl * P.k;
+  const int sig = blockIdx.x % rows_per_g, g = P.g0 + blockIdx.x / rows_per_g;
+  const int s = sig % kSl, gi = sig / kSl;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ny = P.ny;
+  const int nh = P.twist ? 2 : 1;
+  const double* Mbase = (kUpper ? P.Psi : P.Phi) + size_t(s) * kKS * 64;
+  const size_t mstride = size_t(kSl) * kKS * 64;
+  const bool last_row = gi == P.k - 1;
+  int m = 0, n = 0;
+  const bool outt = threadIdx.x < 128;
+  if (outt) slice_coords(threadIdx.x, m, n);
+  const int row = 16 * s + m, ch = g * kG + n;
+  double* out = nullptr;
+  double* out2 = nullptr;
+  double g2 = 0.0;
+  if (kUpper && outt && row < P.nx && ch < P.nchains) {
+    const FastStep st = P.jobs[size_t(ch) * P.nsteps + P.t];
+    if (st.in) {
+      out = st.out;
+      out2 = st.out2;
+      if (st.out2 && st.node2 > 0 && P.gam) g2 = P.gam[st.node2];
+    }
+  }
+  auto Jof = [&](int gr) { return grow(kUpper, gr, gi, P.k, ny); };
+  auto emit = [&](int h, int gr, int J, double v) {
+    const int gv = g + h * P.nreal;
+    if (last_row) st_slot(P.ll + (size_t(gv) * P.ngr + gr) * (KN * kG) + size_t(row) * kG + n, v);
+    P.W0[widx<KN>(gv, J, ny) + size_t(row) * kG + n] = v;
+    const int Ja = h ? P.nyA - 1 - J : J;
+    if (out) out[size_t(Ja) * P.nx + row] = v;
+    if (out2) out2[size_t(Ja) * P.nx + row] = v + g2;
+  };
+  const int2* band = kUpper ? P.bandPsi : P.bandPhi;
+  auto window = [&](int pidx) { return band[size_t(pidx) * kSl + s]; };
+  auto copy_a = [&](int gr, int J, int2 wn) {  // thread 0: this slice's window of the operator row
+    const int pidx = propidx(kUpper, gr, gi, J, P);
+    tma_load(As, Mbase + size_t(pidx) * mstride + size_t(wn.x) * 64, uint32_t(sizeof(double) * 64 * 8 * wn.y), barA);
+  };
+  // this warp's k-range of the slots of (virtual group gv, group step st) -> its part of Bs[buf]
+  auto prefetch = [&](int buf, int gv, int st, int2 wn) {
+    const unsigned long long* src = P.ll + (size_t(gv) * P.ngr + st) * (KN * kG) + size_t(wn.x + warp * wn.y) * 32 + 2 * lane;
+    const uint32_t dst = tma::smem_u32(Bs0 + buf * bsz + size_t(warp) * wmax * 32 + 2 * lane);
+    const int npairs = wn.y >> 1;
+    for (int q = 0; q < npairs; ++q)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + uint32_t(q) * 512),
+                   "l"(__cvta_generic_to_global(src + q * 64))
+                   : "memory");
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  // the prefetched pairs have landed: those that still hold the sentinel are polled as in
+  // v6_chain_kernel (up to 8 loads in flight per lane, only the incomplete pairs re-issued)
+  auto complete = [&](int buf, int gv, int st, int2 wn) {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    const unsigned long long* src = P.ll + (size_t(gv) * P.ngr + st) * (KN * kG) + size_t(wn.x + warp * wn.y) * 32 + 2 * lane;
+    double* dstB = Bs0 + buf * bsz + size_t(warp) * wmax * 32 + 2 * lane;
+    const int npairs = wn.y >> 1;
+#pragma unroll 1
+    for (int q0 = 0; q0 < npairs; q0 += 4) {
+      unsigned pending = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q0 + u < npairs) {
+          const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(dstB + (q0 + u) * 64);
+          if (v.x == kLLEmpty || v.y == kLLEmpty) pending |= 1u << u;
+        }
+      if (P.nopoll) pending = 0;
+      while (pending) {
+        ulonglong2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if ((pending >> u) & 1u) v[u] = ld_slots(src + (q0 + u) * 64);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (((pending >> u) & 1u) && v[u].x != kLLEmpty && v[u].y != kLLEmpty) {
+            *reinterpret_cast<ulonglong2*>(dstB + (q0 + u) * 64) = v[u];
+            pending &= ~(1u << u);
+          }
+      }
+    }
+    __syncwarp();
+  };
+  int2 wn_next = make_int2(0, 2);
+  if (threadIdx.x == 0) {
+    mbar_init(barA, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  {  // group 0 has no inflow: its rows are the zero-inflow chain values
+    const int J = Jof(0);
+    if (J < 0) return;
+    if (outt)
+      for (int h = 0; h < nh; ++h) emit(h, 0, J, __ldcg(P.W1 + widx<KN>(g + h * P.nreal, J, ny) + size_t(row) * kG + n));
+    if (P.ngr > 1 && Jof(1) >= 0) {
+      wn_next = window(propidx(kUpper, 1, gi, Jof(1), P));
+      if (threadIdx.x == 0) copy_a(1, Jof(1), wn_next);
+      // Two CTAs share an SM and its fp64 pipe.  Chain groups are independent, but launched
+      // together they run in phase: both CTAs multiply at once and wait at once.  Starting the
+      // later half of the wave's groups (the second CTA of each SM) half a product later puts one
+      // CTA's product into the other's handoff wait.
+      if (P.phase_ns && g - P.g0 >= (P.gwave + 1) / 2) __nanosleep(P.phase_ns);
+      prefetch(0, g, 0, wn_next);
+    }
+  }
+  const int bo = (lane & 3) * kG + (lane >> 2);
+  const bool tm = P.tim && blockIdx.x == kSl / 2 && threadIdx.x == 0;
+  long long ts[7] = {0, 0, 0, 0, 0, 0, 0}, acc[6] = {0, 0, 0, 0, 0, 0};
+  int rb = 0, buf = 0;
+  for (int idx = 1; idx < P.ngr; ++idx) {
+    const int J = Jof(idx);
+    if (J < 0) break;
+    const int2 wn = wn_next;
+    const bool more = idx + 1 < P.ngr && Jof(idx + 1) >= 0;
+    if (more) wn_next = window(propidx(kUpper, idx + 1, gi, Jof(idx + 1), P));
+    const uint32_t par = uint32_t(idx - 1) & 1u;
+    for (int h = 0; h < nh; ++h) {
+      const int gv = g + h * P.nreal;
+      if (tm) ts[0] = clock64();
+      double cval = 0.0;
+      if (outt) cval = __ldcg(P.W1 + widx<KN>(gv, J, ny) + size_t(row) * kG + n);
+      complete(buf, gv, idx - 1, wn);
+      if (tm) ts[1] = ts[2] = clock64();
+      // the other half of this row was published a whole product ago: fetch it under this product
+      const bool early = h + 1 < nh;
+      if (early) prefetch(buf ^ 1, g + (h + 1) * P.nreal, idx - 1, wn);
+      if (h == 0) mbar_wait(barA, par);  // the operator slice serves both halves
+      if (tm) ts[3] = clock64();
+      double d[2][2][2] = {};
+      const double* Aw = As + size_t(warp * wn.y) * 64 + lane;
+      const double* Bw = Bs0 + buf * bsz + size_t(warp) * wmax * 32 + bo;
+#pragma unroll 1
+      for (int i0 = 0; i0 < wn.y; i0 += 8) {
+        double a0[8], a1[8], b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const bool ok = i0 + u < wn.y;
+          a0[u] = ok ? Aw[(i0 + u) * 64] : 0.0;
+          a1[u] = ok ? Aw[(i0 + u) * 64 + 32] : 0.0;
+          b[u] = ok ? Bw[(i0 + u) * 4 * kG] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (i0 + u < wn.y) {
+            dmma6(d[u & 1][0][0], d[u & 1][0][1], a0[u], b[u]);
+            dmma6(d[u & 1][1][0], d[u & 1][1][1], a1[u], b[u]);
+          }
+        }
+      }
+      // the next row's first half was published during this row: fetch it under the reduction and the stores
+      if (!early && more) prefetch(buf ^ 1, g, idx, wn_next);
+      double* redw = red + rb * (8 * 128);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) redw[warp * 128 + (mt * 32 + lane) * 2 + e] = d[0][mt][e] + d[1][mt][e];
+      if (tm) ts[4] = clock64();
+      __syncthreads();  // As consumed by every warp (last half), red[rb] complete
+      if (outt) emit(h, idx, J, cval + reduce8(redw, threadIdx.x));
+      rb ^= 1;
+      buf ^= 1;
+      if (tm) {
+        ts[5] = ts[6] = clock64();
+        for (int q = 0; q < 6; ++q) acc[q] += ts[q + 1] - ts[q];
+      }
+    }
+    if (more && threadIdx.x == 0) copy_a(idx + 1, Jof(idx + 1), wn_next);
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  if (tm)
+    for (int q = 0; q < 6; ++q) atomicAdd(reinterpret_cast<unsigned long long*>(P.tim + (kUpper ? 6 : 0) + q),
+                                          (unsigned long long)acc[q]);
+}
+
+// The middle row of the twisted elimination: one dense block product per real chain group with
+// packed operator rows, CTA (s, g) = 16 rows x 8 chains, 8 warps split along k (fixed-order sum).
+//   mode 0 (between the inward and the outward chains):
+//     x_M = Dm^{-1} b_M + E (y_{M-1} + y'_{M+1})  ->  Wm (x_M) and the job's out planes at row M
+//   mode 1 (after the outward off-chain products d_j = Ui_j y_j):
+//     d_{M-1} += H_{M-1} x_M for both halves: the inflow of the first outward row
+template <int KN>
+__global__ void __launch_bounds__(kThr6) v6_mid_kernel(V6Params P, int mode) {
+  V6_DIMS
+  __shared__ double red[8 * 128];
+  const int s = blockIdx.x % kSl, g = blockIdx.x / kSl;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bo = (lane & 3) * kG + (lane >> 2);
+  const int M = P.ny;  // rows per half chain = the middle block row
+  const size_t vec = size_t(KN) * kG;
+  double* xm = P.Wm + size_t(P.nreal) * vec + size_t(g) * vec;
+  double d[2][2] = {};
+  auto prod = [&](const double* A, const double* in1, const double* in2) {
+    const double* Aw = A + size_t(s) * kKS * 64 + lane;
+#pragma unroll 4
+    for (int i = 0; i < kKW; ++i) {
+      const int ks = warp * kKW + i;
+      const double a0 = __ldg(Aw + size_t(ks) * 64), a1 = __ldg(Aw + size_t(ks) * 64 + 32);
+      double b = __ldcg(in1 + size_t(4 * ks) * kG + bo);
+      if (in2) b += __ldcg(in2 + size_t(4 * ks) * kG + bo);
+      dmma6(d[0][0], d[0][1], a0, b);
+      dmma6(d[1][0], d[1][1], a1, b);
+    }
+  };
+  if (mode == 0) {
+    prod(P.Dm, P.Wm + size_t(g) * vec, nullptr);
+    prod(P.Em, P.W0 + widx<KN>(g, M - 1, M), P.W0 + widx<KN>(g + P.nreal, M - 1, M));
+  } else {
+    prod(P.Hp + size_t(oprow(M - 1, P.jstar)) * kSl * kKS * 64, xm, nullptr);
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) red[warp * 128 + (mt * 32 + lane) * 2 + e] = d[mt][e];
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    int m, n;
+    slice_coords(threadIdx.x, m, n);
+    const int row = 16 * s + m, ch = g * kG + n;
+    const double v = reduce8(red, threadIdx.x);
+    if (mode == 0) {
+      xm[size_t(row) * kG + n] = v;
+      if (row < P.nx && ch < P.nchains) {
+        const FastStep st = P.jobs[size_t(ch) * P.nsteps + P.t];
+        if (st.in) {
+          if (st.out) st.out[size_t(M) * P.nx + row] = v;
+          if (st.out2) {
+            double g2 = 0.0;
+            if (st.node2 > 0 && P.gam) g2 = P.gam[st.node2];
+            st.out2[size_t(M) * P.nx + row] = v + g2;
+          }
+        }
+      }
+    } else {
+      P.W1[widx<KN>(g, M - 1, M) + size_t(row) * kG + n] += v;
+      P.W1[widx<KN>(g + P.nreal, M - 1, M) + size_t(row) * kG + n] += v;
+    }
+  }
 }
 
 // dev[2J + m] = max |M_J - M_{ny-1}|, mag[2J + m] = max |M_J|, M = Li (m = 0), Ui (m = 1)
@@ -867,11 +1188,13 @@ void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   V6Params p = P;
+  p.gwave = ngroups_wave;
   void* args[] = {&p};
   const bool win = P.ll && P.bandPhi;
+  if (win) cfg.dynamicSmemBytes = chainw_smem<KN>(P.wmax);
   const void* fn =
-      win ? (upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true, true, true>)
-                   : reinterpret_cast<const void*>(&v6_chain_kernel<KN, false, true, true>))
+      win ? (upper ? reinterpret_cast<const void*>(&v6_chainw_kernel<KN, true>)
+                   : reinterpret_cast<const void*>(&v6_chainw_kernel<KN, false>))
           : P.ll ? (upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true, true, false>)
                           : reinterpret_cast<const void*>(&v6_chain_kernel<KN, false, true, false>))
                  : (upper ? reinterpret_cast<const void*>(&v6_chain_kernel<KN, true, false, false>)
@@ -891,8 +1214,8 @@ int chain_capacity() {
     KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
     KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
     KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
-    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
-    KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chainw_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chainw_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
@@ -914,8 +1237,8 @@ int chain_capacity() {
     KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, v6_chain_kernel<KN, true, false, false>, kThr6, cs));
     KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q0, v6_chain_kernel<KN, false, true, false>, kThr6, cs));
     KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q1, v6_chain_kernel<KN, true, true, false>, kThr6, cs));
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r0, v6_chain_kernel<KN, false, true, true>, kThr6, cs));
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, v6_chain_kernel<KN, true, true, true>, kThr6, cs));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r0, v6_chainw_kernel<KN, false>, kThr6, cs));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, v6_chainw_kernel<KN, true>, kThr6, cs));
     p0 = std::min(p0, std::min(q0, r0));
     p1 = std::min(p1, std::min(q1, r1));
     int dev = 0, nsm = kSmCount;
@@ -942,15 +1265,20 @@ void pack(Ctx* c, const double* src, int nJ, double scale, double* dst) {
 
 template <int KN>
 void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
+  V6_DIMS
+  // ngroups: (virtual) chain groups of the block vectors; the chain grid covers the REAL groups
+  const int nchain_groups = P.twist ? P.nreal : ngroups;
   const int gpw = groups_per_wave<KN>(P.k);
   const int og = std::min(P.ny, kSmCount);
   const int npairs = (ngroups + 1) / 2;
   for (int t = 0; t < nsteps; ++t) {
     P.t = t;
     P.g0 = 0;
-    KKT_LAUNCH(c, v6_form_b_kernel<KN>, kSmCount * 8, 256, 0, P);
+    KKT_LAUNCH(c, v6_form_b_kernel<KN>, (ngroups * P.ny + (P.twist ? P.nreal : 0)) * (KN / kFbChunk), kFbChunk, 0, P);
     for (int dir = 0; dir < 2; ++dir) {
       const bool up = dir == 1;
+      if (up && P.twist)  // the two eliminations meet: x_M
+        KKT_LAUNCH(c, v6_mid_kernel<KN>, kSl * P.nreal, kThr6, 0, P, 0);
       if (off_plain() || KN == 256) {  // 256-blocks: one small copy per slice, plain loads measured ahead
         if (up)
           KKT_LAUNCH(c, (v6_off_kernel<KN, true>), og, kThr6, off_smem<KN>(), P);
@@ -975,6 +1303,8 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
             KKT_LAUNCH(c, (v6_off2_kernel<KN, false, 2>), og, kOffThr, (off2_smem<KN, 2>()), P);
         }
       }
+      if (up && P.twist)  // the inflow of the first outward row: d_{M-1} += H_{M-1} x_M
+        KKT_LAUNCH(c, v6_mid_kernel<KN>, kSl * P.nreal, kThr6, 0, P, 1);
       for (int i = 1; i < P.k; ++i) {  // zero-inflow chains inside the groups, every group at once
         P.pass = i;
         if (up && P.rawH)
@@ -986,14 +1316,18 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
         else
           KKT_LAUNCH(c, (v6_inner_kernel<KN, false, false>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
       }
-      KKT_CUDA(cudaMemsetAsync(P.cnt, 0, sizeof(unsigned) * ngroups, c->stream));
-      if (P.ll)  // every handoff slot of this sweep direction back to "empty"
-        KKT_CUDA(cudaMemsetAsync(P.ll, 0xFF, sizeof(unsigned long long) * size_t(ngroups) * P.ngr * KN * kG, c->stream));
-      for (int g0 = 0; g0 < ngroups; g0 += gpw) {
+      if (P.ll)  // every handoff slot of this sweep direction back to "empty", right before the chain: the
+                 // slots are then L2-resident when the chain polls them (refilled a step early, from
+                 // v6_form_b_kernel, they had gone cold: config 2 114 -> 127 ms)
+        KKT_CUDA(cudaMemsetAsync(P.ll, 0xFF, sizeof(unsigned long long) * P.nll, c->stream));
+      else
+        KKT_CUDA(cudaMemsetAsync(P.cnt, 0, sizeof(unsigned) * ngroups, c->stream));  // counter handoff
+      for (int g0 = 0; g0 < nchain_groups; g0 += gpw) {
         P.g0 = g0;
-        launch_chain<KN>(c, up, P, std::min(gpw, ngroups - g0));
+        launch_chain<KN>(c, up, P, std::min(gpw, nchain_groups - g0));
       }
     }
+    if (c->step_hook) c->step_hook(t);  // every output of step t is written (stream order)
   }
 }
 
@@ -1018,7 +1352,7 @@ bool v6_supported(const Ctx* c) {
 // which stay in L2, and only jstar + 1 operator rows are packed.  jstar is the
 // first row from which Li and Ui (and so G, H) stay within tol * max|M| of the
 // last row's (KKT_V6_JTOL, default 1e-15; 0 disables); none: ny.
-static int v6_find_jstar(Ctx* c) {
+static int v6_find_jstar(Ctx* c, int nyv) {  // nyv: block rows the chains run over (ny, or the half chain's)
   const int nx = c->nx, ny = c->ny;
   static const char* jt = std::getenv("KKT_V6_JTOL");
   const double tol = jt ? std::atof(jt) : 1e-15;
@@ -1034,12 +1368,25 @@ static int v6_find_jstar(Ctx* c) {
          hd[2 * (first - 1) + 1] <= tol * hm[2 * (ny - 1) + 1])
     --first;
   const int js = first + 1;  // G_J needs Li_J and Ui_{J-1}
-  return js <= ny - 2 ? js : ny;
+  return js <= nyv - 2 ? js : nyv;
+}
+
+// slot handoff instead of the release counter + bulk copy.  KKT_V6_LL=0/1 forces the choice.
+static bool v6_ll_enabled() {
+  static const char* ll_env = std::getenv("KKT_V6_LL");
+  return ll_env ? std::atoi(ll_env) != 0 : true;
 }
 
 void build_v6(Ctx* c) {
-  const int nx = c->nx, ny = c->ny;
-  c->v6_jstar = v6_find_jstar(c);
+  const int nx = c->nx, nyA = c->ny;
+  // Two-sided (twisted) elimination for odd ny >= 3 (every BASELINE grid): two half-length chains
+  // per spatial solve that meet in the middle block row; needs the slot handoff.  KKT_V6_TWIST=0: off.
+  static const char* tw_env = std::getenv("KKT_V6_TWIST");
+  const bool twist = (tw_env ? std::atoi(tw_env) != 0 : true) && v6_ll_enabled() && nyA >= 3 && (nyA & 1);
+  const int ny = twist ? (nyA - 1) / 2 : nyA;  // block rows of a (half) chain: every "ny" below
+  c->v6_twist = twist;
+  c->v6_nyv = ny;
+  c->v6_jstar = v6_find_jstar(c, ny);
   const int nops = std::min(ny, c->v6_jstar + 1);  // packed operator rows
   if (std::getenv("KKT_V6_TIM")) std::fprintf(stderr, "v6 jstar %d of ny %d\n", c->v6_jstar, ny);
   const int kn = nx <= 255 ? 256 : nx <= 511 ? 512 : 1024;
@@ -1062,10 +1409,11 @@ void build_v6(Ctx* c) {
   pk(c->Li.p, nops, 1.0, Lp);
   pk(c->Ui.p, nops, 1.0, Up);
   KKT_CUDA(cudaMemsetAsync(Gp, 0, sizeof(double) * mat, c->stream));  // G_0: unused
-  if (nops == ny)
+  if (nops == ny && !twist)
     KKT_CUDA(cudaMemsetAsync(Hp + size_t(ny - 1) * mat, 0, sizeof(double) * mat, c->stream));  // H_{ny-1}
-  const int nh = std::min(nops, ny - 1);  // H_J rows computed
-  const int Jb = std::min(ny - 1, 32);
+  // H_J rows computed (twisted: H_{M-1} exists and carries x_M into the first outward row)
+  const int nh = twist ? nops : std::min(nops, ny - 1);
+  const int Jb = std::max(1, std::min(ny - 1, 32));
   DBuf<double> T(size_t(Jb) * nn);
   for (int J0 = 1; J0 < nops; J0 += Jb) {  // G_J = cy Li_J Ui_{J-1}
     const int nb = std::min(Jb, nops - J0);
@@ -1108,10 +1456,21 @@ void build_v6(Ctx* c) {
     KKT_CUDA(cudaMemcpyAsync(h.data(), dev, sizeof(int2) * n, cudaMemcpyDeviceToHost, c->stream));
     KKT_CUDA(cudaStreamSynchronize(c->stream));
     double sum = 0.0;
-    for (const int2& w : h) sum += w.y;
+    int wmax = 2;
+    for (const int2& w : h) {
+      sum += w.y;
+      wmax = std::max(wmax, w.y);
+    }
+    c->v6_wmax = wmax;
     const double frac = sum / (double(n) * (kn / 32));
-    if (std::getenv("KKT_V6_TIM")) std::fprintf(stderr, "v6 band windows: %.0f%% of the k-steps\n", 100.0 * frac);
-    return frac < bfrac;
+    // the windowed chain keeps only the window in shared memory (v6_chainw_kernel) and must not
+    // take more of it than the full-row kernel does (same CTAs per SM)
+    const size_t wsm = kn == 256 ? chainw_smem<256>(wmax) : kn == 512 ? chainw_smem<512>(wmax) : chainw_smem<1024>(wmax);
+    const size_t fsm = kn == 256 ? chain_smem<256>() : kn == 512 ? chain_smem<512>() : chain_smem<1024>();
+    if (std::getenv("KKT_V6_TIM"))
+      std::fprintf(stderr, "v6 band windows: %.0f%% of the k-steps, widest %d k-steps per warp (%zu KB shared)\n", 100.0 * frac, wmax,
+                   wsm >> 10);
+    return frac < bfrac && wsm <= fsm;
   };
   c->v6_band_on = windows_pay(c->v6_band.p, size_t(2) * nops * ksl);
   {  // the raw ranges likewise: k-steps kept, relative to the triangle (Li, Ui) or the full row (G, H)
@@ -1133,6 +1492,16 @@ void build_v6(Ctx* c) {
         std::fprintf(stderr, "v6 band of %s: %.0f%% of the k-steps\n", set == 0 ? "Li" : set == 1 ? "Ui" : set == 2 ? "G" : "H",
                      100.0 * kept / std::max(1.0, full));
     }
+  }
+
+  if (twist) {  // the middle block row: Dm^{-1} and E = cy Dm^{-1} Ui_{M-1}, packed like the operator rows
+    DBuf<double> Dinv(nn), E(nn);
+    build_twist_middle(c, ny, Dinv.p, E.p);
+    c->v6_mid.alloc(2 * mat);
+    pk(Dinv.p, 1, 1.0, c->v6_mid.p);
+    pk(E.p, 1, 1.0, c->v6_mid.p + mat);
+    KKT_CUDA(cudaStreamSynchronize(c->stream));  // the temporaries are freed here
+    if (std::getenv("KKT_V6_TIM")) std::fprintf(stderr, "v6 twisted elimination: %d rows per half chain, middle row %d\n", ny, ny);
   }
 
   // ---- k-row grouping: as many rows per handoff as co-resident CTAs allow for the RASQ chains
@@ -1203,14 +1572,17 @@ void build_v6(Ctx* c) {
 }
 
 void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool coarse_terms) {
-  const int ny = c->ny;
+  const bool twist = c->v6_twist;
+  const int ny = c->v6_nyv;  // block rows of a (half) chain
   const int kn = c->v6_kn;
   const size_t mat = size_t(kn) * kn;
-  const int ngroups = (nchains + kG - 1) / kG;
+  const int nreal = (nchains + kG - 1) / kG;
+  const int ngroups = twist ? 2 * nreal : nreal;  // (virtual) chain groups of the block vectors
   const size_t need = size_t(ngroups) * ny * kn * kG;
-  if (c->v6_w.n < 2 * need || c->v6_cnt.n < size_t(ngroups)) {
+  const size_t midv = twist ? size_t(2) * nreal * kn * kG : 0;  // b_M and x_M
+  if (c->v6_w.n < 2 * need + midv || c->v6_cnt.n < size_t(ngroups)) {
     KKT_CUDA(cudaStreamSynchronize(c->stream));
-    c->v6_w.alloc(2 * need);
+    c->v6_w.alloc(2 * need + midv);
     c->v6_cnt.alloc(ngroups);
   }
   V6Params P;
@@ -1228,6 +1600,20 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.ny = ny;
   P.nchains = nchains;
   P.ngroups = ngroups;
+  P.twist = twist ? 1 : 0;
+  P.wmax = c->v6_wmax;
+  {
+    static const int spin = std::getenv("KKT_V6_SPIN_NS") ? std::atoi(std::getenv("KKT_V6_SPIN_NS")) : 0;
+    P.spin_ns = spin;
+    static const int phase = std::getenv("KKT_V6_PHASE_NS") ? std::atoi(std::getenv("KKT_V6_PHASE_NS")) : 0;
+    P.phase_ns = phase;
+    P.gwave = 0;
+  }
+  P.nyA = c->ny;
+  P.nreal = nreal;
+  P.Wm = c->v6_w.p + 2 * need;
+  P.Dm = twist ? c->v6_mid.p : nullptr;
+  P.Em = twist ? c->v6_mid.p + mat : nullptr;
   P.a1 = c->a1.p;
   P.a2 = c->a2.p;
   P.gam = c->gam.p;
@@ -1236,10 +1622,13 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.cnt = c->v6_cnt.p;
   P.k = c->v6_k;
   P.ngr = (ny + P.k - 1) / P.k;
-  // slot handoff instead of the release counter + bulk copy.  KKT_V6_LL=0/1 forces the choice.
-  static const char* ll_env = std::getenv("KKT_V6_LL");
-  const bool ll_on = ll_env ? std::atoi(ll_env) != 0 : true;
+  const bool ll_on = v6_ll_enabled();
   P.ll = nullptr;
+  P.nll = 0;
+  {
+    static const bool np = std::getenv("KKT_V6_NOPOLL") != nullptr;
+    P.nopoll = np ? 1 : 0;
+  }
   if (ll_on) {
     const size_t npk = size_t(ngroups) * P.ngr * kn * kG;
     if (c->v6_ll.n < npk) {
@@ -1247,6 +1636,7 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
       c->v6_ll.alloc(npk);
     }
     P.ll = c->v6_ll.p;
+    P.nll = npk;
   }
   P.nind = c->v6_nind;
   P.gconv = c->v6_gconv;
@@ -1286,7 +1676,7 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
     KKT_CUDA(cudaStreamSynchronize(c->stream));
     const double rows = double(ny - 1) * nsteps;
     for (int u = 0; u < 2; ++u)
-      std::fprintf(stderr, "v6 %s cycles/row (CTA 0): poll %.0f waitA %.0f waitB %.0f mma %.0f emit %.0f signal %.0f\n",
+      std::fprintf(stderr, "v6 %s cycles/row (middle slice of group 0): poll %.0f waitA %.0f waitB %.0f mma %.0f emit %.0f signal %.0f\n",
                    u ? "U" : "L", h[6 * u] / rows, h[6 * u + 1] / rows, h[6 * u + 2] / rows, h[6 * u + 3] / rows,
                    h[6 * u + 4] / rows, h[6 * u + 5] / rows);
   }
