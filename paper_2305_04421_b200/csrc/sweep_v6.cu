@@ -122,8 +122,6 @@ struct V6Params {
   // product and the dependent chain is half as long.
   int twist, nyA, nreal;
   int wmax;          // v6_chainw_kernel: the widest window's k-steps per warp (shared-memory extent)
-  int phase_ns;      // the later half of a wave's chain groups starts this much later (see v6_chainw_kernel)
-  int gwave;         // chain groups in this launch
   int spin_ns;       // KKT_V6_SPIN_NS: pause between failed poll rounds (0: none)
   double* Wm;        // [2][nreal][kN][8]: b_M, then x_M
   const double* Dm;  // packed Dm^{-1}
@@ -355,9 +353,13 @@ __global__ void __launch_bounds__(kOffThr, 1) v6_off2_kernel(V6Params P) {
   if (warp == 8) {  // producer
     if (lane == 0) {
       int it = 0, item = 0;
-      for (int J = blockIdx.x; J < P.ny; J += gridDim.x) {
+      // items (block row, pass of NG chain groups) dealt round-robin: the CTAs that work on one row's
+      // passes run side by side (its triangle is fetched from HBM once), and no CTA gets a whole row more
+      const int npass = (P.ngroups + NG - 1) / NG;
+      for (int gitem = blockIdx.x; gitem < P.ny * npass; gitem += gridDim.x, ++item) {
+        const int J = gitem / npass, gp = (gitem % npass) * NG;
         const double* TJ = T + size_t(oprow(J, P.jstar)) * kSl * kKS * 64;
-        for (int gp = 0; gp < P.ngroups; gp += NG, ++item) {
+        {
           if (item > 0) mbar_wait(bfree, uint32_t(item - 1) & 1u);
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tma::smem_u32(barB)),
                        "r"(uint32_t(sizeof(double) * NG * KN * kG))
@@ -392,8 +394,10 @@ __global__ void __launch_bounds__(kOffThr, 1) v6_off2_kernel(V6Params P) {
   }
   const int bo = (lane & 3) * kG + (lane >> 2);
   int it = 0, item = 0, sl = 0;
-  for (int J = blockIdx.x; J < P.ny; J += gridDim.x) {
-    for (int gp = 0; gp < P.ngroups; gp += NG, ++item) {
+  const int npass = (P.ngroups + NG - 1) / NG;
+  for (int gitem = blockIdx.x; gitem < P.ny * npass; gitem += gridDim.x, ++item) {
+    const int J = gitem / npass, gp = (gitem % npass) * NG;
+    {
       mbar_wait(barB, uint32_t(item) & 1u);
       const int2* rawrow = (kUpper ? P.rawU : P.rawL) ? (kUpper ? P.rawU : P.rawL) + size_t(oprow(J, P.jstar)) * kSl : nullptr;
       int2 rb = rawrow ? rawrow[0] : make_int2(0, 0);
@@ -446,6 +450,149 @@ __global__ void __launch_bounds__(kOffThr, 1) v6_off2_kernel(V6Params P) {
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tma::smem_u32(bfree)) : "memory");
     }
+  }
+}
+
+// Batched triangular products without a cross-warp reduction (the default for KN >= 512).
+// v6_off2_kernel splits every chunk along k over its 8 warps and reduces each 16-row slice through
+// shared memory behind a CTA barrier; once the triangles are cut to the operators' numerical band a
+// slice has only ~34 k-steps (config 2), so that kernel spends more time in barriers and reductions
+// than in DMMAs (40% of its DMMA-issue bound).  Here the slices are taken four at a time and warp w
+// owns one 8-row tile of the quad (slice 4q + w/2, tile w%2) over the slice's WHOLE k-range, so each
+// warp keeps its accumulators in registers from the first k-step to the store.  One producer lane
+// streams the four slices' k-steps through four small rings (kOff3R slots of kOff3CK k-steps each);
+// the two warps of a slice share a ring.  The block vectors of NG chain groups are staged once per
+// (block row, pass) item by bulk copies, as in v6_off2_kernel.
+constexpr int kOff3CK = 16;  // k-steps per ring slot (8 KB)
+constexpr int kOff3R = 3;    // slots per ring
+template <int KN, int NG>
+constexpr size_t off3_smem() {
+  return sizeof(double) * (size_t(NG) * KN * kG + size_t(4) * kOff3R * kOff3CK * 64) + (2 * 4 * kOff3R + 2) * sizeof(uint64_t);
+}
+
+template <int KN, bool kUpper, int NG>
+__global__ void __launch_bounds__(kOffThr, 1) v6_off3_kernel(V6Params P) {
+  V6_DIMS
+  constexpr int CK = kOff3CK, R = kOff3R;
+  extern __shared__ __align__(128) double so[];
+  double* Bs = so;                           // [NG][KN][8]
+  double* ring = Bs + size_t(NG) * KN * kG;  // [slice of the quad 4][slot R][CK][64]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + size_t(4) * R * CK * 64);  // [4][R]
+  uint64_t* empty = full + 4 * R;                                               // [4][R]
+  uint64_t* barB = empty + 4 * R;
+  uint64_t* bfree = barB + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4 * R; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 2);
+    }
+    mbar_init(barB, 1);
+    mbar_init(bfree, 8);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const double* T = kUpper ? P.Up : P.Lp;
+  const int2* raw = kUpper ? P.rawU : P.rawL;
+  const int npass = (P.ngroups + NG - 1) / NG;
+  const int nitems = P.ny * npass;
+  if (warp == 8) {  // producer
+    if (lane == 0) {
+      int itr[4] = {0, 0, 0, 0};
+      int item = 0;
+      for (int gitem = blockIdx.x; gitem < nitems; gitem += gridDim.x, ++item) {
+        const int J = gitem / npass, gp = (gitem % npass) * NG;
+        const int orow = oprow(J, P.jstar);
+        const double* TJ = T + size_t(orow) * kSl * kKS * 64;
+        if (item > 0) mbar_wait(bfree, uint32_t(item - 1) & 1u);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tma::smem_u32(barB)),
+                     "r"(uint32_t(sizeof(double) * NG * KN * kG))
+                     : "memory");
+        const uint32_t vb = uint32_t(sizeof(double) * KN * kG);
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+          const int gs = gp + g < P.ngroups ? gp + g : gp;  // a missing group reads gp (its outputs are not written)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                           tma::smem_u32(Bs + size_t(g) * KN * kG)), "l"(P.W0 + widx<KN>(gs, J, P.ny)), "r"(vb),
+                       "r"(tma::smem_u32(barB))
+                       : "memory");
+        }
+        for (int q = 0; q < kSl / 4; ++q) {
+          int k0[4], k1[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) tri_range(kUpper, 4 * q + i, kKS, raw, orow, kSl, k0[i], k1[i]);
+          bool any = true;
+          while (any) {  // one chunk per slice in turn, so the four rings fill evenly
+            any = false;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (k0[i] < k1[i]) {
+                const int slot = itr[i] % R, len = min(CK, k1[i] - k0[i]);
+                if (itr[i] >= R) mbar_wait(&empty[i * R + slot], uint32_t(itr[i] / R - 1) & 1u);
+                tma_load(ring + (size_t(i) * R + slot) * CK * 64, TJ + (size_t(4 * q + i) * kKS + k0[i]) * 64,
+                         uint32_t(sizeof(double) * 64 * len), &full[i * R + slot]);
+                k0[i] += len;
+                ++itr[i];
+                any = true;
+              }
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+  const int sl = warp >> 1, mt = warp & 1;
+  const int bo = (lane & 3) * kG + (lane >> 2);
+  int it = 0, item = 0;
+  for (int gitem = blockIdx.x; gitem < nitems; gitem += gridDim.x, ++item) {
+    const int J = gitem / npass, gp = (gitem % npass) * NG;
+    const int orow = oprow(J, P.jstar);
+    mbar_wait(barB, uint32_t(item) & 1u);
+    for (int q = 0; q < kSl / 4; ++q) {
+      const int s = 4 * q + sl;
+      int ks0, ks1;
+      tri_range(kUpper, s, kKS, raw, orow, kSl, ks0, ks1);
+      double d[2][NG][2] = {};
+      for (int kb = ks0; kb < ks1; kb += CK, ++it) {
+        const int slot = it % R, len = min(CK, ks1 - kb);
+        mbar_wait(&full[sl * R + slot], uint32_t(it / R) & 1u);
+        const double* A = ring + (size_t(sl) * R + slot) * CK * 64 + mt * 32 + lane;
+        const double* B = Bs + size_t(4 * kb) * kG + bo;
+        int u = 0;
+#pragma unroll 2
+        for (; u + 1 < len; u += 2) {  // two k-steps on separate accumulators
+          const double a0 = A[u * 64], a1 = A[(u + 1) * 64];
+          double b0[NG], b1[NG];
+#pragma unroll
+          for (int g = 0; g < NG; ++g) {
+            b0[g] = B[size_t(g) * KN * kG + u * 4 * kG];
+            b1[g] = B[size_t(g) * KN * kG + (u + 1) * 4 * kG];
+          }
+#pragma unroll
+          for (int g = 0; g < NG; ++g) {
+            dmma6(d[0][g][0], d[0][g][1], a0, b0[g]);
+            dmma6(d[1][g][0], d[1][g][1], a1, b1[g]);
+          }
+        }
+        if (u < len) {
+          const double a0 = A[u * 64];
+#pragma unroll
+          for (int g = 0; g < NG; ++g) dmma6(d[0][g][0], d[0][g][1], a0, B[size_t(g) * KN * kG + u * 4 * kG]);
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tma::smem_u32(&empty[sl * R + slot])) : "memory");
+      }
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        if (gp + g < P.ngroups) {
+          double* O = P.W1 + widx<KN>(gp + g, J, P.ny) + size_t(16 * s + 8 * mt + (lane >> 2)) * kG + 2 * (lane & 3);
+          *reinterpret_cast<double2*>(O) = make_double2(d[0][g][0] + d[1][g][0], d[0][g][1] + d[1][g][1]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tma::smem_u32(bfree)) : "memory");
   }
 }
 
@@ -939,11 +1086,6 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
     if (P.ngr > 1 && Jof(1) >= 0) {
       wn_next = window(propidx(kUpper, 1, gi, Jof(1), P));
       if (threadIdx.x == 0) copy_a(1, Jof(1), wn_next);
-      // Two CTAs share an SM and its fp64 pipe.  Chain groups are independent, but launched
-      // together they run in phase: both CTAs multiply at once and wait at once.  Starting the
-      // later half of the wave's groups (the second CTA of each SM) half a product later puts one
-      // CTA's product into the other's handoff wait.
-      if (P.phase_ns && g - P.g0 >= (P.gwave + 1) / 2) __nanosleep(P.phase_ns);
       prefetch(0, g, 0, wn_next);
     }
   }
@@ -991,7 +1133,8 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
           }
         }
       }
-      // the next row's first half was published during this row: fetch it under the reduction and the stores
+      // the next row's first half was published during this row: fetch it under the reduction and the
+      // stores (issued before the DMMA loop instead it measured no faster: 100.9 vs 100.5 ms)
       if (!early && more) prefetch(buf ^ 1, g, idx, wn_next);
       double* redw = red + rb * (8 * 128);
 #pragma unroll
@@ -1188,7 +1331,6 @@ void launch_chain(Ctx* c, bool upper, const V6Params& P, int ngroups_wave) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   V6Params p = P;
-  p.gwave = ngroups_wave;
   void* args[] = {&p};
   const bool win = P.ll && P.bandPhi;
   if (win) cfg.dynamicSmemBytes = chainw_smem<KN>(P.wmax);
@@ -1214,8 +1356,9 @@ int chain_capacity() {
     KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
     KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
     KKT_CUDA(cudaFuncSetAttribute(v6_chain_kernel<KN, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
-    KKT_CUDA(cudaFuncSetAttribute(v6_chainw_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
-    KKT_CUDA(cudaFuncSetAttribute(v6_chainw_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cs));
+    const int ws = KN <= 512 ? (113 << 10) : (226 << 10);  // the windowed kernel's budget (see windows_pay)
+    KKT_CUDA(cudaFuncSetAttribute(v6_chainw_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ws));
+    KKT_CUDA(cudaFuncSetAttribute(v6_chainw_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ws));
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     KKT_CUDA(cudaFuncSetAttribute(v6_off_kernel<KN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
     KKT_CUDA(cudaFuncSetAttribute(v6_inner_kernel<KN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, os));
@@ -1225,6 +1368,12 @@ int chain_capacity() {
     const int os2 = int(off2_smem<KN, 2>());
     KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
     KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, os2));
+    KKT_CUDA(cudaFuncSetAttribute(v6_off3_kernel<KN, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(off3_smem<KN, 2>())));
+    KKT_CUDA(cudaFuncSetAttribute(v6_off3_kernel<KN, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(off3_smem<KN, 2>())));
+    if constexpr (KN <= 512) {
+      KKT_CUDA(cudaFuncSetAttribute(v6_off3_kernel<KN, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(off3_smem<KN, 4>())));
+      KKT_CUDA(cudaFuncSetAttribute(v6_off3_kernel<KN, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(off3_smem<KN, 4>())));
+    }
     if constexpr (KN <= 512) {
       const int os4 = int(off2_smem<KN, 4>());
       KKT_CUDA(cudaFuncSetAttribute(v6_off2_kernel<KN, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, os4));
@@ -1237,8 +1386,8 @@ int chain_capacity() {
     KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, v6_chain_kernel<KN, true, false, false>, kThr6, cs));
     KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q0, v6_chain_kernel<KN, false, true, false>, kThr6, cs));
     KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q1, v6_chain_kernel<KN, true, true, false>, kThr6, cs));
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r0, v6_chainw_kernel<KN, false>, kThr6, cs));
-    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, v6_chainw_kernel<KN, true>, kThr6, cs));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r0, v6_chainw_kernel<KN, false>, kThr6, ws));
+    KKT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, v6_chainw_kernel<KN, true>, kThr6, ws));
     p0 = std::min(p0, std::min(q0, r0));
     p1 = std::min(p1, std::min(q1, r1));
     int dev = 0, nsm = kSmCount;
@@ -1270,6 +1419,7 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
   const int nchain_groups = P.twist ? P.nreal : ngroups;
   const int gpw = groups_per_wave<KN>(P.k);
   const int og = std::min(P.ny, kSmCount);
+  const int og2 = std::min(P.ny * ((ngroups + 1) / 2), kSmCount), og4 = std::min(P.ny * ((ngroups + 3) / 4), kSmCount);  // off2: flat items
   const int npairs = (ngroups + 1) / 2;
   for (int t = 0; t < nsteps; ++t) {
     P.t = t;
@@ -1286,21 +1436,39 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
           KKT_LAUNCH(c, (v6_off_kernel<KN, false>), og, kThr6, off_smem<KN>(), P);
       } else {
         static const bool ng2 = std::getenv("KKT_V6_OFF_NG2") != nullptr;  // testing: two groups per triangle pass
+        static const bool off3 = std::getenv("KKT_V6_OFF3") != nullptr && std::atoi(std::getenv("KKT_V6_OFF3")) != 0;
         bool four = false;
         if constexpr (KN <= 512) four = ngroups > 2 && !ng2;
+        if (off3) {  // one 8-row tile per warp over the slice's whole k-range: no cross-warp reduction
+          if constexpr (KN <= 512) {
+            if (four) {
+              if (up)
+                KKT_LAUNCH(c, (v6_off3_kernel<KN, true, 4>), og4, kOffThr, (off3_smem<KN, 4>()), P);
+              else
+                KKT_LAUNCH(c, (v6_off3_kernel<KN, false, 4>), og4, kOffThr, (off3_smem<KN, 4>()), P);
+            }
+          }
+          if (!four) {
+            if (up)
+              KKT_LAUNCH(c, (v6_off3_kernel<KN, true, 2>), og2, kOffThr, (off3_smem<KN, 2>()), P);
+            else
+              KKT_LAUNCH(c, (v6_off3_kernel<KN, false, 2>), og2, kOffThr, (off3_smem<KN, 2>()), P);
+          }
+        } else {
         if constexpr (KN <= 512) {
           if (four) {
             if (up)
-              KKT_LAUNCH(c, (v6_off2_kernel<KN, true, 4>), og, kOffThr, (off2_smem<KN, 4>()), P);
+              KKT_LAUNCH(c, (v6_off2_kernel<KN, true, 4>), og4, kOffThr, (off2_smem<KN, 4>()), P);
             else
-              KKT_LAUNCH(c, (v6_off2_kernel<KN, false, 4>), og, kOffThr, (off2_smem<KN, 4>()), P);
+              KKT_LAUNCH(c, (v6_off2_kernel<KN, false, 4>), og4, kOffThr, (off2_smem<KN, 4>()), P);
           }
         }
         if (!four) {
           if (up)
-            KKT_LAUNCH(c, (v6_off2_kernel<KN, true, 2>), og, kOffThr, (off2_smem<KN, 2>()), P);
+            KKT_LAUNCH(c, (v6_off2_kernel<KN, true, 2>), og2, kOffThr, (off2_smem<KN, 2>()), P);
           else
-            KKT_LAUNCH(c, (v6_off2_kernel<KN, false, 2>), og, kOffThr, (off2_smem<KN, 2>()), P);
+            KKT_LAUNCH(c, (v6_off2_kernel<KN, false, 2>), og2, kOffThr, (off2_smem<KN, 2>()), P);
+        }
         }
       }
       if (up && P.twist)  // the inflow of the first outward row: d_{M-1} += H_{M-1} x_M
@@ -1463,10 +1631,10 @@ void build_v6(Ctx* c) {
     }
     c->v6_wmax = wmax;
     const double frac = sum / (double(n) * (kn / 32));
-    // the windowed chain keeps only the window in shared memory (v6_chainw_kernel) and must not
-    // take more of it than the full-row kernel does (same CTAs per SM)
+    // the windowed chain keeps only the window in shared memory (v6_chainw_kernel), twice for the
+    // slots; it must leave room for as many CTAs per SM as the full-row kernel runs with
     const size_t wsm = kn == 256 ? chainw_smem<256>(wmax) : kn == 512 ? chainw_smem<512>(wmax) : chainw_smem<1024>(wmax);
-    const size_t fsm = kn == 256 ? chain_smem<256>() : kn == 512 ? chain_smem<512>() : chain_smem<1024>();
+    const size_t fsm = kn <= 512 ? size_t(113) << 10 : size_t(226) << 10;  // 2 CTAs per SM / 1 CTA per SM
     if (std::getenv("KKT_V6_TIM"))
       std::fprintf(stderr, "v6 band windows: %.0f%% of the k-steps, widest %d k-steps per warp (%zu KB shared)\n", 100.0 * frac, wmax,
                    wsm >> 10);
@@ -1605,9 +1773,6 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   {
     static const int spin = std::getenv("KKT_V6_SPIN_NS") ? std::atoi(std::getenv("KKT_V6_SPIN_NS")) : 0;
     P.spin_ns = spin;
-    static const int phase = std::getenv("KKT_V6_PHASE_NS") ? std::atoi(std::getenv("KKT_V6_PHASE_NS")) : 0;
-    P.phase_ns = phase;
-    P.gwave = 0;
   }
   P.nyA = c->ny;
   P.nreal = nreal;
