@@ -526,10 +526,45 @@ int kkt_apply_P_inv_host(kkt_ctx* ctx, const double* r_host, double* out_host) {
     KKT_CUDA(cudaEventRecord(ev[0], c->stream));
     KKT_CUDA(cudaStreamWaitEvent(c->e2e_in, ev[0], 0));
     KKT_CUDA(cudaStreamWaitEvent(c->e2e_aux, ev[0], 0));
+    // KKT_E2E_SCHED (measurement only): bit 0 = the sweep waits for all three uploads, bit 1 = the
+    // u/z download waits for the sweep, bit 2 = the u/z upload waits for the sweep
+    static const int sched = std::getenv("KKT_E2E_SCHED") ? std::atoi(std::getenv("KKT_E2E_SCHED")) : 0;
     KKT_CUDA(cudaMemcpyAsync(in + 2 * B, r_host + 2 * B, bytes, cudaMemcpyHostToDevice, c->e2e_in));
     KKT_CUDA(cudaEventRecord(ev[1], c->e2e_in));
-    KKT_CUDA(cudaMemcpyAsync(in, r_host, 2 * bytes, cudaMemcpyHostToDevice, c->e2e_in));
-    KKT_CUDA(cudaEventRecord(ev[2], c->e2e_in));
+    if (!(sched & 4)) {
+      KKT_CUDA(cudaMemcpyAsync(in, r_host, 2 * bytes, cudaMemcpyHostToDevice, c->e2e_in));
+      KKT_CUDA(cudaEventRecord(ev[2], c->e2e_in));
+    }
+    if (sched & 6) {
+      // deferred transfers: run the sweep first, then the rest in order
+      KKT_CUDA(cudaStreamWaitEvent(c->stream, (sched & 1) && !(sched & 4) ? ev[2] : ev[1], 0));
+      kkt::schur_apply(c, in + 2 * B, out + 2 * B);
+      KKT_CUDA(cudaEventRecord(ev[4], c->stream));
+      KKT_CUDA(cudaStreamWaitEvent(c->e2e_in, ev[4], 0));
+      if (sched & 4) {
+        KKT_CUDA(cudaMemcpyAsync(in, r_host, 2 * bytes, cudaMemcpyHostToDevice, c->e2e_in));
+        KKT_CUDA(cudaEventRecord(ev[2], c->e2e_in));
+      }
+      KKT_CUDA(cudaStreamWaitEvent(c->e2e_aux, ev[2], 0));
+      KKT_CUDA(cudaStreamWaitEvent(c->e2e_aux, ev[4], 0));
+      cudaStream_t keep = c->stream;
+      c->stream = c->e2e_aux;
+      try {
+        kkt::op_pinv_uz(c, in, out);
+      } catch (...) {
+        c->stream = keep;
+        throw;
+      }
+      c->stream = keep;
+      KKT_CUDA(cudaEventRecord(ev[3], c->e2e_aux));
+      KKT_CUDA(cudaMemcpyAsync(out_host, out, 3 * bytes, cudaMemcpyDeviceToHost, c->e2e_aux));
+      KKT_CUDA(cudaStreamSynchronize(c->e2e_aux));
+      float t[5] = {0, 0, 0, 0, 0};
+      for (int i = 1; i < 5; ++i) KKT_CUDA(cudaEventElapsedTime(&t[i], ev[0], ev[i]));
+      std::fprintf(stderr, "P_inv_host sched %d ms since start: r_w up %.1f, r_u r_z up %.1f, u z computed %.1f, sweep done %.1f\n",
+                   sched, t[1], t[2], t[3], t[4]);
+      return;
+    }
     // u and z blocks on the side stream (the kernels launch on c->stream: swap it for the call),
     // and their download: enqueued before the sweep so that they do not queue behind it
     KKT_CUDA(cudaStreamWaitEvent(c->e2e_aux, ev[2], 0));
@@ -552,7 +587,7 @@ int kkt_apply_P_inv_host(kkt_ctx* ctx, const double* r_host, double* out_host) {
     // the sweep sends each adjoint step's finished planes to the host behind the step
     // (rasq_apply's step hook, on its own copy stream), so the w download overlaps the sweep
     // instead of following it.
-    KKT_CUDA(cudaStreamWaitEvent(c->stream, ev[1], 0));
+    KKT_CUDA(cudaStreamWaitEvent(c->stream, (sched & 1) ? ev[2] : ev[1], 0));
     {
       static const bool trail_off = std::getenv("KKT_E2E_TRAIL_OFF") != nullptr;  // testing: one copy at the end
       const auto& d = c->desc;

@@ -123,6 +123,7 @@ struct V6Params {
   int twist, nyA, nreal;
   int wmax;          // v6_chainw_kernel: the widest window's k-steps per warp (shared-memory extent)
   int spin_ns;       // KKT_V6_SPIN_NS: pause between failed poll rounds (0: none)
+  int stagger;       // v6_chainw_kernel: cycles by which the upper half of the chain groups starts late
   double* Wm;        // [2][nreal][kN][8]: b_M, then x_M
   const double* Dm;  // packed Dm^{-1}
   const double* Em;  // packed cy Dm^{-1} Ui_{M-1}
@@ -1078,6 +1079,17 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  // Two chain CTAs share an SM (CTA b with b + 148 under the usual placement, i.e. a group of the
+  // lower half with one of the upper half).  Chains of different groups are independent, so
+  // starting the upper half of the groups half a product late puts the two CTAs' DMMA loops in
+  // anti-phase: each then has the SM's fp64 pipe to itself, and the other's slot loads, reduction
+  // and stores run under it.  Nothing restores or destroys the offset (both CTAs are delayed
+  // alike where they do overlap), so it holds along the whole chain.
+  if (P.stagger > 0 && 2 * (blockIdx.x / rows_per_g) >= gridDim.x / rows_per_g) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < P.stagger) {
+    }
+  }
   {  // group 0 has no inflow: its rows are the zero-inflow chain values
     const int J = Jof(0);
     if (J < 0) return;
@@ -1436,7 +1448,7 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
           KKT_LAUNCH(c, (v6_off_kernel<KN, false>), og, kThr6, off_smem<KN>(), P);
       } else {
         static const bool ng2 = std::getenv("KKT_V6_OFF_NG2") != nullptr;  // testing: two groups per triangle pass
-        static const bool off3 = std::getenv("KKT_V6_OFF3") != nullptr && std::atoi(std::getenv("KKT_V6_OFF3")) != 0;
+        static const bool off3 = std::getenv("KKT_V6_OFF3") == nullptr || std::atoi(std::getenv("KKT_V6_OFF3")) != 0;  // default on; 0: v6_off2_kernel
         bool four = false;
         if constexpr (KN <= 512) four = ngroups > 2 && !ng2;
         if (off3) {  // one 8-row tile per warp over the slice's whole k-range: no cross-warp reduction
@@ -1773,6 +1785,8 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   {
     static const int spin = std::getenv("KKT_V6_SPIN_NS") ? std::atoi(std::getenv("KKT_V6_SPIN_NS")) : 0;
     P.spin_ns = spin;
+    static const int stag = std::getenv("KKT_V6_STAGGER") ? std::atoi(std::getenv("KKT_V6_STAGGER")) : 0;
+    P.stagger = stag;
   }
   P.nyA = c->ny;
   P.nreal = nreal;

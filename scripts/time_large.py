@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--T", type=float, default=None, help="final time (config 4's per-GPU slab: --nt 128 --T 0.125)")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--mode", default="fast")
+    ap.add_argument("--e2e", action="store_true", help="also time apply_P_inv_host from pinned host buffers")
     a = ap.parse_args()
     p = P.config(a.config, Nd=a.nd)
     if a.nt:
@@ -59,8 +60,21 @@ def main():
     k_ms = tm(lambda: k.apply_K(v, out), max(3, a.reps))
     p_ms = tm(lambda: k.apply_P_inv(v, out), a.reps)
     unk = 3 * p.block
+    e2e_ms = None
+    if a.e2e:
+        hin = torch.empty(3 * p.block, dtype=torch.float64).pin_memory()
+        hout = torch.empty(3 * p.block, dtype=torch.float64).pin_memory()
+        hin.copy_(v)
+        ts = []
+        for _ in range(a.reps + 1):
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            k.apply_P_inv_host(hin.numpy(), hout.numpy())
+            ts.append((time.perf_counter() - t1) * 1e3)
+        ts = sorted(ts[1:])
+        e2e_ms = ts[len(ts) // 2]
     print(json.dumps({"config": a.config, "Nt": p.Nt, "Nd": p.Nd, "nx": p.nx_int, "setup_s": setup_s,
-                      "apply_K_ms": k_ms, "apply_P_inv_ms": p_ms,
+                      "apply_K_ms": k_ms, "apply_P_inv_ms": p_ms, "e2e_ms": e2e_ms,
                       "P_inv_unknowns_per_s": unk / (p_ms * 1e-3),
                       "finite": bool(torch.isfinite(out).all().item())}), flush=True)
 

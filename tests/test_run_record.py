@@ -23,7 +23,17 @@ def test_to_json_string_matches_reference_layout():
         rec, text, _ = Ref.run_single(p)
         mine = RunRecord(p, rec["iterations"], rec["converged"], rec["true_final_relres"],
                          rec["objective"], rec["setup_seconds"], rec["solve_seconds"])
-        assert to_json_string(mine) == text
+        got, want = to_json_string(mine).split("\n"), text.split("\n")
+        assert len(got) == len(want)
+        for a, b in zip(got, want):
+            if a != b:
+                # nlohmann prints doubles with Grisu2, which is not always the shortest
+                # round-trip string; the two wall-clock fields differ from run to run, so
+                # such a double turns up now and then. Same key, same double is required.
+                ka, va = a.split(":")
+                kb, vb = b.split(":")
+                assert ka == kb and "seconds" in ka, (a, b)
+                assert float(va.rstrip(",")) == float(vb.rstrip(",")), (a, b)
         assert json.loads(text)["converged"] == rec["converged"]
 
 
