@@ -680,9 +680,10 @@ def pinv_rooflines(p, ws, ms_apply, sw_ms, napplies):
     sweep = {
         "kernel": ("RASQ sweep v4 (sweep_v4.cu): group-parallel block-LU substitution chains, 8-CTA clusters, fp64 DMMA"
                    if v4 else
-                   "RASQ sweep v6 (sweep_v6.cu): v6_chain_kernel (device-wide dependent block-row chain over groups of k "
-                   "rows, fp64 DMMA, low-latency packet handoff) + v6_off(2)_kernel (batched triangular products) + "
-                   "v6_inner_kernel (zero-inflow chains inside the groups) + v6_form_b_kernel, all local subdomains in lock step"),
+                   "RASQ sweep v6 (sweep_v6.cu): v6_chain(w)_kernel (device-wide dependent block-row chain of the two-sided "
+                   "block elimination, groups of k rows, fp64 DMMA over the operators' numerical band, prefetched slot handoff) "
+                   "+ v6_off(2|3)_kernel (batched triangular products) + v6_mid_kernel (the middle row) + v6_inner_kernel "
+                   "(zero-inflow chains inside the groups) + v6_form_b_kernel, all local subdomains in lock step"),
         "bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": (gbs / peak) if gbs else None,
         "traffic": ncu_summary("sweep_dram_bytes_per_apply" if v4 else f"sweep_v6_nx{p.nx_int}_dram_bytes_per_apply"),
         "peak_source": peak_src, "algorithmic_bytes_per_launch": sb, "avg_launch_ms": sw_ms, "launches": napplies,
@@ -695,7 +696,8 @@ def pinv_rooflines(p, ws, ms_apply, sw_ms, napplies):
                   "us_per_block_row_step": 1000.0 * sw_ms / rows if sw_ms > 0 else None,
                   "handoff_floor_us": ncu_summary("v6_row_handoff_floor_us"),
                   "note": "the sweep is bound by this dependent chain: (2m+1) lock-step spatial solves x 2 directions x "
-                          "ny block rows; k-row grouping makes one handoff serve k rows"},
+                          "ny block rows; the two-sided elimination runs the two half-length chains of a solve side by side and "
+                          "k-row grouping makes one handoff serve k rows, so the dependent handoffs are ny/(2k) per chain launch"},
     }
     rest_ms = ms_apply - sw_ms
     rest_bytes = (4 + 1) * p.block * 8 // ws  # K8 (4B) + K3 node sums (B), SURVEY 8d

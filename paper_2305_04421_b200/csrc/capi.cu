@@ -29,6 +29,7 @@ Ctx::~Ctx() {
   for (auto& iv : ev_pending) { cudaEventDestroy(iv.a); cudaEventDestroy(iv.b); }
   for (auto e : ev_open) if (e) cudaEventDestroy(e);
   for (auto e : e2e_ev) if (e) cudaEventDestroy(e);
+  for (auto e : e2e_chunk_ev) cudaEventDestroy(e);
   for (auto st : {e2e_in, e2e_out, e2e_aux, e2e_trail}) if (st) cudaStreamDestroy(st);
   if (e2e_step_ev) cudaEventDestroy(e2e_step_ev);
   if (own_stream && stream) cudaStreamDestroy(stream);
@@ -502,10 +503,14 @@ int kkt_gmres_solve_host(kkt_ctx* ctx, const double* b_host, double* x_host,
 
 // apply_P_inv from host buffers, with the copies overlapped with the compute: P^-1 is block
 // diagonal (kkt.cpp:71-81), so the Schur block's sweep needs only r_w.  r_w goes up first and the
-// sweep starts; r_u and r_z follow on the copy-in stream while it runs, their division runs on a
-// side stream and its result goes back down (PCIe is full duplex) while the sweep is still busy;
-// out_w follows when the sweep is done.  With pinned host memory the end-to-end time is the sweep
-// plus one block up and one block down instead of the sweep plus three blocks each way.
+// sweep starts.  r_u and r_z follow in chunks on the copy-in stream while it runs; each chunk is
+// divided on a side stream as soon as it has landed and goes straight back down (PCIe is full
+// duplex), so the u/z download runs one chunk behind the upload instead of after it.  Where the
+// sweep's output is the final w block its finished planes trail the adjoint sweep on a third copy
+// stream.  The kernels of the sweep must not touch a copy engine (a cudaMemsetAsync queued behind
+// the bulk upload stalled the sweep until the upload was over: dev_fill is a kernel).  With pinned
+// host memory the end-to-end time approaches one block up plus the larger of the sweep and three
+// blocks down, instead of the sweep plus three blocks each way.
 int kkt_apply_P_inv_host(kkt_ctx* ctx, const double* r_host, double* out_host) {
   return kkt::guard(ctx, [&](Ctx* c) {
     kkt::need(r_host && out_host, "kkt_apply_P_inv_host: bad arguments");
@@ -521,73 +526,51 @@ int kkt_apply_P_inv_host(kkt_ctx* ctx, const double* r_host, double* out_host) {
     double* in = c->e2e_b.p;
     double* out = c->e2e_x.p;
     const size_t bytes = sizeof(double) * B;
-    cudaEvent_t* ev = c->e2e_ev;  // 0: start, 1: r_w up, 2: r_u r_z up, 3: u z done, 4: w done
+    cudaEvent_t* ev = c->e2e_ev;  // 0: start, 1: r_w up, 2: r_u r_z up, 3: u z computed, 4: w done
+    // KKT_E2E_CHUNK_KB: KB of each block per chunk of the u/z pipeline (default 64 MB; 0: the blocks whole)
+    static const long chunk_kb = std::getenv("KKT_E2E_CHUNK_KB") ? std::atol(std::getenv("KKT_E2E_CHUNK_KB")) : 65536;
+    const size_t chunk = chunk_kb > 0 ? std::min(B, size_t(chunk_kb) << 7) : B;  // doubles per block per chunk
+    const size_t nchunks = (B + chunk - 1) / chunk;
+    while (c->e2e_chunk_ev.size() < nchunks) {
+      cudaEvent_t e;
+      KKT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->e2e_chunk_ev.push_back(e);
+    }
     // the staging vectors may still be read by earlier work on the context stream
     KKT_CUDA(cudaEventRecord(ev[0], c->stream));
     KKT_CUDA(cudaStreamWaitEvent(c->e2e_in, ev[0], 0));
     KKT_CUDA(cudaStreamWaitEvent(c->e2e_aux, ev[0], 0));
-    // KKT_E2E_SCHED (measurement only): bit 0 = the sweep waits for all three uploads, bit 1 = the
-    // u/z download waits for the sweep, bit 2 = the u/z upload waits for the sweep
-    static const int sched = std::getenv("KKT_E2E_SCHED") ? std::atoi(std::getenv("KKT_E2E_SCHED")) : 0;
     KKT_CUDA(cudaMemcpyAsync(in + 2 * B, r_host + 2 * B, bytes, cudaMemcpyHostToDevice, c->e2e_in));
     KKT_CUDA(cudaEventRecord(ev[1], c->e2e_in));
-    if (!(sched & 4)) {
-      KKT_CUDA(cudaMemcpyAsync(in, r_host, 2 * bytes, cudaMemcpyHostToDevice, c->e2e_in));
-      KKT_CUDA(cudaEventRecord(ev[2], c->e2e_in));
-    }
-    if (sched & 6) {
-      // deferred transfers: run the sweep first, then the rest in order
-      KKT_CUDA(cudaStreamWaitEvent(c->stream, (sched & 1) && !(sched & 4) ? ev[2] : ev[1], 0));
-      kkt::schur_apply(c, in + 2 * B, out + 2 * B);
-      KKT_CUDA(cudaEventRecord(ev[4], c->stream));
-      KKT_CUDA(cudaStreamWaitEvent(c->e2e_in, ev[4], 0));
-      if (sched & 4) {
-        KKT_CUDA(cudaMemcpyAsync(in, r_host, 2 * bytes, cudaMemcpyHostToDevice, c->e2e_in));
-        KKT_CUDA(cudaEventRecord(ev[2], c->e2e_in));
-      }
-      KKT_CUDA(cudaStreamWaitEvent(c->e2e_aux, ev[2], 0));
-      KKT_CUDA(cudaStreamWaitEvent(c->e2e_aux, ev[4], 0));
+    // u and z blocks, chunk by chunk: up on the copy-in stream, divided and sent down on the side
+    // stream (the kernels launch on c->stream: swap it for the calls).  Enqueued before the sweep
+    // so that none of it queues behind the sweep's launches.
+    for (size_t q = 0; q < nchunks; ++q) {
+      const size_t o = q * chunk, len = std::min(chunk, B - o);
+      KKT_CUDA(cudaMemcpyAsync(in + o, r_host + o, sizeof(double) * len, cudaMemcpyHostToDevice, c->e2e_in));
+      KKT_CUDA(cudaMemcpyAsync(in + B + o, r_host + B + o, sizeof(double) * len, cudaMemcpyHostToDevice, c->e2e_in));
+      KKT_CUDA(cudaEventRecord(c->e2e_chunk_ev[q], c->e2e_in));
+      KKT_CUDA(cudaStreamWaitEvent(c->e2e_aux, c->e2e_chunk_ev[q], 0));
       cudaStream_t keep = c->stream;
       c->stream = c->e2e_aux;
       try {
-        kkt::op_pinv_uz(c, in, out);
+        kkt::op_pinv_uz_range(c, in, out, int64_t(o), int64_t(o + len));
       } catch (...) {
         c->stream = keep;
         throw;
       }
       c->stream = keep;
-      KKT_CUDA(cudaEventRecord(ev[3], c->e2e_aux));
-      KKT_CUDA(cudaMemcpyAsync(out_host, out, 3 * bytes, cudaMemcpyDeviceToHost, c->e2e_aux));
-      KKT_CUDA(cudaStreamSynchronize(c->e2e_aux));
-      float t[5] = {0, 0, 0, 0, 0};
-      for (int i = 1; i < 5; ++i) KKT_CUDA(cudaEventElapsedTime(&t[i], ev[0], ev[i]));
-      std::fprintf(stderr, "P_inv_host sched %d ms since start: r_w up %.1f, r_u r_z up %.1f, u z computed %.1f, sweep done %.1f\n",
-                   sched, t[1], t[2], t[3], t[4]);
-      return;
+      if (q + 1 == nchunks) KKT_CUDA(cudaEventRecord(ev[3], c->e2e_aux));
+      KKT_CUDA(cudaMemcpyAsync(out_host + o, out + o, sizeof(double) * len, cudaMemcpyDeviceToHost, c->e2e_aux));
+      KKT_CUDA(cudaMemcpyAsync(out_host + B + o, out + B + o, sizeof(double) * len, cudaMemcpyDeviceToHost, c->e2e_aux));
     }
-    // u and z blocks on the side stream (the kernels launch on c->stream: swap it for the call),
-    // and their download: enqueued before the sweep so that they do not queue behind it
-    KKT_CUDA(cudaStreamWaitEvent(c->e2e_aux, ev[2], 0));
-    {
-      cudaStream_t keep = c->stream;
-      c->stream = c->e2e_aux;
-      try {
-        kkt::op_pinv_uz(c, in, out);
-      } catch (...) {
-        c->stream = keep;
-        throw;
-      }
-      c->stream = keep;
-    }
-    KKT_CUDA(cudaEventRecord(ev[3], c->e2e_aux));
-    KKT_CUDA(cudaStreamWaitEvent(c->e2e_out, ev[3], 0));
-    KKT_CUDA(cudaMemcpyAsync(out_host, out, 2 * bytes, cudaMemcpyDeviceToHost, c->e2e_out));
+    KKT_CUDA(cudaEventRecord(ev[2], c->e2e_in));
     // Schur block on the context stream.  Where the RASQ sweep's output is the final w block
     // (one-level; two-level literal; the fused multiplicative form) and the host buffer is pinned,
     // the sweep sends each adjoint step's finished planes to the host behind the step
     // (rasq_apply's step hook, on its own copy stream), so the w download overlaps the sweep
     // instead of following it.
-    KKT_CUDA(cudaStreamWaitEvent(c->stream, (sched & 1) ? ev[2] : ev[1], 0));
+    KKT_CUDA(cudaStreamWaitEvent(c->stream, ev[1], 0));
     {
       static const bool trail_off = std::getenv("KKT_E2E_TRAIL_OFF") != nullptr;  // testing: one copy at the end
       const auto& d = c->desc;
@@ -622,18 +605,19 @@ int kkt_apply_P_inv_host(kkt_ctx* ctx, const double* r_host, double* out_host) {
       KKT_CUDA(cudaStreamSynchronize(c->e2e_trail));
     }
     KKT_CUDA(cudaStreamSynchronize(c->e2e_out));
+    KKT_CUDA(cudaStreamSynchronize(c->e2e_aux));
     KKT_CUDA(cudaStreamSynchronize(c->stream));
     static const bool tim = std::getenv("KKT_E2E_TIM") != nullptr;  // stage completion times since the start
     if (tim) {
       cudaEvent_t done;
       KKT_CUDA(cudaEventCreate(&done));
-      KKT_CUDA(cudaEventRecord(done, c->e2e_out));
+      KKT_CUDA(cudaEventRecord(done, c->stream));  // everything has been synchronised: the end of the call
       KKT_CUDA(cudaEventSynchronize(done));
       float t[5] = {0, 0, 0, 0, 0};
       for (int i = 1; i < 5; ++i) KKT_CUDA(cudaEventElapsedTime(&t[i], ev[0], ev[i]));
       KKT_CUDA(cudaEventElapsedTime(&t[0], ev[0], done));
-      std::fprintf(stderr, "P_inv_host ms since start: r_w up %.1f, r_u r_z up %.1f, u z computed %.1f, sweep done %.1f, all down %.1f%s\n",
-                   t[1], t[2], t[3], t[4], t[0], c->e2e_trailed ? " (w planes trailed the adjoint sweep)" : "");
+      std::fprintf(stderr, "P_inv_host ms since start: r_w up %.1f, r_u r_z up %.1f, u z computed %.1f, sweep done %.1f, all down %.1f (%zu u/z chunks%s)\n",
+                   t[1], t[2], t[3], t[4], t[0], nchunks, c->e2e_trailed ? "; w planes trailed the adjoint sweep" : "");
       cudaEventDestroy(done);
     }
   });

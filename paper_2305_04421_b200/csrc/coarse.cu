@@ -450,7 +450,7 @@ void build_coarse(Ctx* c) {
   c->cvec.alloc(dim);
   c->call.alloc(size_t(dim) * c->nranks);
   c->gam.alloc(Nt + 2);
-  KKT_CUDA(cudaMemsetAsync(c->gam.p, 0, sizeof(double) * (Nt + 2), c->stream));
+  dev_fill(c, c->gam.p, 0, sizeof(double) * (Nt + 2));
 
   // ---- a1 = Ahat 1, a2 = Ahat a1 (fast analytic Shat y_c)
   c->a1.alloc(nsp);
@@ -528,7 +528,7 @@ void two_level_apply(Ctx* c, const double* r, double* out, int form) {
     // y_c = prolong_add(S0^{-1} restrict(r)) into zeros (schur.cpp:421-424)
     coarse_restrict(c, r, c->cvec.p);
     perdof_solve(c, c->cvec.p);
-    KKT_CUDA(cudaMemsetAsync(yc, 0, sizeof(double) * c->B, c->stream));
+    dev_fill(c, yc, 0, sizeof(double) * c->B);
     perdof_prolong_add(c, c->cvec.p, yc);
   } else {
     coarse_gamma(c, r);

@@ -187,6 +187,11 @@ struct Ctx {
   DBuf<double> tmpB1, tmpB2, tmpB3;  // block-sized scratch
   DBuf<double> sweep_ws;          // per-subdomain work planes for the sweep
   DBuf<char> jobs_strict, jobs_fast;  // chain descriptors (sweep.cu)
+  // what each of the two holds, so that an unchanged table (the same vectors applied again, as in
+  // every GMRES iteration) is not sent again: a small host-to-device copy on the context stream
+  // queues behind any bulk upload another stream has in flight (kkt_apply_P_inv_host) and the sweep
+  // stood still until that was over
+  std::vector<char> jobs_strict_held, jobs_fast_held;
   DBuf<double> red;               // reduction partials
   DBuf<unsigned> red_count;
   DBuf<double> hbuf;              // Hessenberg column on device
@@ -199,6 +204,7 @@ struct Ctx {
   DBuf<double> e2e_b, e2e_x;       // kkt_gmres_solve_host staging
   cudaStream_t e2e_in = nullptr, e2e_out = nullptr, e2e_aux = nullptr;  // kkt_apply_P_inv_host: copy / side streams
   cudaEvent_t e2e_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> e2e_chunk_ev;  // one per u/z chunk: its upload has landed
   // kkt_apply_P_inv_host: the w block's planes go back to the host as the adjoint sweep finishes
   // them.  e2e_w_host (pinned) is set for the duration of the call; rasq_apply installs step_hook
   // when its output is the final w block, the step-by-step sweep (v6) calls it after every step,
@@ -254,6 +260,8 @@ struct Halo {
 Halo exchange_halo(Ctx* c, const double* v, int slot_prev, int slot_next, bool want_prev, bool want_next);
 void op_apply_K(Ctx* c, const double* v, double* out, const double* b_minus);
 void op_pinv_uz(Ctx* c, const double* r, double* out);
+void op_pinv_uz_range(Ctx* c, const double* r, double* out, int64_t i0, int64_t i1);  // points [i0, i1) of both blocks
+void dev_fill(Ctx* c, void* p, int byte, size_t nbytes);  // cudaMemsetAsync as a kernel on c->stream
 void op_shat(Ctx* c, const double* v, double* out, double* tmp);
 
 // ---- batched fp64 tensor-core GEMM (spectral.cu): C[b] = A[b] B[b], row-major

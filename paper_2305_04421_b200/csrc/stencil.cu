@@ -138,14 +138,24 @@ __global__ void __launch_bounds__(kTX * kTY) apply_K_kernel(Stencil s, int nt, i
 }
 
 // apply_P_inv's diagonal blocks (kkt.cpp:76-79): divisions, as the reference.
-__global__ void __launch_bounds__(kThreads) pinv_uz_kernel(int64_t B, double ms, double oms,
+__global__ void __launch_bounds__(kThreads) pinv_uz_kernel(int64_t B, int64_t i0, int64_t i1, double ms, double oms,
                                                            const double* __restrict__ r,
                                                            double* __restrict__ out) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < B;
+  for (int64_t i = i0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < i1;
        i += int64_t(gridDim.x) * blockDim.x) {
     out[i] = sdiv(r[i], ms);
     out[i + B] = sdiv(r[i + B], oms);
   }
+}
+
+// memset as a kernel: a cudaMemsetAsync may be scheduled on a copy engine, where it queues behind
+// whatever bulk host transfer another stream has in flight (kkt_apply_P_inv_host's uploads)
+__global__ void __launch_bounds__(kThreads) fill_words_kernel(int64_t n, unsigned word, unsigned* __restrict__ p) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) p[i] = word;
+}
+__global__ void __launch_bounds__(kThreads) fill_quads_kernel(int64_t n, unsigned word, uint4* __restrict__ p) {
+  const uint4 v = make_uint4(word, word, word, word);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) p[i] = v;
 }
 
 }  // namespace
@@ -240,7 +250,21 @@ void op_apply_K(Ctx* c, const double* v, double* out, const double* b_minus) {
 }
 
 void op_pinv_uz(Ctx* c, const double* r, double* out) {
-  KKT_LAUNCH(c, pinv_uz_kernel, grid_for(c->B), kThreads, 0, c->B, c->ms, c->oms, r, out);
+  KKT_LAUNCH(c, pinv_uz_kernel, grid_for(c->B), kThreads, 0, c->B, int64_t(0), c->B, c->ms, c->oms, r, out);
+}
+
+void op_pinv_uz_range(Ctx* c, const double* r, double* out, int64_t i0, int64_t i1) {
+  if (i1 > i0) KKT_LAUNCH(c, pinv_uz_kernel, grid_for(i1 - i0), kThreads, 0, c->B, i0, i1, c->ms, c->oms, r, out);
+}
+
+void dev_fill(Ctx* c, void* p, int byte, size_t nbytes) {
+  if (nbytes % 4 != 0 || reinterpret_cast<uintptr_t>(p) % 4 != 0) throw Error(KKT_EINVAL, "dev_fill: 4-byte granularity");
+  const unsigned b = unsigned(byte) & 0xFFu, word = b | (b << 8) | (b << 16) | (b << 24);
+  if (nbytes == 0) return;
+  if (nbytes % 16 == 0 && reinterpret_cast<uintptr_t>(p) % 16 == 0)
+    KKT_LAUNCH(c, fill_quads_kernel, grid_for(int64_t(nbytes / 16)), kThreads, 0, int64_t(nbytes / 16), word, static_cast<uint4*>(p));
+  else
+    KKT_LAUNCH(c, fill_words_kernel, grid_for(int64_t(nbytes / 4)), kThreads, 0, int64_t(nbytes / 4), word, static_cast<unsigned*>(p));
 }
 
 // apply_shat (schur.cpp:71-78): t = Jhat^T v; t /= ms; out = Jhat t.  On a

@@ -124,6 +124,7 @@ struct V6Params {
   int wmax;          // v6_chainw_kernel: the widest window's k-steps per warp (shared-memory extent)
   int spin_ns;       // KKT_V6_SPIN_NS: pause between failed poll rounds (0: none)
   int stagger;       // v6_chainw_kernel: cycles by which the upper half of the chain groups starts late
+  int nohold;        // KKT_V6_NOHOLD (testing): fetch the operator window for every row, also an unchanged one
   double* Wm;        // [2][nreal][kN][8]: b_M, then x_M
   const double* Dm;  // packed Dm^{-1}
   const double* Em;  // packed cy Dm^{-1} Ui_{M-1}
@@ -1026,9 +1027,21 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
   };
   const int2* band = kUpper ? P.bandPsi : P.bandPhi;
   auto window = [&](int pidx) { return band[size_t(pidx) * kSl + s]; };
-  auto copy_a = [&](int gr, int J, int2 wn) {  // thread 0: this slice's window of the operator row
+  // This slice's window of the operator row of (group step gr, block row J) -> As, unless As holds
+  // it already: the rows past jstar share one converged operator set (70% of config 2's rows), so
+  // the chain keeps that window in shared memory instead of fetching it again for every row.
+  // Every thread keeps the bookkeeping (held row, copies issued, one in flight); thread 0 copies.
+  int held = -1;
+  uint32_t ncopy = 0;
+  bool inflight = false;
+  auto copy_a = [&](int gr, int J, int2 wn) {
     const int pidx = propidx(kUpper, gr, gi, J, P);
-    tma_load(As, Mbase + size_t(pidx) * mstride + size_t(wn.x) * 64, uint32_t(sizeof(double) * 64 * 8 * wn.y), barA);
+    if (pidx == held && !P.nohold) return;
+    held = pidx;
+    ++ncopy;
+    inflight = true;
+    if (threadIdx.x == 0)
+      tma_load(As, Mbase + size_t(pidx) * mstride + size_t(wn.x) * 64, uint32_t(sizeof(double) * 64 * 8 * wn.y), barA);
   };
   // this warp's k-range of the slots of (virtual group gv, group step st) -> its part of Bs[buf]
   auto prefetch = [&](int buf, int gv, int st, int2 wn) {
@@ -1085,6 +1098,11 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
   // anti-phase: each then has the SM's fp64 pipe to itself, and the other's slot loads, reduction
   // and stores run under it.  Nothing restores or destroys the offset (both CTAs are delayed
   // alike where they do overlap), so it holds along the whole chain.
+  if (P.tim && threadIdx.x == 0 && blockIdx.x < 1024) {  // KKT_V6_TIM: which SM this CTA runs on
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    P.tim[12 + blockIdx.x] = (long long)smid;
+  }
   if (P.stagger > 0 && 2 * (blockIdx.x / rows_per_g) >= gridDim.x / rows_per_g) {
     const long long t0 = clock64();
     while (clock64() - t0 < P.stagger) {
@@ -1097,7 +1115,7 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
       for (int h = 0; h < nh; ++h) emit(h, 0, J, __ldcg(P.W1 + widx<KN>(g + h * P.nreal, J, ny) + size_t(row) * kG + n));
     if (P.ngr > 1 && Jof(1) >= 0) {
       wn_next = window(propidx(kUpper, 1, gi, Jof(1), P));
-      if (threadIdx.x == 0) copy_a(1, Jof(1), wn_next);
+      copy_a(1, Jof(1), wn_next);
       prefetch(0, g, 0, wn_next);
     }
   }
@@ -1111,7 +1129,6 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
     const int2 wn = wn_next;
     const bool more = idx + 1 < P.ngr && Jof(idx + 1) >= 0;
     if (more) wn_next = window(propidx(kUpper, idx + 1, gi, Jof(idx + 1), P));
-    const uint32_t par = uint32_t(idx - 1) & 1u;
     for (int h = 0; h < nh; ++h) {
       const int gv = g + h * P.nreal;
       if (tm) ts[0] = clock64();
@@ -1122,7 +1139,10 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
       // the other half of this row was published a whole product ago: fetch it under this product
       const bool early = h + 1 < nh;
       if (early) prefetch(buf ^ 1, g + (h + 1) * P.nreal, idx - 1, wn);
-      if (h == 0) mbar_wait(barA, par);  // the operator slice serves both halves
+      if (inflight) {  // the operator slice serves both halves
+        mbar_wait(barA, (ncopy - 1u) & 1u);
+        inflight = false;
+      }
       if (tm) ts[3] = clock64();
       double d[2][2][2] = {};
       const double* Aw = As + size_t(warp * wn.y) * 64 + lane;
@@ -1155,6 +1175,8 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
         for (int e = 0; e < 2; ++e) redw[warp * 128 + (mt * 32 + lane) * 2 + e] = d[0][mt][e] + d[1][mt][e];
       if (tm) ts[4] = clock64();
       __syncthreads();  // As consumed by every warp (last half), red[rb] complete
+      // the next row's operator window, as soon as As is free (before this half's stores)
+      if (h + 1 == nh && more) copy_a(idx + 1, Jof(idx + 1), wn_next);
       if (outt) emit(h, idx, J, cval + reduce8(redw, threadIdx.x));
       rb ^= 1;
       buf ^= 1;
@@ -1163,7 +1185,6 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
         for (int q = 0; q < 6; ++q) acc[q] += ts[q + 1] - ts[q];
       }
     }
-    if (more && threadIdx.x == 0) copy_a(idx + 1, Jof(idx + 1), wn_next);
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   if (tm)
@@ -1499,9 +1520,9 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
       if (P.ll)  // every handoff slot of this sweep direction back to "empty", right before the chain: the
                  // slots are then L2-resident when the chain polls them (refilled a step early, from
                  // v6_form_b_kernel, they had gone cold: config 2 114 -> 127 ms)
-        KKT_CUDA(cudaMemsetAsync(P.ll, 0xFF, sizeof(unsigned long long) * P.nll, c->stream));
+        dev_fill(c, P.ll, 0xFF, sizeof(unsigned long long) * P.nll);
       else
-        KKT_CUDA(cudaMemsetAsync(P.cnt, 0, sizeof(unsigned) * ngroups, c->stream));  // counter handoff
+        dev_fill(c, P.cnt, 0, sizeof(unsigned) * ngroups);  // counter handoff
       for (int g0 = 0; g0 < nchain_groups; g0 += gpw) {
         P.g0 = g0;
         launch_chain<KN>(c, up, P, std::min(gpw, nchain_groups - g0));
@@ -1650,7 +1671,9 @@ void build_v6(Ctx* c) {
     if (std::getenv("KKT_V6_TIM"))
       std::fprintf(stderr, "v6 band windows: %.0f%% of the k-steps, widest %d k-steps per warp (%zu KB shared)\n", 100.0 * frac, wmax,
                    wsm >> 10);
-    return frac < bfrac && wsm <= fsm;
+    // KKT_V6_CFRAC (tuning): the chain's own threshold (default: the common one)
+    static const double cfrac = std::getenv("KKT_V6_CFRAC") ? std::atof(std::getenv("KKT_V6_CFRAC")) : bfrac;
+    return frac < cfrac && wsm <= fsm;
   };
   c->v6_band_on = windows_pay(c->v6_band.p, size_t(2) * nops * ksl);
   {  // the raw ranges likewise: k-steps kept, relative to the triangle (Li, Ui) or the full row (G, H)
@@ -1787,6 +1810,8 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
     P.spin_ns = spin;
     static const int stag = std::getenv("KKT_V6_STAGGER") ? std::atoi(std::getenv("KKT_V6_STAGGER")) : 0;
     P.stagger = stag;
+    static const bool nohold = std::getenv("KKT_V6_NOHOLD") != nullptr;
+    P.nohold = nohold ? 1 : 0;
   }
   P.nyA = c->ny;
   P.nreal = nreal;
@@ -1837,7 +1862,8 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   DBuf<long long> tim;
   P.tim = nullptr;
   if (dbg) {
-    tim.alloc(12);
+    tim.alloc(12 + 1024);
+    KKT_CUDA(cudaMemsetAsync(tim.p, 0xFF, sizeof(long long) * (12 + 1024), c->stream));
     KKT_CUDA(cudaMemsetAsync(tim.p, 0, sizeof(long long) * 12, c->stream));
     P.tim = tim.p;
   }
@@ -1850,9 +1876,27 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
     run_steps<1024>(c, P, nsteps, ngroups);
   c->tend(3);
   if (dbg) {
-    long long h[12];
+    static long long h[12 + 1024];
     KKT_CUDA(cudaMemcpyAsync(h, tim.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     KKT_CUDA(cudaStreamSynchronize(c->stream));
+    {  // chain CTAs per SM, and how many co-resident pairs come from different halves of the groups
+      int ncta = 0;
+      while (ncta < 1024 && h[12 + ncta] >= 0) ++ncta;
+      if (ncta > 0) {
+        const int per_g = ncta / std::max(1, nreal);
+        int same = 0, diff = 0, alone = 0;
+        for (int a = 0; a < ncta; ++a) {
+          int mate = -1;
+          for (int b = 0; b < ncta; ++b)
+            if (b != a && h[12 + b] == h[12 + a]) mate = b;
+          if (mate < 0) ++alone;
+          else if ((2 * (a / per_g) >= nreal) != (2 * (mate / per_g) >= nreal)) ++diff;
+          else ++same;
+        }
+        std::fprintf(stderr, "v6 chain placement: %d CTAs, alone on their SM %d, paired across the halves %d, paired inside a half %d; CTA 0..3 on SM %lld %lld %lld %lld, CTA 148 on SM %lld\n",
+                     ncta, alone, diff, same, h[12], h[13], h[14], h[15], ncta > 148 ? h[12 + 148] : -1LL);
+      }
+    }
     const double rows = double(ny - 1) * nsteps;
     for (int u = 0; u < 2; ++u)
       std::fprintf(stderr, "v6 %s cycles/row (middle slice of group 0): poll %.0f waitA %.0f waitB %.0f mma %.0f emit %.0f signal %.0f\n",

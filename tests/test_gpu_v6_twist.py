@@ -146,12 +146,14 @@ def test_twisted_full_solve_against_one_sided(tmp_path):
     assert _rel(xa, xb) <= 1e-7, _rel(xa, xb)
 
 
-@pytest.mark.parametrize("env", [{}, {"KKT_E2E_TRAIL_OFF": "1"}], ids=["trailed", "whole_copy"])
+@pytest.mark.parametrize("env", [{}, {"KKT_E2E_TRAIL_OFF": "1"}, {"KKT_E2E_CHUNK_KB": "100"}, {"KKT_E2E_CHUNK_KB": "0"}],
+                         ids=["trailed", "whole_copy", "ragged_chunks", "whole_blocks"])
 def test_host_pinv_trailing_download(env):
     """kkt_apply_P_inv_host on a v6 grid with pinned host buffers: the w block's planes go back to
     the host behind each adjoint step of the sweep (rasq_apply's step hook) instead of in one
     copy after it.  The result is bitwise the device-resident application either way, for the
-    fused two-level form and for one-level RASQ; pageable buffers take the whole-copy path."""
+    fused two-level form and for one-level RASQ; pageable buffers take the whole-copy path.  The
+    u and z blocks travel in chunks (up, divided, down): one chunk, several ragged ones, or whole."""
     code = (
         "import numpy as np, torch; from paper_2305_04421_b200 import problems as P; "
         "from paper_2305_04421_b200.solver import HeatKKT\n"
@@ -172,4 +174,6 @@ def test_host_pinv_trailing_download(env):
     lines = [x for x in r.stderr.splitlines() if x.startswith("P_inv_host ms")]
     assert len(lines) == 4, r.stderr[-1500:]
     trailed = [("trailed" in x) for x in lines]
-    assert trailed == ([True, False, True, False] if not env else [False] * 4), lines
+    assert trailed == ([False] * 4 if "KKT_E2E_TRAIL_OFF" in env else [True, False, True, False]), lines
+    if env.get("KKT_E2E_CHUNK_KB") == "100":  # 299 x 11 x 24 doubles per block in 12,800-double chunks
+        assert all("(7 u/z chunks" in x for x in lines), lines
