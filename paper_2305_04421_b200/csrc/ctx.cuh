@@ -143,8 +143,9 @@ struct Ctx {
   // two-sided (twisted) elimination: block rows 0..M-1 and ny-1..M+1 run as two half-length chains
   // that meet in the middle row M = (ny-1)/2 (ny odd); v6_nyv = rows per half chain (ny: off)
   bool v6_twist = false;
+  bool v6_thomas = false;          // the inverse-block ("Thomas") form of the twisted elimination is built (sweep_v6.cu)
   int v6_nyv = 0;
-  DBuf<double> v6_mid;             // packed Dm^{-1} and E = cy Dm^{-1} Ui_{M-1} (factor_block.cu)
+  DBuf<double> v6_mid;             // packed Dm^{-1}, E = cy Dm^{-1} Ui_{M-1} and E2 = cy Dm^{-1} H_{M-1} (factor_block.cu)
   DBuf<unsigned> v4_flags;
   int v4_nsets = 0;
   bool v4_coop = false, v4_registered = false;
@@ -243,7 +244,7 @@ struct Ctx {
 void build_factor(Ctx* c);
 void build_block_inverses(Ctx* c);
 void build_block_recursion(Ctx* c);
-void build_twist_middle(Ctx* c, int M, double* Dinv, double* E);
+void build_twist_middle(Ctx* c, int M, double* Dinv, double* E, double* E2);
 void build_coarse(Ctx* c);
 
 // ---- operators (stencil.cu)

@@ -253,7 +253,10 @@ void build_block_recursion(Ctx* c) {
 //     Dm = T - cy^2 D_{M-1}^{-1} - cy^2 D'_{M+1}^{-1} = T - 2 cy^2 Ui_{M-1} Li_{M-1}.
 // Outputs (nx x nx, row-major): Dinv = Dm^{-1}, E = cy Dm^{-1} Ui_{M-1}, so that
 //     x_M = Dinv b_M + E (y_{M-1} + y'_{M+1}).
-void build_twist_middle(Ctx* c, int M, double* Dinv, double* E) {
+// E2 (optional) = cy Dm^{-1} H_{M-1} = cy^2 Dm^{-1} Ui_{M-1} Li_{M-1}: the same row in the inverse-block
+// form of the elimination (sweep_v6.cu, "Thomas form"), where the chains carry y_J = b_J/cy + z_{J-1}
+// and z_{M-1} = H_{M-1} y_{M-1}:  x_M = Dinv b_M + E2 (y_{M-1} + y'_{M+1}).
+void build_twist_middle(Ctx* c, int M, double* Dinv, double* E, double* E2) {
   const int nx = c->nx;
   const int64_t nn = int64_t(nx) * nx;
   const double tol = 1e-14 * ahat_inf_norm(c);
@@ -264,11 +267,17 @@ void build_twist_middle(Ctx* c, int M, double* Dinv, double* E) {
   const double* Lp = c->Li.p + int64_t(M - 1) * nn;
   const double* Up = c->Ui.p + int64_t(M - 1) * nn;
   KKT_LAUNCH(c, gemm_kernel, gg, gb, 0, nx, Up, Lp, S.p);
+  DBuf<double> S2(E2 ? nn : 0);
+  if (E2) KKT_CUDA(cudaMemcpyAsync(S2.p, S.p, sizeof(double) * nn, cudaMemcpyDeviceToDevice, c->stream));
   KKT_LAUNCH(c, form_d_kernel, kSmCount * 2, 256, 0, nx, c->Ahat.diag, c->Ahat.mcx, 2.0 * c->cy * c->cy, S.p, D.p);
   lu_and_inverses(c, tol, D.p, Lm.p, Um.p, st, bar);
   KKT_LAUNCH(c, gemm_kernel, gg, gb, 0, nx, Um.p, Lm.p, Dinv);
   KKT_LAUNCH(c, gemm_kernel, gg, gb, 0, nx, Dinv, Up, S.p);
   KKT_LAUNCH(c, scale_copy_kernel, kSmCount * 2, 256, 0, nn, c->cy, S.p, E);
+  if (E2) {
+    KKT_LAUNCH(c, gemm_kernel, gg, gb, 0, nx, Dinv, S2.p, S.p);
+    KKT_LAUNCH(c, scale_copy_kernel, kSmCount * 2, 256, 0, nn, c->cy * c->cy, S.p, E2);
+  }
   int hs = -1;
   KKT_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   KKT_CUDA(cudaStreamSynchronize(c->stream));

@@ -124,6 +124,16 @@ struct V6Params {
   int wmax;          // v6_chainw_kernel: the widest window's k-steps per warp (shared-memory extent)
   int spin_ns;       // KKT_V6_SPIN_NS: pause between failed poll rounds (0: none)
   int stagger;       // v6_chainw_kernel: cycles by which the upper half of the chain groups starts late
+  // Inverse-block ("Thomas") form of the twisted elimination (k == 1, slot handoff): with
+  // H_J = cy D_J^{-1} the forward elimination is z_J = H_J (b_J/cy + z_{J-1}) and the back
+  // substitution x_J = z_J + H_J x_{J+1} = H_J (y_J + x_{J+1}), y_J = b_J/cy + z_{J-1}.  Both map
+  // onto the chain recurrences with H as the only operator set and NO off-chain products:
+  //   L chain:  y_0 = c_0,  y_J = c_J + H_{J-1} y_{J-1},  c = b/cy (written by v6_form_b_kernel)
+  //   middle:   x_M = Dm^{-1} b_M + E2 (y_{M-1} + y'_{M+1}),  E2 = cy Dm^{-1} H_{M-1}
+  //   U chain:  X_{M-1} = y_{M-1} + x_M,  X_J = y_J + H_{J+1} X_{J+1};  the product is x_{J+1}
+  //   last:     x_0 = H_0 X_0  (v6_mid_kernel, mode 2)
+  int thomas;
+  double inv_cy;
   int nohold;        // KKT_V6_NOHOLD (testing): fetch the operator window for every row, also an unchanged one
   double* Wm;        // [2][nreal][kN][8]: b_M, then x_M
   const double* Dm;  // packed Dm^{-1}
@@ -159,7 +169,7 @@ __global__ void __launch_bounds__(kFbChunk) v6_form_b_kernel(V6Params P) {
     const int h = gv >= P.nreal ? 1 : 0;
     g = gv - h * P.nreal;
     J = h ? P.nyA - 1 - j : j;
-    dst = P.W0 + size_t(rb) * KN * kG;
+    dst = (P.thomas ? P.W1 : P.W0) + size_t(rb) * KN * kG;  // Thomas form: c = b / cy, straight to the chain
   } else {
     g = rb - nrb;
     J = P.ny;  // the middle row of the twisted elimination
@@ -184,7 +194,7 @@ __global__ void __launch_bounds__(kFbChunk) v6_form_b_kernel(V6Params P) {
         }
       }
     }
-    tile[threadIdx.x][c] = v;
+    tile[threadIdx.x][c] = (P.thomas && rb < nrb) ? v * P.inv_cy : v;
   }
   __syncthreads();
   double* o = dst + size_t(chunk) * kFbChunk * kG;
@@ -606,6 +616,7 @@ __device__ __forceinline__ int grow(bool upper, int gr, int i, int k, int ny) {
 }
 // Packed propagator index of (group gr, row i): see V6Params.
 __device__ __forceinline__ int propidx(bool upper, int gr, int i, int J, const V6Params& P) {
+  if (P.thomas) return oprow(upper ? J + 1 : (J > 0 ? J - 1 : 0), P.jstar);  // H_{J+1} / H_{J-1}
   if (P.k == 1) return oprow(J, P.jstar);
   if (upper) return gr < P.gconv ? i : P.k + (gr - P.gconv) * P.k + i;
   return gr < P.nind ? gr * P.k + i : P.nind * P.k + i;
@@ -769,14 +780,19 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
     }
   }
   auto Jof = [&](int gr) { return grow(kUpper, gr, gi, P.k, ny); };  // this CTA's row of group gr
-  auto emit = [&](int h, int gr, int J, double v) {
+  // v: the chain value of row J (slot, W0); pv: the product alone.  Thomas form, U: the product is
+  // x_{J+1} (the start row has none)
+  auto emit = [&](int h, int gr, int J, double v, double pv, bool start) {
     const int gv = g + h * P.nreal;
     if (kLL && last_row)
       st_slot(P.ll + (size_t(gv) * P.ngr + gr) * (KN * kG) + size_t(row) * kG + n, v);
     P.W0[widx<KN>(gv, J, ny) + size_t(row) * kG + n] = v;
-    const int Ja = h ? P.nyA - 1 - J : J;  // the block row of the grid (bottom half: mirrored)
-    if (out) out[size_t(Ja) * P.nx + row] = v;
-    if (out2) out2[size_t(Ja) * P.nx + row] = v + g2;
+    if (P.thomas && start) return;
+    const int Jo = P.thomas ? J + 1 : J;
+    const double ov = P.thomas ? pv : v;
+    const int Ja = h ? P.nyA - 1 - Jo : Jo;  // the block row of the grid (bottom half: mirrored)
+    if (out) out[size_t(Ja) * P.nx + row] = ov;
+    if (out2) out2[size_t(Ja) * P.nx + row] = ov + g2;
   };
   // each output warp publishes its own stores (release after __syncwarp), so
   // no CTA-wide barrier sits between the stores and the count; 4 per CTA and row
@@ -807,7 +823,8 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
     const int J = Jof(0);
     if (J < 0) return;
     if (outt)
-      for (int h = 0; h < nh; ++h) emit(h, 0, J, __ldcg(P.W1 + widx<KN>(g + h * P.nreal, J, ny) + size_t(row) * kG + n));
+      for (int h = 0; h < nh; ++h)
+        emit(h, 0, J, __ldcg(P.W1 + widx<KN>(g + h * P.nreal, J, ny) + size_t(row) * kG + n), 0.0, true);
     signal();
     if (P.ngr > 1 && Jof(1) >= 0) {
       wn_next = window(propidx(kUpper, 1, gi, Jof(1), P));
@@ -830,7 +847,7 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
       const int gv = g + h * P.nreal;
       if (tm) ts[0] = clock64();
       double cval = 0.0;
-      if (outt) cval = __ldcg(P.W1 + widx<KN>(gv, J, ny) + size_t(row) * kG + n);
+      if (outt) cval = __ldcg(((kUpper && P.thomas) ? P.W0 : P.W1) + widx<KN>(gv, J, ny) + size_t(row) * kG + n);
       if (!kLL) {
         if (threadIdx.x == 0) {
           const unsigned target = unsigned(idx) * kSl * 4;
@@ -954,7 +971,10 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
       // As / Bs consumed by every warp, red[rb] complete.  The other buffer is written next, after
       // this barrier, which every reader of its previous contents has passed: one barrier per product.
       __syncthreads();
-      if (outt) emit(h, idx, J, cval + reduce8(redw, threadIdx.x));
+      if (outt) {
+        const double pv = reduce8(redw, threadIdx.x);
+        emit(h, idx, J, cval + pv, pv, false);
+      }
       rb ^= 1;
       if (tm) {
         ts[5] = ts[6] = clock64();
@@ -1017,13 +1037,16 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
     }
   }
   auto Jof = [&](int gr) { return grow(kUpper, gr, gi, P.k, ny); };
-  auto emit = [&](int h, int gr, int J, double v) {
+  auto emit = [&](int h, int gr, int J, double v, double pv, bool start) {  // as in v6_chain_kernel
     const int gv = g + h * P.nreal;
     if (last_row) st_slot(P.ll + (size_t(gv) * P.ngr + gr) * (KN * kG) + size_t(row) * kG + n, v);
     P.W0[widx<KN>(gv, J, ny) + size_t(row) * kG + n] = v;
-    const int Ja = h ? P.nyA - 1 - J : J;
-    if (out) out[size_t(Ja) * P.nx + row] = v;
-    if (out2) out2[size_t(Ja) * P.nx + row] = v + g2;
+    if (P.thomas && start) return;
+    const int Jo = P.thomas ? J + 1 : J;
+    const double ov = P.thomas ? pv : v;
+    const int Ja = h ? P.nyA - 1 - Jo : Jo;
+    if (out) out[size_t(Ja) * P.nx + row] = ov;
+    if (out2) out2[size_t(Ja) * P.nx + row] = ov + g2;
   };
   const int2* band = kUpper ? P.bandPsi : P.bandPhi;
   auto window = [&](int pidx) { return band[size_t(pidx) * kSl + s]; };
@@ -1114,7 +1137,8 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
     const int J = Jof(0);
     if (J < 0) return;
     if (outt)
-      for (int h = 0; h < nh; ++h) emit(h, 0, J, __ldcg(P.W1 + widx<KN>(g + h * P.nreal, J, ny) + size_t(row) * kG + n));
+      for (int h = 0; h < nh; ++h)
+        emit(h, 0, J, __ldcg(P.W1 + widx<KN>(g + h * P.nreal, J, ny) + size_t(row) * kG + n), 0.0, true);
     if (P.ngr > 1 && Jof(1) >= 0) {
       wn_next = window(propidx(kUpper, 1, gi, Jof(1), P));
       copy_a(1, Jof(1), wn_next);
@@ -1135,7 +1159,7 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
       const int gv = g + h * P.nreal;
       if (tm) ts[0] = clock64();
       double cval = 0.0;
-      if (outt) cval = __ldcg(P.W1 + widx<KN>(gv, J, ny) + size_t(row) * kG + n);
+      if (outt) cval = __ldcg(((kUpper && P.thomas) ? P.W0 : P.W1) + widx<KN>(gv, J, ny) + size_t(row) * kG + n);
       complete(buf, gv, idx - 1, wn);
       if (tm) ts[1] = ts[2] = clock64();
       // the other half of this row was published a whole product ago: fetch it under this product
@@ -1179,7 +1203,10 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
       __syncthreads();  // As consumed by every warp (last half), red[rb] complete
       // the next row's operator window, as soon as As is free (before this half's stores)
       if (h + 1 == nh && more) copy_a(idx + 1, Jof(idx + 1), wn_next);
-      if (outt) emit(h, idx, J, cval + reduce8(redw, threadIdx.x));
+      if (outt) {
+        const double pv = reduce8(redw, threadIdx.x);
+        emit(h, idx, J, cval + pv, pv, false);
+      }
       rb ^= 1;
       buf ^= 1;
       if (tm) {
@@ -1204,7 +1231,10 @@ template <int KN>
 __global__ void __launch_bounds__(kThr6) v6_mid_kernel(V6Params P, int mode) {
   V6_DIMS
   __shared__ double red[8 * 128];
-  const int s = blockIdx.x % kSl, g = blockIdx.x / kSl;
+  const int s = blockIdx.x % kSl;
+  const int gq = blockIdx.x / kSl;                 // mode 2: a virtual chain group; else a real one
+  const int h2 = (mode == 2 && gq >= P.nreal) ? 1 : 0;
+  const int g = gq - h2 * P.nreal;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bo = (lane & 3) * kG + (lane >> 2);
   const int M = P.ny;  // rows per half chain = the middle block row
@@ -1226,7 +1256,9 @@ __global__ void __launch_bounds__(kThr6) v6_mid_kernel(V6Params P, int mode) {
   if (mode == 0) {
     prod(P.Dm, P.Wm + size_t(g) * vec, nullptr);
     prod(P.Em, P.W0 + widx<KN>(g, M - 1, M), P.W0 + widx<KN>(g + P.nreal, M - 1, M));
-  } else {
+  } else if (mode == 2) {  // Thomas form, after the outward chains: x_0 = H_0 X_0 of this half
+    prod(P.Hp, P.W0 + widx<KN>(gq, 0, M), nullptr);
+  } else if (!P.thomas) {
     prod(P.Hp + size_t(oprow(M - 1, P.jstar)) * kSl * kKS * 64, xm, nullptr);
   }
 #pragma unroll
@@ -1252,6 +1284,24 @@ __global__ void __launch_bounds__(kThr6) v6_mid_kernel(V6Params P, int mode) {
           }
         }
       }
+    } else if (mode == 2) {
+      if (row < P.nx && ch < P.nchains) {
+        const FastStep st = P.jobs[size_t(ch) * P.nsteps + P.t];
+        if (st.in) {
+          const int Ja = h2 ? P.nyA - 1 : 0;
+          if (st.out) st.out[size_t(Ja) * P.nx + row] = v;
+          if (st.out2) {
+            double g2 = 0.0;
+            if (st.node2 > 0 && P.gam) g2 = P.gam[st.node2];
+            st.out2[size_t(Ja) * P.nx + row] = v + g2;
+          }
+        }
+      }
+    } else if (P.thomas) {  // the start of the outward chains: X_{M-1} = y_{M-1} + x_M, both halves
+      const double x = xm[size_t(row) * kG + n];
+      const size_t a = widx<KN>(g, M - 1, M) + size_t(row) * kG + n, b = widx<KN>(g + P.nreal, M - 1, M) + size_t(row) * kG + n;
+      P.W1[a] = P.W0[a] + x;
+      P.W1[b] = P.W0[b] + x;
     } else {
       P.W1[widx<KN>(g, M - 1, M) + size_t(row) * kG + n] += v;
       P.W1[widx<KN>(g + P.nreal, M - 1, M) + size_t(row) * kG + n] += v;
@@ -1464,7 +1514,9 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
       const bool up = dir == 1;
       if (up && P.twist)  // the two eliminations meet: x_M
         KKT_LAUNCH(c, v6_mid_kernel<KN>, kSl * P.nreal, kThr6, 0, P, 0);
-      if (off_plain() || KN == 256) {  // 256-blocks: one small copy per slice, plain loads measured ahead
+      if (P.thomas) {
+        // inverse-block form: no off-chain products (c = b / cy comes from v6_form_b_kernel, d = y)
+      } else if (off_plain() || KN == 256) {  // 256-blocks: one small copy per slice, plain loads measured ahead
         if (up)
           KKT_LAUNCH(c, (v6_off_kernel<KN, true>), og, kThr6, off_smem<KN>(), P);
         else
@@ -1528,6 +1580,10 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
       for (int g0 = 0; g0 < nchain_groups; g0 += gpw) {
         P.g0 = g0;
         launch_chain<KN>(c, up, P, std::min(gpw, nchain_groups - g0));
+      }
+      if (up && P.thomas) {  // x_0 = H_0 X_0 of both halves
+        P.g0 = 0;
+        KKT_LAUNCH(c, v6_mid_kernel<KN>, kSl * ngroups, kThr6, 0, P, 2);
       }
     }
     if (c->step_hook) c->step_hook(t);  // every output of step t is written (stream order)
@@ -1700,11 +1756,13 @@ void build_v6(Ctx* c) {
   }
 
   if (twist) {  // the middle block row: Dm^{-1} and E = cy Dm^{-1} Ui_{M-1}, packed like the operator rows
-    DBuf<double> Dinv(nn), E(nn);
-    build_twist_middle(c, ny, Dinv.p, E.p);
-    c->v6_mid.alloc(2 * mat);
+    DBuf<double> Dinv(nn), E(nn), E2(nn);
+    build_twist_middle(c, ny, Dinv.p, E.p, E2.p);
+    c->v6_mid.alloc(3 * mat);
     pk(Dinv.p, 1, 1.0, c->v6_mid.p);
     pk(E.p, 1, 1.0, c->v6_mid.p + mat);
+    pk(E2.p, 1, 1.0, c->v6_mid.p + 2 * mat);
+    c->v6_thomas = true;
     KKT_CUDA(cudaStreamSynchronize(c->stream));  // the temporaries are freed here
     if (std::getenv("KKT_V6_TIM")) std::fprintf(stderr, "v6 twisted elimination: %d rows per half chain, middle row %d\n", ny, ny);
   }
@@ -1860,6 +1918,16 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   const bool win = !band_off && c->v6_band_on;
   P.bandPhi = win ? c->v6_band.p : nullptr;
   P.bandPsi = win ? c->v6_band.p + size_t(P.k == 1 ? nops : c->v6_nphi) * (kn / 16) : nullptr;
+  {  // the inverse-block form (see V6Params::thomas): H is the only operator set, no off-chain products
+    static const bool th_env = std::getenv("KKT_V6_THOMAS") == nullptr || std::atoi(std::getenv("KKT_V6_THOMAS")) != 0;  // default on; 0: the L/U form
+    P.thomas = (th_env && c->v6_thomas && twist && P.k == 1 && ll_on && ny >= 2) ? 1 : 0;
+    P.inv_cy = 1.0 / c->cy;
+    if (P.thomas) {
+      P.Phi = P.Psi = P.Hp;
+      P.bandPhi = P.bandPsi;
+      P.Em = c->v6_mid.p + 2 * mat;
+    }
+  }
   static const bool dbg = std::getenv("KKT_V6_TIM") != nullptr;
   DBuf<long long> tim;
   P.tim = nullptr;
@@ -1869,6 +1937,7 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
     KKT_CUDA(cudaMemsetAsync(tim.p, 0, sizeof(long long) * 12, c->stream));
     P.tim = tim.p;
   }
+  if (dbg) std::fprintf(stderr, "v6 elimination form: %s\n", P.thomas ? "inverse blocks (no off-chain products)" : "L/U factors");
   c->tbegin(3);
   if (kn == 256)
     run_steps<256>(c, P, nsteps, ngroups);

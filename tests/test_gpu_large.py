@@ -48,3 +48,39 @@ def test_large_grid_ops_against_reference(path):
         assert err <= 1e-10, (blk, err)
         n = np.linalg.norm(Pv[blk * B:(blk + 1) * B])
         assert abs(n - rec["apply_P_inv"]["norms"][blk]) <= 1e-10 * rec["apply_P_inv"]["norms"][blk]
+
+
+@pytest.mark.parametrize("env", [{"KKT_V6_K": "1"}, {"KKT_V6_K": "1", "KKT_V6_THOMAS": "0"}], ids=["inverse_blocks", "lu_factors"])
+def test_large_grid_pinv_row_by_row_forms_against_reference(env, tmp_path):
+    """The records' time axes are short, so the default run above groups the chain's rows (k > 1) and
+    takes the L/U form.  The full-size configs run row by row (k = 1), where the default is the
+    inverse-block form of the two-sided elimination (H_J = cy D_J^-1 as the only operator set, no
+    off-chain products).  Forced here on the same records, both forms, against the reference's
+    P^-1 samples (1e-10 per block).  Subprocess: the switches are read once per process."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import json, sys, numpy as np, torch\n"
+        "from paper_2305_04421_b200 import problems as P\n"
+        "from paper_2305_04421_b200.solver import HeatKKT\n"
+        "for path in sys.argv[1:]:\n"
+        "    rec = json.load(open(path)); samp = np.load(path.replace('.json', '_sample.npz'))\n"
+        "    p = P.config(rec['config']).replace(Nt=rec['problem']['Nt'], Nd=rec['problem']['Nd'])\n"
+        "    v = P.random_kkt(p, 0)\n"
+        "    k = HeatKKT(p, mode='fast'); Pv = k.apply_P_inv(torch.from_numpy(v).cuda()).cpu().numpy()\n"
+        "    del k; torch.cuda.empty_cache()\n"
+        "    B, stride = p.block, rec['stride']; want = samp['apply_P_inv']; got = Pv[::stride]\n"
+        "    idx = np.arange(0, 3 * B, stride); worst = 0.0\n"
+        "    for blk in range(3):\n"
+        "        sel = (idx >= blk * B) & (idx < (blk + 1) * B)\n"
+        "        worst = max(worst, float(np.linalg.norm(got[sel] - want[sel]) / np.linalg.norm(want[sel])))\n"
+        "    print('REL', worst)\n")
+    r = subprocess.run([sys.executable, "-c", code] + RECORDS, env=dict(os.environ, KKT_V6_TIM="1", **env),
+                       capture_output=True, text=True, timeout=1500, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rels = [float(x.split()[1]) for x in r.stdout.splitlines() if x.startswith("REL")]
+    assert len(rels) == len(RECORDS) and max(rels) <= 1e-10, r.stdout
+    forms = [x for x in r.stderr.splitlines() if x.startswith("v6 elimination form")]
+    want = "inverse blocks" if env.get("KKT_V6_THOMAS") != "0" else "L/U factors"
+    assert forms and all(want in x for x in forms), forms[:3]
