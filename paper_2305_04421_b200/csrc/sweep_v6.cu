@@ -616,8 +616,7 @@ __device__ __forceinline__ int grow(bool upper, int gr, int i, int k, int ny) {
 }
 // Packed propagator index of (group gr, row i): see V6Params.
 __device__ __forceinline__ int propidx(bool upper, int gr, int i, int J, const V6Params& P) {
-  if (P.thomas) return oprow(upper ? J + 1 : (J > 0 ? J - 1 : 0), P.jstar);  // H_{J+1} / H_{J-1}
-  if (P.k == 1) return oprow(J, P.jstar);
+  if (P.k == 1) return P.thomas ? oprow(upper ? J + 1 : (J > 0 ? J - 1 : 0), P.jstar) : oprow(J, P.jstar);  // Thomas: H_{J+1} / H_{J-1}
   if (upper) return gr < P.gconv ? i : P.k + (gr - P.gconv) * P.k + i;
   return gr < P.nind ? gr * P.k + i : P.nind * P.k + i;
 }
@@ -645,14 +644,17 @@ __global__ void __launch_bounds__(kThr6, 1) v6_inner_kernel(V6Params P) {
     reinterpret_cast<double2*>(Bs)[i] = v;
   }
   __syncthreads();
-  const bool res = J >= P.jstar;
+  // the row's operator: G_J / H_J, or in the inverse-block form H_{J-1} / H_{J+1} (V6Params::thomas)
+  const int Jop = P.thomas ? Jp : J;
+  const bool useH = kUpper || P.thomas;
+  const bool res = Jop >= P.jstar;
   for (int s = warp; s < kSl; s += 8) {
-    const double* A = (kUpper ? P.Hp : P.Gp) + (size_t(oprow(J, P.jstar)) * kSl + s) * kKS * 64 + lane;
+    const double* A = (useH ? P.Hp : P.Gp) + (size_t(oprow(Jop, P.jstar)) * kSl + s) * kKS * 64 + lane;
     double d[2][2][2] = {};
     double ac[kOffChunk][2], an[kOffChunk][2];
     int ks0 = 0, ks1 = kKS;  // compile-time constants without the band
     if constexpr (kBand) {
-      const int2 b = (kUpper ? P.rawH : P.rawG)[size_t(oprow(J, P.jstar)) * kSl + s];
+      const int2 b = (useH ? P.rawH : P.rawG)[size_t(oprow(Jop, P.jstar)) * kSl + s];
       ks0 = b.x;
       ks1 = b.y;
     }
@@ -786,10 +788,15 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
     const int gv = g + h * P.nreal;
     if (kLL && last_row)
       st_slot(P.ll + (size_t(gv) * P.ngr + gr) * (KN * kG) + size_t(row) * kG + n, v);
-    P.W0[widx<KN>(gv, J, ny) + size_t(row) * kG + n] = v;
-    if (P.thomas && start) return;
+    (void)start;
+    double* w0 = P.W0 + widx<KN>(gv, J, ny) + size_t(row) * kG + n;
+    // Thomas form, U, grouped rows: the chain value is X_J = y_J + x_{J+1} and y_J is still in W0
+    double yv = 0.0;
+    if (kUpper && P.thomas && P.k > 1 && (out || out2)) yv = __ldcg(w0);
+    *w0 = v;
+    if (kUpper && P.thomas && J == ny - 1) return;  // X_{M-1} = y_{M-1} + x_M: the start row has no output
     const int Jo = P.thomas ? J + 1 : J;
-    const double ov = P.thomas ? pv : v;
+    const double ov = P.thomas ? (P.k == 1 ? pv : v - yv) : v;
     const int Ja = h ? P.nyA - 1 - Jo : Jo;  // the block row of the grid (bottom half: mirrored)
     if (out) out[size_t(Ja) * P.nx + row] = ov;
     if (out2) out2[size_t(Ja) * P.nx + row] = ov + g2;
@@ -847,7 +854,7 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
       const int gv = g + h * P.nreal;
       if (tm) ts[0] = clock64();
       double cval = 0.0;
-      if (outt) cval = __ldcg(((kUpper && P.thomas) ? P.W0 : P.W1) + widx<KN>(gv, J, ny) + size_t(row) * kG + n);
+      if (outt) cval = __ldcg(((kUpper && P.thomas && P.k == 1) ? P.W0 : P.W1) + widx<KN>(gv, J, ny) + size_t(row) * kG + n);
       if (!kLL) {
         if (threadIdx.x == 0) {
           const unsigned target = unsigned(idx) * kSl * 4;
@@ -1040,10 +1047,15 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
   auto emit = [&](int h, int gr, int J, double v, double pv, bool start) {  // as in v6_chain_kernel
     const int gv = g + h * P.nreal;
     if (last_row) st_slot(P.ll + (size_t(gv) * P.ngr + gr) * (KN * kG) + size_t(row) * kG + n, v);
-    P.W0[widx<KN>(gv, J, ny) + size_t(row) * kG + n] = v;
-    if (P.thomas && start) return;
+    (void)start;
+    double* w0 = P.W0 + widx<KN>(gv, J, ny) + size_t(row) * kG + n;
+    // Thomas form, U, grouped rows: the chain value is X_J = y_J + x_{J+1} and y_J is still in W0
+    double yv = 0.0;
+    if (kUpper && P.thomas && P.k > 1 && (out || out2)) yv = __ldcg(w0);
+    *w0 = v;
+    if (kUpper && P.thomas && J == ny - 1) return;  // X_{M-1} = y_{M-1} + x_M: the start row has no output
     const int Jo = P.thomas ? J + 1 : J;
-    const double ov = P.thomas ? pv : v;
+    const double ov = P.thomas ? (P.k == 1 ? pv : v - yv) : v;
     const int Ja = h ? P.nyA - 1 - Jo : Jo;
     if (out) out[size_t(Ja) * P.nx + row] = ov;
     if (out2) out2[size_t(Ja) * P.nx + row] = ov + g2;
@@ -1159,7 +1171,7 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
       const int gv = g + h * P.nreal;
       if (tm) ts[0] = clock64();
       double cval = 0.0;
-      if (outt) cval = __ldcg(((kUpper && P.thomas) ? P.W0 : P.W1) + widx<KN>(gv, J, ny) + size_t(row) * kG + n);
+      if (outt) cval = __ldcg(((kUpper && P.thomas && P.k == 1) ? P.W0 : P.W1) + widx<KN>(gv, J, ny) + size_t(row) * kG + n);
       complete(buf, gv, idx - 1, wn);
       if (tm) ts[1] = ts[2] = clock64();
       // the other half of this row was published a whole product ago: fetch it under this product
@@ -1393,6 +1405,10 @@ __global__ void v6_pack_kernel(const double* __restrict__ src, int nx, int nJ, d
   }
 }
 
+__global__ void v6_copy_kernel(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) b[e] = a[e];
+}
+
 __global__ void v6_scale_kernel(int64_t n, double f, double* __restrict__ a) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) a[e] *= f;
 }
@@ -1558,6 +1574,10 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
         }
         }
       }
+      if (up && P.thomas && P.k > 1) {  // grouped rows: the in-group passes run in place in W1, so d = y goes there
+        const int64_t tot = int64_t(ngroups) * P.ny * KN * kG;
+        KKT_LAUNCH(c, v6_copy_kernel, kSmCount * 8, 256, 0, tot, P.W0, P.W1);
+      }
       if (up && P.twist)  // the inflow of the first outward row: d_{M-1} += H_{M-1} x_M
         KKT_LAUNCH(c, v6_mid_kernel<KN>, kSl * P.nreal, kThr6, 0, P, 1);
       for (int i = 1; i < P.k; ++i) {  // zero-inflow chains inside the groups, every group at once
@@ -1566,7 +1586,7 @@ void run_steps(Ctx* c, V6Params& P, int nsteps, int ngroups) {
           KKT_LAUNCH(c, (v6_inner_kernel<KN, true, true>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
         else if (up)
           KKT_LAUNCH(c, (v6_inner_kernel<KN, true, false>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
-        else if (P.rawG)
+        else if (P.thomas ? P.rawH != nullptr : P.rawG != nullptr)
           KKT_LAUNCH(c, (v6_inner_kernel<KN, false, true>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
         else
           KKT_LAUNCH(c, (v6_inner_kernel<KN, false, false>), P.ngr * npairs, kThr6, off_smem<KN>(), P);
@@ -1762,7 +1782,9 @@ void build_v6(Ctx* c) {
     pk(Dinv.p, 1, 1.0, c->v6_mid.p);
     pk(E.p, 1, 1.0, c->v6_mid.p + mat);
     pk(E2.p, 1, 1.0, c->v6_mid.p + 2 * mat);
-    c->v6_thomas = true;
+    // the inverse-block form (V6Params::thomas) is the default with the twisted elimination; KKT_V6_THOMAS=0: L/U factors
+    static const bool th_env = std::getenv("KKT_V6_THOMAS") == nullptr || std::atoi(std::getenv("KKT_V6_THOMAS")) != 0;
+    c->v6_thomas = th_env;
     KKT_CUDA(cudaStreamSynchronize(c->stream));  // the temporaries are freed here
     if (std::getenv("KKT_V6_TIM")) std::fprintf(stderr, "v6 twisted elimination: %d rows per half chain, middle row %d\n", ny, ny);
   }
@@ -1780,7 +1802,8 @@ void build_v6(Ctx* c) {
   const int ngr = (ny + k - 1) / k;
   // L groups [0, nind) are built row by row, groups >= nind (all rows >= js) share one converged set;
   // U groups (from the top) [0, gconv) share the converged set, the rest are built row by row
-  const int nind = js >= ny ? ngr : std::min(ngr, (js + k - 1) / k);
+  const int jsl = c->v6_thomas ? js + 1 : js;  // inverse-block form: L row J applies H_{J-1}, converged from row js + 1 on
+  const int nind = jsl >= ny ? ngr : std::min(ngr, (jsl + k - 1) / k);
   const int gconv = js >= ny ? 0 : std::min(ngr, (ny - js) / k);
   c->v6_nind = nind;
   c->v6_gconv = gconv;
@@ -1805,11 +1828,13 @@ void build_v6(Ctx* c) {
     KKT_LAUNCH(c, v6_scale_kernel, kSmCount * 8, 256, 0, tot, c->cy, Hu.p);
   }
   // one group's propagators: P_0 = M_{J(0)}, P_i = M_{J(i)} P_{i-1}; packed to dst[i]
-  auto build_group = [&](const double* Mu, auto rowof, double* dst) {
+  // Inverse-block form: row J's operator is H_{J-1} (L) / H_{J+1} (U) instead of G_J / H_J
+  const bool th = c->v6_thomas;
+  auto build_group = [&](const double* Mu, auto rowof, double* dst, int shift) {
     for (int i = 0; i < k; ++i) {
       const int J = rowof(i);
       if (J < 0 || J >= ny) break;
-      const double* M = Mu + size_t(opr(J)) * nn;
+      const double* M = Mu + size_t(opr(std::max(0, J + shift))) * nn;
       if (i == 0) {
         KKT_CUDA(cudaMemcpyAsync(Pu.p, M, sizeof(double) * nn, cudaMemcpyDeviceToDevice, c->stream));
       } else {
@@ -1819,12 +1844,14 @@ void build_v6(Ctx* c) {
       pk(Pu.p + size_t(i) * nn, 1, 1.0, dst + size_t(i) * mat);
     }
   };
+  const double* GL = th ? Hu.p : Gu.p;
+  const int sl = th ? -1 : 0, su = th ? 1 : 0;
   for (int gr = 1; gr < nind; ++gr)  // group 0 has no inflow
-    build_group(Gu.p, [&](int i) { return gr * k + i; }, Phi + size_t(gr) * k * mat);
-  if (nind < ngr) build_group(Gu.p, [&](int i) { (void)i; return js; }, Phi + size_t(nind) * k * mat);
-  if (gconv > 0) build_group(Hu.p, [&](int i) { (void)i; return js; }, Psi);
+    build_group(GL, [&](int i) { return gr * k + i; }, Phi + size_t(gr) * k * mat, sl);
+  if (nind < ngr) build_group(GL, [&](int i) { (void)i; return jsl; }, Phi + size_t(nind) * k * mat, sl);
+  if (gconv > 0) build_group(Hu.p, [&](int i) { (void)i; return js; }, Psi, 0);
   for (int gr = std::max(1, gconv); gr < ngr; ++gr)
-    build_group(Hu.p, [&](int i) { return ny - 1 - gr * k - i; }, Psi + size_t(k + (gr - gconv) * k) * mat);
+    build_group(Hu.p, [&](int i) { return ny - 1 - gr * k - i; }, Psi + size_t(k + (gr - gconv) * k) * mat, su);
   c->v6_band.alloc(size_t(c->v6_nphi + c->v6_npsi) * ksl);  // k > 1: the windows of the propagator sets
   make_band(Phi, c->v6_nphi, c->v6_band.p, nullptr);
   make_band(Psi, c->v6_npsi, c->v6_band.p + size_t(c->v6_nphi) * ksl, nullptr);
@@ -1920,11 +1947,14 @@ void v6_chains(Ctx* c, const FastStep* jobs_dev, int nchains, int nsteps, bool c
   P.bandPsi = win ? c->v6_band.p + size_t(P.k == 1 ? nops : c->v6_nphi) * (kn / 16) : nullptr;
   {  // the inverse-block form (see V6Params::thomas): H is the only operator set, no off-chain products
     static const bool th_env = std::getenv("KKT_V6_THOMAS") == nullptr || std::atoi(std::getenv("KKT_V6_THOMAS")) != 0;  // default on; 0: the L/U form
-    P.thomas = (th_env && c->v6_thomas && twist && P.k == 1 && ll_on && ny >= 2) ? 1 : 0;
+    (void)th_env;
+    P.thomas = (c->v6_thomas && twist && ll_on) ? 1 : 0;  // decided at setup (build_v6): the grouped propagators follow it
     P.inv_cy = 1.0 / c->cy;
     if (P.thomas) {
-      P.Phi = P.Psi = P.Hp;
-      P.bandPhi = P.bandPsi;
+      if (P.k == 1) {
+        P.Phi = P.Psi = P.Hp;
+        P.bandPhi = P.bandPsi;
+      }
       P.Em = c->v6_mid.p + 2 * mat;
     }
   }

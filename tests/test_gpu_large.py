@@ -50,13 +50,15 @@ def test_large_grid_ops_against_reference(path):
         assert abs(n - rec["apply_P_inv"]["norms"][blk]) <= 1e-10 * rec["apply_P_inv"]["norms"][blk]
 
 
-@pytest.mark.parametrize("env", [{"KKT_V6_K": "1"}, {"KKT_V6_K": "1", "KKT_V6_THOMAS": "0"}], ids=["inverse_blocks", "lu_factors"])
+@pytest.mark.parametrize("env", [{"KKT_V6_K": "1"}, {"KKT_V6_K": "1", "KKT_V6_THOMAS": "0"}, {"KKT_V6_THOMAS": "0"}],
+                         ids=["inverse_blocks", "lu_factors", "lu_factors_grouped"])
 def test_large_grid_pinv_row_by_row_forms_against_reference(env, tmp_path):
-    """The records' time axes are short, so the default run above groups the chain's rows (k > 1) and
-    takes the L/U form.  The full-size configs run row by row (k = 1), where the default is the
-    inverse-block form of the two-sided elimination (H_J = cy D_J^-1 as the only operator set, no
-    off-chain products).  Forced here on the same records, both forms, against the reference's
-    P^-1 samples (1e-10 per block).  Subprocess: the switches are read once per process."""
+    """The records' time axes are short, so the default run above groups the chain's rows (k > 1);
+    config 2 and the config-4 slab at full size run row by row (k = 1).  Forced here on the same
+    records: row by row in the inverse-block form of the two-sided elimination (the default:
+    H_J = cy D_J^-1 as the only operator set, no off-chain products) and in the L/U form, and the
+    grouped L/U form, against the reference's P^-1 samples (1e-10 per block).  Subprocess: the
+    switches are read once per process."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

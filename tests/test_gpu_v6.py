@@ -205,8 +205,11 @@ def test_block_lu_grid_kernel_bitwise(tmp_path):
 
 @pytest.mark.parametrize("env", [{"KKT_V6_K": "1"}, {"KKT_V6_K": "3"}, {"KKT_V6_K": "8"},
                                  {"KKT_V6_K": "5", "KKT_V6_LL": "0"}, {"KKT_V6_LL": "0"}, {"KKT_V6_OFF_NG2": "1"},
-                                 {"KKT_V6_OFF3": "0"}, {"KKT_V6_OFF3": "0", "KKT_V6_OFF_NG2": "1"}, {"KKT_V6_STAGGER": "1500"}],
-                         ids=["k1", "k3", "k8", "k5_counter", "counter", "off_ng2", "off2", "off2_ng2", "stagger"])
+                                 {"KKT_V6_OFF3": "0", "KKT_V6_THOMAS": "0"}, {"KKT_V6_OFF3": "0", "KKT_V6_OFF_NG2": "1", "KKT_V6_THOMAS": "0"},
+                                 {"KKT_V6_STAGGER": "1500"}, {"KKT_V6_K": "1", "KKT_V6_THOMAS": "0"},
+                                 {"KKT_V6_K": "3", "KKT_V6_THOMAS": "0"}, {"KKT_V6_OFF_NG2": "1", "KKT_V6_THOMAS": "0"}],
+                         ids=["k1", "k3", "k8", "k5_counter", "counter", "off_ng2", "off2", "off2_ng2", "stagger", "k1_lu", "k3_lu",
+                              "off3_ng2_lu"])
 def test_v6_grouping_and_handoff_variants_against_strict(env):
     """The chain's k-row grouping (propagator products over groups of k block rows, zero-inflow
     chains inside the groups) and its two row handoffs (low-latency packets / release counter) are

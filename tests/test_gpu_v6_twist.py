@@ -82,8 +82,11 @@ def test_twisted_window_and_band_solves(Nx, Ny):
 
 @pytest.mark.parametrize("env", [{"KKT_V6_TWIST": "0"}, {"KKT_V6_K": "1"}, {"KKT_V6_K": "4"}, {"KKT_V6_K": "7"},
                                  {"KKT_V6_NOBAND": "1"}, {"KKT_V6_LL": "0"}, {"KKT_V6_K": "1", "KKT_V6_THOMAS": "0"},
-                                 {"KKT_V6_K": "1", "KKT_V6_NOBAND": "1"}, {"KKT_V6_K": "1", "KKT_V6_NOHOLD": "1"}],
-                         ids=["one_sided", "k1", "k4", "k7", "noband", "counter", "k1_lu_form", "k1_noband", "k1_nohold"])
+                                 {"KKT_V6_K": "1", "KKT_V6_NOBAND": "1"}, {"KKT_V6_K": "1", "KKT_V6_NOHOLD": "1"},
+                                 {"KKT_V6_K": "4", "KKT_V6_THOMAS": "0"}, {"KKT_V6_K": "7", "KKT_V6_THOMAS": "0"},
+                                 {"KKT_V6_THOMAS": "0"}],
+                         ids=["one_sided", "k1", "k4", "k7", "noband", "counter", "k1_lu_form", "k1_noband", "k1_nohold",
+                              "k4_lu_form", "k7_lu_form", "lu_form"])
 def test_twisted_variants_against_strict(env):
     """The twisted elimination combined with the chain's other re-associations (row grouping k,
     full rows instead of the numerical band), the one-sided elimination (KKT_V6_TWIST=0) and the
@@ -110,10 +113,10 @@ def test_twisted_variants_against_strict(env):
         assert float(row[1]) <= 1e-10 and row[3] == "True", (env, rows)
     twisted = "v6 twisted elimination" in r.stderr
     assert twisted == (env.get("KKT_V6_TWIST") != "0" and env.get("KKT_V6_LL") != "0"), r.stderr[-1500:]
-    # row by row (k = 1) the twisted elimination takes the inverse-block form (no off-chain products)
-    # unless KKT_V6_THOMAS=0 asks for the L/U factors
+    # the twisted elimination takes the inverse-block form (no off-chain products), row by row or
+    # grouped, unless KKT_V6_THOMAS=0 asks for the L/U factors
     inverse = any("v6 elimination form: inverse blocks" in x for x in r.stderr.splitlines())
-    assert inverse == (twisted and env.get("KKT_V6_K") == "1" and env.get("KKT_V6_THOMAS") != "0"), r.stderr[-1500:]
+    assert inverse == (twisted and env.get("KKT_V6_THOMAS") != "0"), r.stderr[-1500:]
 
 
 def test_twisted_full_solve_against_one_sided(tmp_path):
