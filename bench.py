@@ -681,9 +681,9 @@ def pinv_rooflines(p, ws, ms_apply, sw_ms, napplies):
         "kernel": ("RASQ sweep v4 (sweep_v4.cu): group-parallel block-LU substitution chains, 8-CTA clusters, fp64 DMMA"
                    if v4 else
                    "RASQ sweep v6 (sweep_v6.cu): v6_chain(w)_kernel (device-wide dependent block-row chain of the two-sided "
-                   "block elimination, groups of k rows, fp64 DMMA over the operators' numerical band, prefetched slot handoff) "
-                   "+ v6_off(2|3)_kernel (batched triangular products) + v6_mid_kernel (the middle row) + v6_inner_kernel "
-                   "(zero-inflow chains inside the groups) + v6_form_b_kernel, all local subdomains in lock step"),
+                   "block elimination in its inverse-block form, groups of k rows, fp64 DMMA over the operators' numerical "
+                   "band, prefetched slot handoff) + v6_mid_kernel (the middle row, the first row) + v6_inner_kernel "
+                   "(zero-inflow chains inside the groups, k > 1) + v6_form_b_kernel, all local subdomains in lock step"),
         "bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": (gbs / peak) if gbs else None,
         "traffic": ncu_summary("sweep_dram_bytes_per_apply" if v4 else f"sweep_v6_nx{p.nx_int}_dram_bytes_per_apply"),
         "peak_source": peak_src, "algorithmic_bytes_per_launch": sb, "avg_launch_ms": sw_ms, "launches": napplies,
