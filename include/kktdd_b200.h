@@ -160,7 +160,10 @@ int kkt_band_solve_transpose(kkt_ctx* ctx, double* b, int32_t nrhs);
 int kkt_apply_K(kkt_ctx* ctx, const double* v, double* out);      /* kkt.cpp:50-65 */
 int kkt_apply_P_inv(kkt_ctx* ctx, const double* r, double* out);  /* kkt.cpp:71-81 */
 /* apply_P_inv end to end from HOST buffers (pageable or pinned): copies r in, applies, copies
- * the result out; returns when out_host is complete. */
+ * the result out; returns when out_host is complete.  The copies overlap the compute (the w block
+ * goes up first and the sweep starts; the u and z blocks follow in chunks that are divided and
+ * sent back as they land; with pinned buffers the w planes go back behind the adjoint sweep);
+ * the result is bitwise that of kkt_apply_P_inv. */
 int kkt_apply_P_inv_host(kkt_ctx* ctx, const double* r_host, double* out_host);
 /* ||rhs - K v|| / ||rhs|| (kkt.cpp:110-124). */
 int kkt_residual(kkt_ctx* ctx, const double* v, const double* rhs, double* relres);
