@@ -784,16 +784,13 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
   auto Jof = [&](int gr) { return grow(kUpper, gr, gi, P.k, ny); };  // this CTA's row of group gr
   // v: the chain value of row J (slot, W0); pv: the product alone.  Thomas form, U: the product is
   // x_{J+1} (the start row has none)
-  auto emit = [&](int h, int gr, int J, double v, double pv, bool start) {
+  auto emit = [&](int h, int gr, int J, double v, double pv, double yv) {
     const int gv = g + h * P.nreal;
     if (kLL && last_row)
       st_slot(P.ll + (size_t(gv) * P.ngr + gr) * (KN * kG) + size_t(row) * kG + n, v);
-    (void)start;
-    double* w0 = P.W0 + widx<KN>(gv, J, ny) + size_t(row) * kG + n;
-    // Thomas form, U, grouped rows: the chain value is X_J = y_J + x_{J+1} and y_J is still in W0
-    double yv = 0.0;
-    if (kUpper && P.thomas && P.k > 1 && (out || out2)) yv = __ldcg(w0);
-    *w0 = v;
+    // Thomas form, U, grouped rows: the chain value is X_J = y_J + x_{J+1}; yv = y_J was read from W0
+    // (this same element) before this store, at the start of the product
+    P.W0[widx<KN>(gv, J, ny) + size_t(row) * kG + n] = v;
     if (kUpper && P.thomas && J == ny - 1) return;  // X_{M-1} = y_{M-1} + x_M: the start row has no output
     const int Jo = P.thomas ? J + 1 : J;
     const double ov = P.thomas ? (P.k == 1 ? pv : v - yv) : v;
@@ -830,8 +827,11 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
     const int J = Jof(0);
     if (J < 0) return;
     if (outt)
-      for (int h = 0; h < nh; ++h)
-        emit(h, 0, J, __ldcg(P.W1 + widx<KN>(g + h * P.nreal, J, ny) + size_t(row) * kG + n), 0.0, true);
+      for (int h = 0; h < nh; ++h) {
+        const size_t e = widx<KN>(g + h * P.nreal, J, ny) + size_t(row) * kG + n;
+        const double y0 = (kUpper && P.thomas && P.k > 1) ? __ldcg(P.W0 + e) : 0.0;
+        emit(h, 0, J, __ldcg(P.W1 + e), 0.0, y0);
+      }
     signal();
     if (P.ngr > 1 && Jof(1) >= 0) {
       wn_next = window(propidx(kUpper, 1, gi, Jof(1), P));
@@ -854,7 +854,12 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
       const int gv = g + h * P.nreal;
       if (tm) ts[0] = clock64();
       double cval = 0.0;
-      if (outt) cval = __ldcg(((kUpper && P.thomas && P.k == 1) ? P.W0 : P.W1) + widx<KN>(gv, J, ny) + size_t(row) * kG + n);
+      double yv = 0.0;  // Thomas form, U, grouped rows: y_J, still in W0 until this row's emit overwrites it
+      if (outt) {
+        const size_t e = widx<KN>(gv, J, ny) + size_t(row) * kG + n;
+        cval = __ldcg(((kUpper && P.thomas && P.k == 1) ? P.W0 : P.W1) + e);
+        if (kUpper && P.thomas && P.k > 1) yv = __ldcg(P.W0 + e);
+      }
       if (!kLL) {
         if (threadIdx.x == 0) {
           const unsigned target = unsigned(idx) * kSl * 4;
@@ -980,7 +985,7 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chain_kernel
       __syncthreads();
       if (outt) {
         const double pv = reduce8(redw, threadIdx.x);
-        emit(h, idx, J, cval + pv, pv, false);
+        emit(h, idx, J, cval + pv, pv, yv);
       }
       rb ^= 1;
       if (tm) {
@@ -1044,15 +1049,12 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
     }
   }
   auto Jof = [&](int gr) { return grow(kUpper, gr, gi, P.k, ny); };
-  auto emit = [&](int h, int gr, int J, double v, double pv, bool start) {  // as in v6_chain_kernel
+  auto emit = [&](int h, int gr, int J, double v, double pv, double yv) {  // as in v6_chain_kernel
     const int gv = g + h * P.nreal;
     if (last_row) st_slot(P.ll + (size_t(gv) * P.ngr + gr) * (KN * kG) + size_t(row) * kG + n, v);
-    (void)start;
-    double* w0 = P.W0 + widx<KN>(gv, J, ny) + size_t(row) * kG + n;
-    // Thomas form, U, grouped rows: the chain value is X_J = y_J + x_{J+1} and y_J is still in W0
-    double yv = 0.0;
-    if (kUpper && P.thomas && P.k > 1 && (out || out2)) yv = __ldcg(w0);
-    *w0 = v;
+    // Thomas form, U, grouped rows: the chain value is X_J = y_J + x_{J+1}; yv = y_J was read from W0
+    // (this same element) before this store, at the start of the product
+    P.W0[widx<KN>(gv, J, ny) + size_t(row) * kG + n] = v;
     if (kUpper && P.thomas && J == ny - 1) return;  // X_{M-1} = y_{M-1} + x_M: the start row has no output
     const int Jo = P.thomas ? J + 1 : J;
     const double ov = P.thomas ? (P.k == 1 ? pv : v - yv) : v;
@@ -1149,8 +1151,11 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
     const int J = Jof(0);
     if (J < 0) return;
     if (outt)
-      for (int h = 0; h < nh; ++h)
-        emit(h, 0, J, __ldcg(P.W1 + widx<KN>(g + h * P.nreal, J, ny) + size_t(row) * kG + n), 0.0, true);
+      for (int h = 0; h < nh; ++h) {
+        const size_t e = widx<KN>(g + h * P.nreal, J, ny) + size_t(row) * kG + n;
+        const double y0 = (kUpper && P.thomas && P.k > 1) ? __ldcg(P.W0 + e) : 0.0;
+        emit(h, 0, J, __ldcg(P.W1 + e), 0.0, y0);
+      }
     if (P.ngr > 1 && Jof(1) >= 0) {
       wn_next = window(propidx(kUpper, 1, gi, Jof(1), P));
       copy_a(1, Jof(1), wn_next);
@@ -1171,7 +1176,12 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
       const int gv = g + h * P.nreal;
       if (tm) ts[0] = clock64();
       double cval = 0.0;
-      if (outt) cval = __ldcg(((kUpper && P.thomas && P.k == 1) ? P.W0 : P.W1) + widx<KN>(gv, J, ny) + size_t(row) * kG + n);
+      double yv = 0.0;  // Thomas form, U, grouped rows: y_J, still in W0 until this row's emit overwrites it
+      if (outt) {
+        const size_t e = widx<KN>(gv, J, ny) + size_t(row) * kG + n;
+        cval = __ldcg(((kUpper && P.thomas && P.k == 1) ? P.W0 : P.W1) + e);
+        if (kUpper && P.thomas && P.k > 1) yv = __ldcg(P.W0 + e);
+      }
       complete(buf, gv, idx - 1, wn);
       if (tm) ts[1] = ts[2] = clock64();
       // the other half of this row was published a whole product ago: fetch it under this product
@@ -1217,7 +1227,7 @@ __global__ void __launch_bounds__(kThr6, chain_min_blocks<KN>()) v6_chainw_kerne
       if (h + 1 == nh && more) copy_a(idx + 1, Jof(idx + 1), wn_next);
       if (outt) {
         const double pv = reduce8(redw, threadIdx.x);
-        emit(h, idx, J, cval + pv, pv, false);
+        emit(h, idx, J, cval + pv, pv, yv);
       }
       rb ^= 1;
       buf ^= 1;
